@@ -1,0 +1,356 @@
+"""Throughput benchmark of the B200 VP-FV RK4 step (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload landau2d-128]
+
+Metric (BASELINE.json): phase-space cell-updates per second per RK4 step
+(sum over species of interior cells / wall time of one RK4 step; a step is 4
+fused stages + moments + rho + Poisson + tables, the per-step non-finite check
+included).  Default workload: 2D-2V Landau damping 128^2 x 128^2, fp64
+(config 4), fixed dt = 0.9 * max_dt at t = 0.  Inputs
+(2.58 GB per buffer) are far larger than L2, so no flush is needed.
+
+Multi-GPU (torchrun, one rank per GPU): the same global problem is split
+along x across ranks (strong scaling) by paper_2410_12155_b200.parallel.
+
+``--impl reference`` times the reference algorithm on the host cores: the
+threaded C restatement of the reference kernels in oracle/ (bitwise equal to
+the reference numba kernels; the reference itself is pure Python and absent
+on the GPU box), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (config description, builder args)
+    "landau2d-128": "2D2V Landau damping 128^2 x 128^2, single electron species (BASELINE config 4)",
+    "landau2d-64": "2D2V Landau damping 64^2 x 64^2 (reduced, for quick runs)",
+    "twostream-1024": "1D1V two-stream 1024 x 1024 (BASELINE config 2)",
+    "weibel-256": "1D2V bi-Maxwellian 256^3 (BASELINE config 3)",
+    "ep2d2v-64": "2D2V electron-proton m_r=1836, 64^4 per species (BASELINE config 5, per GPU)",
+}
+
+STAGE_BYTES = (16, 24, 24, 32)  # algorithmic bytes/cell of RK stages 1..4
+
+
+def make_setup(name):
+    from paper_2410_12155_b200 import problems as P
+
+    if name == "landau2d-128":
+        return P.make_problem(P.landau_spec(), 128, 128)
+    if name == "landau2d-64":
+        return P.make_problem(P.landau_spec(), 64, 64)
+    if name == "twostream-1024":
+        return P.make_problem(P.ProblemSpec("two-stream"), 1024, 1024)
+    if name == "weibel-256":
+        return P.make_bimaxwellian_1d2v(256, 256, 256)
+    if name == "ep2d2v-64":
+        return P.make_electron_proton_2d2v(64, 64)
+    raise ValueError(name)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except (OSError, ValueError):
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = set()
+        for _, _, bits in self.samples:
+            for b, n in REASON_BITS.items():
+                if bits & b and n != "gpu_idle":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the threaded C restatement of the reference (oracle/)
+
+
+def cpu_reference_steps(setup, dt, steps, budget_s=60.0):
+    """Time RK4 steps of the oracle's C restatement; returns (cells/s, info)."""
+    from oracle import cbackend as C
+
+    grids = [f.grid for f in setup.dists]
+    sim = C.CSimulation(grids, setup.species, [np.array(f.data) for f in setup.dists], dt=dt)
+    cells = sum(int(np.prod(g.N)) for g in grids)
+    t0 = time.perf_counter()
+    sim.advance(dt)  # first step also warms the C library / page-faults the buffers
+    first = time.perf_counter() - t0
+    n = max(1, min(steps, int(budget_s / max(first, 1e-9))))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        sim.advance(dt)
+    el = time.perf_counter() - t0
+    return cells * n / el, dict(steps=n, seconds=el, cores=C.num_threads())
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def run_b200(args, rank, world, device):
+    import torch
+
+    from paper_2410_12155_b200 import runner as R
+    from paper_2410_12155_b200.kernels import stream_handle  # noqa: F401
+
+    setup = make_setup(args.workload)
+    if world > 1:
+        from paper_2410_12155_b200.parallel import DistributedSimulation
+
+        sim = DistributedSimulation(setup, dt=None, device=device)
+        dt = 0.9 * sim.max_dt()
+        sim.fixed_dt = dt
+    else:
+        sim = R.Simulation(setup, device=device)
+        dt = 0.9 * sim.max_dt()
+        sim.fixed_dt = dt
+    cells_global = sum(int(np.prod(f.grid.N)) for f in setup.dists)
+    cells_local = sim.local_cells() if hasattr(sim, "local_cells") else cells_global
+    stream = torch.cuda.current_stream(device)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(device)
+
+    sim.enable_stage_timing(True)  # timed graph variant is captured during warm-up
+    for _ in range(args.warmup):
+        sim.advance(dt)
+    sim.enable_stage_timing(True)  # reset the accumulators
+    barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            sim.advance(dt)
+        stop.record(stream)
+        barrier()
+    ms_local = start.elapsed_time(stop)
+    stage_ms = sim.stage_kernel_ms()  # per RK stage slot, summed over timed steps and species
+    sim.enable_stage_timing(False)
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = cells_global * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the fused stage), from in-graph events
+    stage_bytes = sum(b * cells_local for b in STAGE_BYTES) * args.steps
+    stage_s = sum(stage_ms) / 1e3
+    peak, peak_kind = load_peaks()
+    achieved = stage_bytes / stage_s / 1e9 if stage_s > 0 else None
+    share = stage_s / (ms_local / 1e3)
+
+    # end to end through the public API with host buffers:
+    # H2D of the step's input state from pinned memory, step, D2H of the result
+    e2e = None
+    if rank == 0 and world == 1 and args.e2e_steps > 0:
+        e2e = e2e_measure(sim, dt, args.e2e_steps, device, cells_global)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference_steps(make_setup(args.workload), dt, 2, budget_s=args.cpu_budget)
+        cpu = {"value": v, "unit": "cell-updates/s", "cores": info["cores"], "kind": "port",
+               "sample": f"{info['steps']} full RK4 step(s) of the same {args.workload} problem "
+                         f"({info['seconds']:.1f} s), threaded C restatement of the reference kernels "
+                         f"(oracle/stage_ref.c, bitwise = reference numba) + numpy FFT"}
+    launches = sim.launches_per_step() * args.steps
+    line = {
+        "metric": "phase-space cell-updates/sec per RK4 step",
+        "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
+                   "cells": cells_global, "dt": dt, "l2": "inputs larger than L2 (2.58 GB/buffer)",
+                   "parallelism": f"x-slab x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "kernel": "vpfv stage_2d2v (fused RHS + RK4 update)",
+                     "algorithmic_bytes_per_cell_per_step": sum(STAGE_BYTES),
+                     "stage_ms_per_step": [m / args.steps for m in stage_ms],
+                     "share_of_step": share, "peak_kind": peak_kind},
+        "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
+                          "frac": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9 / peak},
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    return line
+
+
+def e2e_measure(sim, dt, steps, device, cells):
+    import torch
+
+    stream = torch.cuda.current_stream(device)
+    host_in = [a.detach().cpu().pin_memory() for a in sim.ctx.f0]
+    host_out = [torch.empty_like(h).pin_memory() for h in host_in]
+    nbytes = sum(h.numel() * h.element_size() for h in host_in)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for d, h in zip(sim.ctx.f0, host_in):
+            d.copy_(h, non_blocking=True)
+        sim.advance(dt)
+        for h, d in zip(host_out, sim.ctx.f0):
+            h.copy_(d, non_blocking=True)
+        stream.synchronize()
+    el = time.perf_counter() - t0
+    return {"value": cells * steps / el, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes,
+            "how": "per step: H2D of the state f0 from pinned host memory, Simulation.advance "
+                   "(graph-replayed RK4 step + non-finite check), D2H of the new state"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+
+def run_reference(args):
+    setup = make_setup(args.workload)
+    from paper_2410_12155_b200.fvm import max_speed_per_dim
+    from oracle import vpfv_oracle as O
+    from oracle import cbackend as C
+
+    grids = [f.grid for f in setup.dists]
+    sim0 = C.CSimulation(grids, setup.species, [np.array(f.data) for f in setup.dists])
+    dt = 0.9 * sim0.max_dt()
+    del sim0
+    cells = sum(int(np.prod(g.N)) for g in grids)
+    sim = C.CSimulation(grids, setup.species, [np.array(f.data) for f in setup.dists], dt=dt)
+    for _ in range(min(args.warmup, 1)):
+        sim.advance(dt)
+    budget = args.cpu_budget * 2
+    t0 = time.perf_counter()
+    n = 0
+    while n < args.steps:
+        sim.advance(dt)
+        n += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    el = time.perf_counter() - t0
+    value = cells * n / el
+    _ = (max_speed_per_dim, O)
+    sample = (f"{n} of {args.steps} requested RK4 steps of the full {args.workload} problem "
+              f"(time-capped at {budget:.0f} s), warmup {min(args.warmup, 1)}")
+    return {
+        "impl": "reference", "metric": "phase-space cell-updates/sec per RK4 step", "value": value,
+        "unit": "cell-updates/s", "n_gpus": 0, "steps": n, "warmup": min(args.warmup, 1),
+        "ms_per_step": el / n * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload], "cells": cells,
+                   "dt": dt},
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": C.num_threads(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="landau2d-128", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=device)
+    line = run_b200(args, rank, world, device)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/* vpfv.h -- C ABI of the B200-native VP-FV stage library (libvpfv.so, sm_100a).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `vpfv` (/root/reference/pkg/src/vpfv).  Every entry point takes plain
+ * device pointers, sizes and a cudaStream_t (passed as void*), never
+ * allocates, never synchronises, and is safe to capture in a CUDA graph.
+ * All return an int status (VPFV_OK on success).
+ *
+ * Arrays named like the reference's are the reference's arrays: padded
+ * float64 C-order storage `(N_0+6, ..., N_{D-1}+6)` with velocity dims
+ * fastest (grid.py:3-8, :62-64), per-line tables as built by the reference
+ * dispatcher `fused_stage` (_kernels.py:330-365).
+ */
+#ifndef VPFV_H
+#define VPFV_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -- mapped to the reference's exceptions by the
+ * Python host layer: EALIAS/EDIM/EARG -> ValueError (_kernels.py:328-329,
+ * :366-367), ENONFINITE -> FloatingPointError (_kernels.py:368-373). */
+#define VPFV_OK          0
+#define VPFV_EALIAS      1
+#define VPFV_EDIM        2
+#define VPFV_ENONFINITE  3
+#define VPFV_ECUDA       4
+#define VPFV_EARG        5
+#define VPFV_ENCCL       6
+
+/* stage flags */
+#define VPFV_EXACT       0x1   /* evaluate in the reference kernels' exact
+                                  operation order (no FMA, IEEE division):
+                                  bitwise equal to the numba kernels */
+#define VPFV_WRAP_SHIFT  1     /* bit (1+k): dim k is periodic and is read by
+                                  modular indexing into the interior instead
+                                  of from its ghost storage */
+#define VPFV_WRAP(k)     (1u << (VPFV_WRAP_SHIFT + (k)))
+
+/* "no non-finite value seen" value of the non-finite index word */
+#define VPFV_FINITE      0xFFFFFFFFFFFFFFFFull
+
+/* ---------------------------------------------------------------------- */
+/* Fused stage: dest = ca*A + cb*B + cd*dest + cL*RHS(src) on the interior.
+ *
+ * Replaces `stage_1d1v(dest, A, B, src, ca, cb, cd, cL, ax, avx, c1, hx, hv)`
+ * (/root/reference/pkg/src/vpfv/_kernels.py:92-114), `stage_1d2v(...)`
+ * (:153-197) and `stage_2d2v(...)` (:254-317), plus the non-finite scan of
+ * `fused_stage` (:368-373), which is folded into the epilogue: if
+ * `nonfinite` is non-NULL the C-order interior flat index of the first
+ * non-finite output is atomically min-ed into it (initialise to
+ * VPFV_FINITE).  `cL` is used as given unless `dt_dev` is non-NULL, in
+ * which case cL = (*dt_dev) / cL_div is read on the device (lets one CUDA
+ * graph serve every time step).  dest == src -> VPFV_EALIAS.
+ */
+int vpfv_stage_1d1v(double *dest, const double *A, const double *B, const double *src,
+                    double ca, double cb, double cd, double cL,
+                    const double *ax, const double *avx, const double *c1,
+                    double hx, double hv, int Nx, int Nv,
+                    unsigned flags, const double *dt_dev, double cL_div,
+                    unsigned long long *nonfinite, void *stream);
+
+int vpfv_stage_1d2v(double *dest, const double *A, const double *B, const double *src,
+                    double ca, double cb, double cd, double cL,
+                    const double *vxc, const double *vyc /* Nvy+1, last = cB */,
+                    const double *evx, const double *avy, const double *c1, double c2,
+                    double hx, double hvx, double hvy, int Nx, int Nvx, int Nvy,
+                    unsigned flags, const double *dt_dev, double cL_div,
+                    unsigned long long *nonfinite, void *stream);
+
+int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double *src,
+                    double ca, double cb, double cd, double cL,
+                    const double *vxc, const double *vyc, const double *evx,
+                    const double *evy, double cB, const double *c1, double c2,
+                    const double *c3, const double *c4, const double *c5,
+                    double hx, double hy, double hvx, double hvy,
+                    int Nx, int Ny, int Nvx, int Nvy,
+                    unsigned flags, const double *dt_dev, double cL_div,
+                    unsigned long long *nonfinite, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Velocity moment.  n[p] = fold_tree(f[p, :]) * vol over the velocity dims,
+ * fastest axis first, adjacent pairs with the odd tail carried -- bitwise
+ * the reference `zeroth_moment(f, "velocity-major")` (fields.py:28-47,
+ * 86-111).  N holds the d+v interior extents. */
+int vpfv_moment(const double *f, double *n, int d, int v, const int *N, double vol,
+                void *stream);
+
+/* rho = sum_s q[s] * n[s*nphys + p], then rho -= mean(rho)
+ * (fields.py:164-169; the mean is a fixed-order tree sum / nphys). */
+int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,
+                        double *rho, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Spectral Poisson solve (fields.py:172-213), hand-written fp64 FFT.
+ * Host-precomputed tables (numpy, bitwise the reference's k arrays):
+ *   tw*  : exp(-2 pi i m / N) for m < N, interleaved (re, im)
+ *   k2   : |k|^2 per mode (1D: N; 2D: kx/ky passed separately)
+ *   kd   : derivative wavenumber with the even-N Nyquist entry zeroed
+ * scratch: >= 4*Nx*Ny complex values (2D), unused in 1D.  phi may be NULL. */
+int vpfv_poisson_1d(const double *rho, double *Ex, double *phi, int N,
+                    const double *tw, const double *k2, const double *kd, void *stream);
+int vpfv_poisson_2d(const double *rho, double *Ex, double *Ey, double *phi, int Nx, int Ny,
+                    const double *twx, const double *twy, const double *kx, const double *ky,
+                    const double *kxd, const double *kyd, double *scratch, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Per-stage line tables from E, in the reference dispatcher's arithmetic
+ * (_kernels.py:330-365, fvm.py:168-201):
+ *   e[i]  = qmk2*E[i] + g                          (avx / evx)
+ *   c1[i] = t1 + (qmk2*(E[i+1]-E[i-1])) / den1      (periodic differences)
+ * 2D adds evy, c3, c4, c5 with nqmk2 = (-qm)*kappa2. */
+int vpfv_tables_1d(const double *Ex, double *e, double *c1, int Nx,
+                   double qmk2, double g, double t1, double den1, void *stream);
+int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, double *evy,
+                   double *c1, double *c3, double *c4, double *c5, int Nx, int Ny,
+                   double qmk2, double nqmk2, double gx, double gy,
+                   double t1, double t4, double denx, double deny, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Ghost fill of the periodic dims named in dims_mask (bit k = dim k), whole
+ * columns, ascending dims -- the periodic half of fill_local_ghosts
+ * (grid.py:263-277).  Frozen velocity slabs are written once at set-up. */
+int vpfv_wrap_fill(double *f, int ndim, const int *N, unsigned dims_mask, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Strided box copy between padded arrays (halo pack/unpack, scatter/gather):
+ * copies the box `ext` (D extents) from src at origin so[] (strides ss[])
+ * to dst at origin do[] (strides ds[]).  Strides/origins in elements. */
+int vpfv_box_copy(double *dst, const long long *ds, const int *dorig,
+                  const double *src, const long long *ss, const int *sorig,
+                  int ndim, const int *ext, void *stream);
+
+/* ---------------------------------------------------------------------- */
+int vpfv_version(void);
+/* 0 if device `dev` is an sm_100 part this library was built for. */
+int vpfv_check_device(int dev);
+const char *vpfv_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPFV_H */

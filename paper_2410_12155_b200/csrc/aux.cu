@@ -1,0 +1,216 @@
+// Per-stage line tables, charge density, ghost wraps, box copies, errors.
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace vpfv {
+
+static thread_local char g_err[256] = "";
+
+int set_error(int code, const char *msg) {
+    snprintf(g_err, sizeof g_err, "%s", msg);
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+        return VPFV_ECUDA;
+    }
+    return VPFV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// line tables (the arithmetic of the reference dispatcher, _kernels.py:330-365,
+// and correction_coeffs, fvm.py:168-201; every operation rounded once, no FMA)
+
+__global__ void tables1d_kernel(const double *__restrict__ E, double *__restrict__ e,
+                                double *__restrict__ c1, int n, double qmk2, double g, double t1,
+                                double den1) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double Ei = E[i];
+    const double dE = __dsub_rn(E[i + 1 < n ? i + 1 : 0], E[i > 0 ? i - 1 : n - 1]);
+    e[i] = __dadd_rn(__dmul_rn(qmk2, Ei), g);
+    c1[i] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, dE), den1));
+}
+
+__global__ void tables2d_kernel(const double *__restrict__ Ex, const double *__restrict__ Ey,
+                                double *__restrict__ evx, double *__restrict__ evy,
+                                double *__restrict__ c1, double *__restrict__ c3,
+                                double *__restrict__ c4, double *__restrict__ c5, int nx, int ny,
+                                double qmk2, double nqmk2, double gx, double gy, double t1,
+                                double t4, double denx, double deny) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nx * ny) return;
+    const int i = p / ny, j = p - i * ny;
+    const int ip = (i + 1 < nx ? i + 1 : 0) * ny + j, im = (i > 0 ? i - 1 : nx - 1) * ny + j;
+    const int jp = i * ny + (j + 1 < ny ? j + 1 : 0), jm = i * ny + (j > 0 ? j - 1 : ny - 1);
+    const double dEx_x = __dsub_rn(Ex[ip], Ex[im]);
+    const double dEy_y = __dsub_rn(Ey[jp], Ey[jm]);
+    const double dEx_y = __dsub_rn(Ex[jp], Ex[jm]);
+    const double dEy_x = __dsub_rn(Ey[ip], Ey[im]);
+    evx[p] = __dadd_rn(__dmul_rn(qmk2, Ex[p]), gx);
+    evy[p] = __dadd_rn(__dmul_rn(qmk2, Ey[p]), gy);
+    c1[p] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, dEx_x), denx));
+    c3[p] = __ddiv_rn(__dmul_rn(nqmk2, dEx_y), denx);
+    c4[p] = __dadd_rn(t4, __ddiv_rn(__dmul_rn(qmk2, dEy_y), deny));
+    c5[p] = __ddiv_rn(__dmul_rn(nqmk2, dEy_x), deny);
+}
+
+// ---------------------------------------------------------------------------
+// charge density: rho = sum_s q_s n_s - mean (one CTA, fixed-order sums)
+
+struct Charges {
+    double q[8];
+};
+
+__global__ void charge_kernel(const double *__restrict__ n, Charges q, int ns, int nphys,
+                              double *__restrict__ rho) {
+    __shared__ double part[1024];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double acc = 0.0;
+    for (int p = tid; p < nphys; p += nt) {
+        double r = __dmul_rn(q.q[0], n[p]);
+        for (int s = 1; s < ns; ++s) r = __dadd_rn(r, __dmul_rn(q.q[s], n[(long long)s * nphys + p]));
+        rho[p] = r;
+        acc = __dadd_rn(acc, r);
+    }
+    part[tid] = acc;
+    __syncthreads();
+    for (int w = 1; w < nt; w <<= 1) {  // adjacent-pair tree over thread partials
+        if ((tid % (2 * w)) == 0 && tid + w < nt) part[tid] = __dadd_rn(part[tid], part[tid + w]);
+        __syncthreads();
+    }
+    const double mean = __ddiv_rn(part[0], (double)nphys);
+    for (int p = tid; p < nphys; p += nt) rho[p] = __dsub_rn(rho[p], mean);
+}
+
+// ---------------------------------------------------------------------------
+// generic strided box copy (up to 4 dims)
+
+struct Box {
+    long long ds[4], ss[4];
+    int dorig[4], sorig[4], ext[4];
+    int ndim;
+    long long total;
+};
+
+__global__ void box_copy_kernel(double *__restrict__ dst, const double *__restrict__ src, Box b) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < b.total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long r = t, doff = 0, soff = 0;
+        for (int k = b.ndim - 1; k >= 0; --k) {
+            const long long c = r % b.ext[k];
+            r /= b.ext[k];
+            doff += (c + b.dorig[k]) * b.ds[k];
+            soff += (c + b.sorig[k]) * b.ss[k];
+        }
+        dst[doff] = src[soff];
+    }
+}
+
+static int launch_box(double *dst, const double *src, const Box &b, cudaStream_t s) {
+    if (b.total <= 0) return VPFV_OK;
+    long long blocks = (b.total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    box_copy_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, b);
+    return check_launch("box_copy");
+}
+
+}  // namespace vpfv
+
+using namespace vpfv;
+
+extern "C" int vpfv_tables_1d(const double *Ex, double *e, double *c1, int Nx, double qmk2,
+                              double g, double t1, double den1, void *stream) {
+    tables1d_kernel<<<(Nx + 255) / 256, 256, 0, (cudaStream_t)stream>>>(Ex, e, c1, Nx, qmk2, g, t1,
+                                                                       den1);
+    return check_launch("tables_1d");
+}
+
+extern "C" int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, double *evy,
+                              double *c1, double *c3, double *c4, double *c5, int Nx, int Ny,
+                              double qmk2, double nqmk2, double gx, double gy, double t1, double t4,
+                              double denx, double deny, void *stream) {
+    int n = Nx * Ny;
+    tables2d_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        Ex, Ey, evx, evy, c1, c3, c4, c5, Nx, Ny, qmk2, nqmk2, gx, gy, t1, t4, denx, deny);
+    return check_launch("tables_2d");
+}
+
+extern "C" int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,
+                                   double *rho, void *stream) {
+    if (nspecies < 1 || nspecies > 8) return set_error(VPFV_EARG, "1..8 species supported");
+    Charges q;
+    for (int s = 0; s < 8; ++s) q.q[s] = s < nspecies ? q_host[s] : 0.0;
+    charge_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n, q, nspecies, nphys, rho);
+    return check_launch("charge_density");
+}
+
+extern "C" int vpfv_box_copy(double *dst, const long long *ds, const int *dorig, const double *src,
+                             const long long *ss, const int *sorig, int ndim, const int *ext,
+                             void *stream) {
+    if (ndim < 1 || ndim > 4) return set_error(VPFV_EARG, "box_copy: 1..4 dims");
+    Box b;
+    b.ndim = ndim;
+    b.total = 1;
+    for (int k = 0; k < ndim; ++k) {
+        b.ds[k] = ds[k];
+        b.ss[k] = ss[k];
+        b.dorig[k] = dorig[k];
+        b.sorig[k] = sorig[k];
+        b.ext[k] = ext[k];
+        b.total *= ext[k];
+    }
+    return launch_box(dst, src, b, (cudaStream_t)stream);
+}
+
+extern "C" int vpfv_wrap_fill(double *f, int ndim, const int *N, unsigned dims_mask, void *stream) {
+    if (ndim < 2 || ndim > 4) return set_error(VPFV_EDIM, "wrap_fill: 2..4 dims");
+    long long st[4];
+    int P[4];
+    for (int k = 0; k < ndim; ++k) P[k] = N[k] + 2 * NG;
+    st[ndim - 1] = 1;
+    for (int k = ndim - 2; k >= 0; --k) st[k] = st[k + 1] * P[k + 1];
+    for (int k = 0; k < ndim; ++k) {
+        if (!(dims_mask & (1u << k))) continue;
+        Box b;
+        b.ndim = ndim;
+        b.total = 1;
+        for (int m = 0; m < ndim; ++m) {
+            b.ds[m] = b.ss[m] = st[m];
+            b.ext[m] = (m == k) ? NG : P[m];
+            b.dorig[m] = b.sorig[m] = 0;
+            b.total *= b.ext[m];
+        }
+        // low ghosts <- last interior slab; high ghosts <- first interior slab
+        b.dorig[k] = 0;
+        b.sorig[k] = N[k];
+        int rc = launch_box(f, f, b, (cudaStream_t)stream);
+        if (rc) return rc;
+        b.dorig[k] = N[k] + NG;
+        b.sorig[k] = NG;
+        rc = launch_box(f, f, b, (cudaStream_t)stream);
+        if (rc) return rc;
+    }
+    return VPFV_OK;
+}
+
+extern "C" int vpfv_version(void) { return 100; }
+
+extern "C" int vpfv_check_device(int dev) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess)
+        return set_error(VPFV_ECUDA, "cudaGetDeviceProperties failed");
+    if (p.major != 10 || p.minor != 0) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "device is sm_%d%d; libvpfv is built for sm_100a", p.major, p.minor);
+        return set_error(VPFV_EDIM, buf);
+    }
+    return VPFV_OK;
+}
+
+extern "C" const char *vpfv_last_error(void) { return g_err; }

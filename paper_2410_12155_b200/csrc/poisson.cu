@@ -1,0 +1,235 @@
+// Spectral periodic Poisson solve and field reconstruction (fields.py:172-213).
+//
+//   rho_hat = FFT(rho);  phi_hat = rho_hat / |k|^2 (k != 0), phi_hat_0 = 0
+//   E_hat_d = -i kd_d phi_hat   (kd: Nyquist entry zeroed for even N)
+//   E_d = Re IFFT(E_hat_d)
+//
+// Hand-written fp64 transforms in shared memory: radix-2 decimation-in-time
+// for power-of-two lines, a direct O(N^2) DFT with exact (k*n mod N) twiddle
+// indices otherwise.  Twiddles exp(-2 pi i m/N) and the wavenumber tables are
+// built on the host with numpy (bitwise the reference's k arrays).
+// 1D: one CTA does the whole solve.  2D: row pass -> column pass (with the
+// spectral multiply and both inverse column transforms) -> inverse row pass.
+#include "common.cuh"
+
+namespace vpfv {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// In-place transform of n complex values held in smem `a` by the whole CTA.
+// pow2: `a` must already be in bit-reversed order.  Otherwise `tmp` holds the
+// natural-order input and the DFT result is written to `a`.
+__device__ void line_transform(double2 *a, double2 *tmp, int n, const double2 *__restrict__ tw,
+                               bool inverse, bool pow2) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (pow2) {
+        for (int len = 2; len <= n; len <<= 1) {
+            const int half = len >> 1, step = n / len;
+            for (int j = tid; j < (n >> 1); j += nt) {
+                const int grp = j / half, pos = j - grp * half;
+                const int i1 = grp * len + pos, i2 = i1 + half;
+                double2 w = tw[pos * step];
+                if (inverse) w.y = -w.y;
+                double2 t = cmul(w, a[i2]);
+                double2 x = a[i1];
+                a[i1] = make_double2(x.x + t.x, x.y + t.y);
+                a[i2] = make_double2(x.x - t.x, x.y - t.y);
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int k = tid; k < n; k += nt) {
+            double2 acc = make_double2(0.0, 0.0);
+            long long idx = 0;
+            for (int m = 0; m < n; ++m) {
+                double2 w = tw[idx];
+                if (inverse) w.y = -w.y;
+                double2 t = cmul(w, tmp[m]);
+                acc.x += t.x;
+                acc.y += t.y;
+                idx += k;
+                if (idx >= n) idx -= n;
+            }
+            a[k] = acc;
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ int bitrev(int x, int logn) { return (int)(__brev((unsigned)x) >> (32 - logn)); }
+
+// store natural-order value v for position m into the transform input
+__device__ __forceinline__ void put(double2 *a, double2 *tmp, int m, double2 v, bool pow2, int logn) {
+    if (pow2) a[bitrev(m, logn)] = v;
+    else tmp[m] = v;
+}
+
+// ---------------------------------------------------------------------------
+// 1D: single CTA
+
+__global__ void poisson1d_kernel(const double *__restrict__ rho, double *__restrict__ Ex,
+                                 double *__restrict__ phi, int n, const double2 *__restrict__ tw,
+                                 const double *__restrict__ k2, const double *__restrict__ kd,
+                                 int pow2, int logn) {
+    extern __shared__ double2 sm2[];
+    double2 *a = sm2, *tmp = sm2 + n, *ph = sm2 + 2 * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int m = tid; m < n; m += nt) put(a, tmp, m, make_double2(rho[m], 0.0), pow2, logn);
+    __syncthreads();
+    line_transform(a, tmp, n, tw, false, pow2);
+    // phi_hat and E_hat (E_hat = -i kd phi_hat = (kd*ph.y, -kd*ph.x))
+    for (int k = tid; k < n; k += nt) {
+        double2 p = make_double2(0.0, 0.0);
+        if (k > 0) p = make_double2(a[k].x / k2[k], a[k].y / k2[k]);
+        ph[k] = p;
+    }
+    __syncthreads();
+    for (int pass = (phi ? 0 : 1); pass < 2; ++pass) {
+        for (int k = tid; k < n; k += nt) {
+            double2 v = ph[k];
+            if (pass == 1) v = make_double2(kd[k] * v.y, -(kd[k] * v.x));
+            put(a, tmp, k, v, pow2, logn);
+        }
+        __syncthreads();
+        line_transform(a, tmp, n, tw, true, pow2);
+        const double inv = 1.0 / (double)n;
+        double *out = pass == 0 ? phi : Ex;
+        for (int m = tid; m < n; m += nt) out[m] = a[m].x * inv;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 2D: three passes over lines
+
+// forward row transforms: C[i, :] = FFT_y(rho[i, :])
+__global__ void rows_fwd_kernel(const double *__restrict__ rho, double2 *__restrict__ C, int nx,
+                                int ny, const double2 *__restrict__ twy, int pow2, int logn) {
+    extern __shared__ double2 sm2[];
+    double2 *a = sm2, *tmp = sm2 + ny;
+    const int i = blockIdx.x;
+    for (int m = threadIdx.x; m < ny; m += blockDim.x)
+        put(a, tmp, m, make_double2(rho[(long long)i * ny + m], 0.0), pow2, logn);
+    __syncthreads();
+    line_transform(a, tmp, ny, twy, false, pow2);
+    for (int m = threadIdx.x; m < ny; m += blockDim.x) C[(long long)i * ny + m] = a[m];
+}
+
+// column pass: FFT_x, spectral multiply, inverse FFT_x for each requested
+// output; D[o][:, j] (o = 0: Ex, 1: Ey, 2: phi) scaled by 1/nx.
+__global__ void cols_kernel(const double2 *__restrict__ C, double2 *__restrict__ D, int nx, int ny,
+                            const double2 *__restrict__ twx, const double *__restrict__ kx,
+                            const double *__restrict__ ky, const double *__restrict__ kxd,
+                            const double *__restrict__ kyd, int nout, int pow2, int logn) {
+    extern __shared__ double2 sm2[];
+    double2 *a = sm2, *tmp = sm2 + nx, *ph = sm2 + 2 * nx;
+    const int j = blockIdx.x;
+    const long long plane = (long long)nx * ny;
+    for (int m = threadIdx.x; m < nx; m += blockDim.x)
+        put(a, tmp, m, C[(long long)m * ny + j], pow2, logn);
+    __syncthreads();
+    line_transform(a, tmp, nx, twx, false, pow2);
+    const double kyj = ky[j];
+    for (int m = threadIdx.x; m < nx; m += blockDim.x) {
+        const double kk = kx[m] * kx[m] + kyj * kyj;
+        ph[m] = kk > 0.0 ? make_double2(a[m].x / kk, a[m].y / kk) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const double inv = 1.0 / (double)nx;
+    for (int o = 0; o < nout; ++o) {
+        for (int m = threadIdx.x; m < nx; m += blockDim.x) {
+            double2 v = ph[m];
+            if (o < 2) {
+                const double kd = (o == 0) ? kxd[m] : kyd[j];
+                v = make_double2(kd * v.y, -(kd * v.x));
+            }
+            put(a, tmp, m, v, pow2, logn);
+        }
+        __syncthreads();
+        line_transform(a, tmp, nx, twx, true, pow2);
+        for (int m = threadIdx.x; m < nx; m += blockDim.x)
+            D[o * plane + (long long)m * ny + j] = make_double2(a[m].x * inv, a[m].y * inv);
+        __syncthreads();
+    }
+}
+
+// inverse row transforms: out_o[i, :] = Re IFFT_y(D[o][i, :])
+__global__ void rows_inv_kernel(const double2 *__restrict__ D, double *__restrict__ Ex,
+                                double *__restrict__ Ey, double *__restrict__ phi, int nx, int ny,
+                                const double2 *__restrict__ twy, int nout, int pow2, int logn) {
+    extern __shared__ double2 sm2[];
+    double2 *a = sm2, *tmp = sm2 + ny;
+    const int i = blockIdx.x;
+    const long long plane = (long long)nx * ny;
+    const double inv = 1.0 / (double)ny;
+    for (int o = 0; o < nout; ++o) {
+        for (int m = threadIdx.x; m < ny; m += blockDim.x)
+            put(a, tmp, m, D[o * plane + (long long)i * ny + m], pow2, logn);
+        __syncthreads();
+        line_transform(a, tmp, ny, twy, true, pow2);
+        double *out = o == 0 ? Ex : (o == 1 ? Ey : phi);
+        for (int m = threadIdx.x; m < ny; m += blockDim.x) out[(long long)i * ny + m] = a[m].x * inv;
+        __syncthreads();
+    }
+}
+
+static int ilog2_if_pow2(int n) {
+    if (n <= 0 || (n & (n - 1))) return -1;
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+
+static void allow_smem(const void *fn) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+}  // namespace vpfv
+
+using namespace vpfv;
+
+extern "C" int vpfv_poisson_1d(const double *rho, double *Ex, double *phi, int N, const double *tw,
+                               const double *k2, const double *kd, void *stream) {
+    if (N < 2) return set_error(VPFV_EARG, "poisson_1d: N < 2");
+    const int logn = ilog2_if_pow2(N);
+    size_t smem = sizeof(double2) * 3 * (size_t)N;
+    if (smem > 200 * 1024) return set_error(VPFV_EARG, "poisson_1d: N too large for one CTA");
+    static bool once = false;
+    if (!once) {
+        allow_smem((const void *)poisson1d_kernel);
+        once = true;
+    }
+    poisson1d_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(
+        rho, Ex, phi, N, (const double2 *)tw, k2, kd, logn >= 0, logn < 0 ? 0 : logn);
+    return check_launch("poisson_1d");
+}
+
+extern "C" int vpfv_poisson_2d(const double *rho, double *Ex, double *Ey, double *phi, int Nx,
+                               int Ny, const double *twx, const double *twy, const double *kx,
+                               const double *ky, const double *kxd, const double *kyd,
+                               double *scratch, void *stream) {
+    if (Nx < 2 || Ny < 2) return set_error(VPFV_EARG, "poisson_2d: extents < 2");
+    const int lx = ilog2_if_pow2(Nx), ly = ilog2_if_pow2(Ny);
+    size_t smx = sizeof(double2) * 3 * (size_t)Nx, smy = sizeof(double2) * 2 * (size_t)Ny;
+    if (smx > 200 * 1024 || smy > 200 * 1024) return set_error(VPFV_EARG, "poisson_2d: too large");
+    static bool once = false;
+    if (!once) {
+        allow_smem((const void *)rows_fwd_kernel);
+        allow_smem((const void *)cols_kernel);
+        allow_smem((const void *)rows_inv_kernel);
+        once = true;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    double2 *C = (double2 *)scratch;
+    double2 *D = C + (size_t)Nx * Ny;  // up to 3 planes follow... reuse C's plane for phi
+    const int nout = phi ? 3 : 2;
+    // D needs nout planes; scratch holds 1 + 3 planes when phi is requested
+    rows_fwd_kernel<<<Nx, 256, smy, s>>>(rho, C, Nx, Ny, (const double2 *)twy, ly >= 0, ly < 0 ? 0 : ly);
+    cols_kernel<<<Ny, 256, smx, s>>>(C, D, Nx, Ny, (const double2 *)twx, kx, ky, kxd, kyd, nout,
+                                     lx >= 0, lx < 0 ? 0 : lx);
+    rows_inv_kernel<<<Nx, 256, smy, s>>>(D, Ex, Ey, phi, Nx, Ny, (const double2 *)twy, nout,
+                                         ly >= 0, ly < 0 ? 0 : ly);
+    return check_launch("poisson_2d");
+}

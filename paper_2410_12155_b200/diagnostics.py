@@ -1,0 +1,141 @@
+"""Conserved-quantity rows, field amplitude, growth-rate fits (host side).
+
+Mirrors /root/reference/pkg/src/vpfv/diagnostics.py: ``DiagnosticsRow``,
+``DIAGNOSTICS_SCHEMA``, ``field_amplitude``, ``conserved_quantities``,
+``fit_growth_rate``.  These run per output cadence, not per stage, on host
+copies of the device state (moving them onto the device is SURVEY.md 8f
+row 1).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .grid import NGHOST
+
+DIAGNOSTICS_SCHEMA = "vpfv-diagnostics-1"
+
+
+@dataclass(frozen=True)
+class DiagnosticsRow:
+    t: float
+    dt: float
+    mass: tuple
+    momentum: float
+    field_energy: float
+    kinetic_energy: float
+    total_energy: float
+    field_amplitude: float
+
+    @staticmethod
+    def header(species_names):
+        return (["t", "dt"] + [f"mass_{n}" for n in species_names]
+                + ["momentum", "field_energy", "kinetic_energy", "total_energy", "field_amplitude"])
+
+    def values(self):
+        return ([self.t, self.dt] + [m for _, m in self.mass]
+                + [self.momentum, self.field_energy, self.kinetic_energy, self.total_energy,
+                   self.field_amplitude])
+
+
+def _fold(x, axis):
+    x = np.moveaxis(x, axis, -1)
+    while x.shape[-1] > 1:
+        n = x.shape[-1]
+        m = n // 2
+        s = x[..., 0:2 * m:2] + x[..., 1:2 * m:2]
+        x = np.concatenate([s, x[..., 2 * m:]], axis=-1) if n % 2 else s
+    return np.moveaxis(x, -1, axis)
+
+
+def fold_tree_sum(x, axes):
+    """Deterministic pairwise tree, fastest axis first (fields.py:42-47)."""
+    out = np.array(x, dtype=np.float64, copy=True)
+    for ax in sorted(axes, reverse=True):
+        out = _fold(out, ax)
+    return np.squeeze(out, axis=tuple(sorted(axes)))
+
+
+def field_amplitude(E, grid):
+    """sqrt(integral E.E dx) (diagnostics.py:74-82)."""
+    vol = 1.0
+    for k in range(grid.d):
+        vol *= grid.h[k]
+    total = 0.0
+    for comp in E.values():
+        total += float(np.sum(np.square(np.asarray(comp))))
+    return math.sqrt(total * vol)
+
+
+def higher_moments(data, grid):
+    """Momentum and kinetic-energy densities with the midpoint-to-average lift
+    (fields.py:131-161); ghosts of ``data`` must be synchronised."""
+    g = grid
+    inner = g.interior_slices()
+    f = data[inner]
+    vol = 1.0
+    for k in g.velocity_dims:
+        vol *= g.h[k]
+    vaxes = tuple(g.velocity_dims)
+    mom, kin = [], 0.0
+    for d in g.velocity_dims:
+        shape = [1] * g.ndim
+        shape[d] = g.N[d]
+        vc = g.centers(d).reshape(shape)
+        h2 = g.h[d] ** 2
+        lo = [0] * g.ndim
+        hi = [0] * g.ndim
+        lo[d], hi[d] = -1, 1
+        sh = lambda off: data[tuple(slice(NGHOST + o, NGHOST + o + n) for o, n in zip(off, g.N))]  # noqa: E731
+        dfd = (sh(hi) - sh(lo)) / (2.0 * g.h[d])
+        mom.append((vc * f + (h2 / 12.0) * dfd).sum(axis=vaxes) * vol)
+        kin = kin + ((vc ** 2 + h2 / 12.0) * f + (h2 / 6.0) * vc * dfd).sum(axis=vaxes) * vol
+    return mom, 0.5 * kin
+
+
+def conserved_quantities(datas, grids, species, E, t, dt):
+    """One DiagnosticsRow from host padded arrays with synchronised ghosts
+    (diagnostics.py:85-122)."""
+    masses = []
+    mom_tot = None
+    kinetic = 0.0
+    for data, g, sp in zip(datas, grids, species):
+        cellvol = 1.0
+        for w in g.h:
+            cellvol *= w
+        interior = data[g.interior_slices()]
+        masses.append((sp.name, float(fold_tree_sum(interior, tuple(range(g.ndim)))) * cellvol))
+        mom, kin = higher_moments(data, g)
+        physvol = 1.0
+        for k in range(g.d):
+            physvol *= g.h[k]
+        if mom_tot is None:
+            mom_tot = [0.0] * len(mom)
+        for k, mk in enumerate(mom):
+            mom_tot[k] += sp.m * float(np.sum(mk)) * physvol
+        kinetic += sp.m * float(np.sum(kin)) * physvol
+    U = 0.5 * field_amplitude(E, grids[0]) ** 2
+    return DiagnosticsRow(t=t, dt=dt, mass=tuple(masses), momentum=math.sqrt(sum(p * p for p in mom_tot)),
+                          field_energy=U, kinetic_energy=kinetic, total_energy=U + kinetic,
+                          field_amplitude=field_amplitude(E, grids[0]))
+
+
+def fit_growth_rate(ts, amps, t_min=None, t_max=None, peaks=False):
+    """Least-squares slope of log |E| (the amplitude convention of
+    diagnostics.py:133-160); ``peaks=True`` fits only local maxima, the robust
+    choice for damped oscillations."""
+    ts = np.asarray(ts, dtype=float)
+    a = np.asarray(amps, dtype=float)
+    lo = -np.inf if t_min is None else t_min
+    hi = np.inf if t_max is None else t_max
+    if peaks:
+        idx = [i for i in range(1, len(a) - 1)
+               if a[i] >= a[i - 1] and a[i] > a[i + 1] and lo <= ts[i] <= hi]
+    else:
+        idx = [i for i in range(len(a)) if lo <= ts[i] <= hi]
+    if len(idx) < 2:
+        raise ValueError("not enough samples in the fit window")
+    return float(np.polyfit(ts[idx], np.log(a[idx]), 1)[0])

@@ -1,0 +1,181 @@
+"""The fused stage operator on the B200: tables + launch + the drop-in API.
+
+``fused_stage(dest, A, B, src, ca, cb, cd, cL, grid, species, E, check=True)``
+is the drop-in replacement for the reference dispatcher
+(/root/reference/pkg/src/vpfv/_kernels.py:320-373): same arguments, same
+in-place semantics on the interior, same errors (``ValueError`` for
+``dest is src`` or an unsupported dimensionality, ``FloatingPointError`` with
+the interior multi-index of the first non-finite output).  Arrays may be
+host numpy arrays (copied to/from the device around the call) or float64
+CUDA tensors.  ``exact=True`` (the default here) evaluates in the reference
+kernels' operation order and is bitwise equal to them; the drivers default to
+the FMA fast path.
+
+``StageTables`` holds one species' per-line tables on the device: static
+ones (velocity centres, the magnetic factor, ...) built once on the host in
+the reference's numpy arithmetic, and the E-dependent ones recomputed on the
+device each stage by ``vpfv_tables_*``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fvm import _g, magnetic_factor
+
+SUPPORTED = ((1, 1), (1, 2), (2, 2))
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(device=None):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class StageTables:
+    """Per-species device tables for the fused stage kernel."""
+
+    def __init__(self, grid, species, device, corrections=True):
+        if (grid.d, grid.v) not in SUPPORTED:
+            raise ValueError(f"unsupported dimensionality ({grid.d},{grid.v})")
+        self.grid, self.species, self.device = grid, species, device
+        self.corrections = corrections
+        s, g, h = species, grid, grid.h
+        gx, gy = _g(s)[:2]
+        cB = magnetic_factor(s)
+        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)  # noqa: E731
+        self.gx, self.gy, self.cB = gx, gy, cB
+        self.qmk2 = s.qm * s.kappa2            # (_kernels.py:337) qm*kappa2 first
+        self.nqmk2 = -s.qm * s.kappa2          # (fvm.py:198) (-qm)*kappa2
+        nphys = int(np.prod(g.N[:g.d]))
+        phys_shape = tuple(g.N[:g.d])
+        if (g.d, g.v) == (1, 1):
+            self.ax = dev(g.centers(1))
+            self.t1, self.den1 = h[1] / (48.0 * h[0]), 96.0 * h[1]
+            self.e = torch.empty(phys_shape, dtype=torch.float64, device=device)   # avx
+            self.c1 = torch.empty(phys_shape, dtype=torch.float64, device=device)
+        elif (g.d, g.v) == (1, 2):
+            self.vxc = dev(g.centers(1))
+            vyc = np.empty(g.N[2] + 1)
+            vyc[:-1] = g.centers(2)
+            vyc[-1] = cB
+            self.vyc = dev(vyc)
+            self.avy = dev(-cB * g.centers(1) + gy)
+            self.c2 = float(s.qm * (s.kappa_c / 48.0) * s.Bz * (h[1] / h[2] - h[2] / h[1]))
+            self.t1, self.den1 = h[1] / (48.0 * h[0]), 96.0 * h[1]
+            self.e = torch.empty(phys_shape, dtype=torch.float64, device=device)   # evx
+            self.c1 = torch.empty(phys_shape, dtype=torch.float64, device=device)
+        else:
+            self.vxc = dev(g.centers(2))
+            self.vyc = dev(g.centers(3))
+            self.c2 = float(s.qm * (s.kappa_c / 48.0) * s.Bz * (h[2] / h[3] - h[3] / h[2]))
+            self.t1, self.t4 = h[2] / (48.0 * h[0]), h[3] / (48.0 * h[1])
+            self.denx, self.deny = 96.0 * h[2], 96.0 * h[3]
+            mk = lambda: torch.empty(phys_shape, dtype=torch.float64, device=device)  # noqa: E731
+            self.evx, self.evy, self.c1, self.c3, self.c4, self.c5 = (mk() for _ in range(6))
+        if not corrections:
+            self.c2 = 0.0
+        self.nphys = nphys
+
+    # -- per-stage tables from E (device arrays on the physical grid) ---------
+    def update(self, E, stream):
+        g = self.grid
+        if g.d == 1:
+            Ex = E["Ex"]
+            _lib.call("vpfv_tables_1d", Ex.data_ptr(), self.e.data_ptr(), self.c1.data_ptr(),
+                      g.N[0], self.qmk2, self.gx, self.t1, self.den1, stream)
+            if not self.corrections:
+                self.c1.zero_()
+        else:
+            _lib.call("vpfv_tables_2d", E["Ex"].data_ptr(), E["Ey"].data_ptr(),
+                      self.evx.data_ptr(), self.evy.data_ptr(), self.c1.data_ptr(),
+                      self.c3.data_ptr(), self.c4.data_ptr(), self.c5.data_ptr(), g.N[0], g.N[1],
+                      self.qmk2, self.nqmk2, self.gx, self.gy, self.t1, self.t4, self.denx,
+                      self.deny, stream)
+            if not self.corrections:
+                for c in (self.c1, self.c3, self.c4, self.c5):
+                    c.zero_()
+
+    # -- launch ---------------------------------------------------------------
+    def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
+               nonfinite=None):
+        g, h, N = self.grid, self.grid.h, self.grid.N
+        common_tail = (flags, _ptr(dt_dev), float(cL_div), _ptr(nonfinite), stream)
+        head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
+                float(ca), float(cb), float(cd), float(cL))
+        if (g.d, g.v) == (1, 1):
+            _lib.call("vpfv_stage_1d1v", *head, self.ax.data_ptr(), self.e.data_ptr(),
+                      self.c1.data_ptr(), h[0], h[1], N[0], N[1], *common_tail)
+        elif (g.d, g.v) == (1, 2):
+            _lib.call("vpfv_stage_1d2v", *head, self.vxc.data_ptr(), self.vyc.data_ptr(),
+                      self.e.data_ptr(), self.avy.data_ptr(), self.c1.data_ptr(), self.c2,
+                      h[0], h[1], h[2], N[0], N[1], N[2], *common_tail)
+        else:
+            _lib.call("vpfv_stage_2d2v", *head, self.vxc.data_ptr(), self.vyc.data_ptr(),
+                      self.evx.data_ptr(), self.evy.data_ptr(), self.cB, self.c1.data_ptr(),
+                      self.c2, self.c3.data_ptr(), self.c4.data_ptr(), self.c5.data_ptr(),
+                      h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3], *common_tail)
+
+
+def wrap_flags(grid, dims=None):
+    """Stage flags reading the given (default: all periodic) dims by modular index."""
+    f = 0
+    for k in range(grid.ndim):
+        if grid.periodic[k] and (dims is None or k in dims):
+            f |= _lib.VPFV_WRAP(k)
+    return f
+
+
+def nonfinite_index(flag_value, grid):
+    """Interior multi-index of a flat C-order interior offset."""
+    return tuple(int(i) for i in np.unravel_index(int(flag_value), grid.N))
+
+
+def _to_device(a, device, cache):
+    if isinstance(a, torch.Tensor):
+        if not a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("device arrays must be contiguous float64 CUDA tensors")
+        return a
+    key = id(a)
+    if key not in cache:
+        cache[key] = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+    return cache[key]
+
+
+def fused_stage(dest, A, B, src, ca, cb, cd, cL, grid, species, E, check=True, exact=True):
+    """Drop-in for the reference ``fused_stage`` (_kernels.py:320-373)."""
+    if dest is src:
+        raise ValueError("dest must not alias src")
+    if (grid.d, grid.v) not in SUPPORTED:
+        raise ValueError(f"unsupported dimensionality ({grid.d},{grid.v})")
+    device = src.device if isinstance(src, torch.Tensor) else torch.device("cuda", torch.cuda.current_device())
+    _lib.check_device(device.index if device.index is not None else torch.cuda.current_device())
+    cache = {}
+    d_dest = _to_device(dest, device, cache)
+    d_A, d_B, d_src = (_to_device(x, device, cache) for x in (A, B, src))
+    if d_dest.data_ptr() == d_src.data_ptr():
+        raise ValueError("dest must not alias src")
+    for x in (d_dest, d_A, d_B, d_src):
+        if tuple(x.shape) != grid.padded_shape:
+            raise ValueError(f"array shape {tuple(x.shape)} != padded {grid.padded_shape}")
+    E_dev = {k: _to_device(v, device, cache) for k, v in E.items()}
+    tables = StageTables(grid, species, device)
+    stream = stream_handle(device)
+    tables.update(E_dev, stream)
+    flag = None
+    if check:
+        flag = torch.full((1,), -1, dtype=torch.int64, device=device)
+    flags = _lib.VPFV_EXACT if exact else 0
+    tables.launch(d_dest, d_A, d_B, d_src, ca, cb, cd, cL, flags, stream, nonfinite=flag)
+    if not isinstance(dest, torch.Tensor):
+        inner = grid.interior_slices()
+        dest[inner] = d_dest[inner].cpu().numpy()
+    if check:
+        v = int(flag.item()) & 0xFFFFFFFFFFFFFFFF
+        if v != _lib.VPFV_FINITE:
+            mi = nonfinite_index(v, grid)
+            raise FloatingPointError(f"non-finite stage output at interior index {mi}")

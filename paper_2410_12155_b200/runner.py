@@ -1,0 +1,265 @@
+"""Single-GPU driver: the reference ``Simulation`` with its state on the B200.
+
+Mirrors /root/reference/pkg/src/vpfv/runner.py:126-256 (``Simulation``,
+``RunDiverged``, ``stable_dt``): same constructor, ``advance``/``run``/
+``current_dt``/``max_dt``/``interiors``/``state``/``diagnostics_row``/
+``persistent_buffers`` and the three persistent buffers per species in a
+``StepContext`` (here float64 CUDA tensors in the reference's padded layout).
+
+Per stage (runner.py:183-191) the device runs
+    moments (fold tree) -> rho -> Poisson/E -> line tables -> fused stage
+and ``advance`` replays one CUDA graph holding all four stages of a step
+(cL read on the device as dt / cL_div, so one graph serves every dt).
+Ghosts: frozen velocity slabs are written into all three buffers once at
+set-up (kernels write interiors only); periodic dims are read by modular
+indexing inside the stage kernel, so no per-stage ghost fill exists.
+The non-finite check of ``advance`` (runner.py:219-227) is the stage-4
+epilogue flag, read back once per step, with the reference's rollback.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .diagnostics import conserved_quantities
+from .fields import FieldSolver
+from .fvm import max_speed_per_dim
+from .grid import DistField, FrozenGhosts, fill_local_ghosts
+from .kernels import StageTables, stream_handle, wrap_flags
+from .timestepping import DEFAULT_SIGMA, RK4_STAGES, StepContext, max_stable_dt
+
+
+class RunDiverged(RuntimeError):
+    """Non-finite state; f0 holds the last completed state (runner.py:64-66)."""
+
+
+def stable_dt(grids, species, E, sigma=DEFAULT_SIGMA):
+    """min over species of sigma / sum_d max|A_d|/h_d (runner.py:98-103)."""
+    return min(max_stable_dt([max_speed_per_dim(g, sp, E)], g.h, sigma=sigma)
+               for g, sp in zip(grids, species))
+
+
+def _host_filled(f):
+    """Padded float64 host copy of a set-up field with its ghosts filled the
+    way the reference's first stage fills them, plus its frozen slabs."""
+    data = f.data.detach().cpu().numpy() if isinstance(f.data, torch.Tensor) else f.data
+    data = np.array(data, dtype=np.float64, copy=True)
+    df = DistField(f.grid, f.species, data)
+    frozen = FrozenGhosts.capture(df)
+    fill_local_ghosts(df, frozen)
+    return data, frozen
+
+
+def require_cuda(device=None):
+    if not torch.cuda.is_available():
+        raise _lib.VpfvError("no CUDA device visible: the B200 path has no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    _lib.check_device(dev.index)
+    return dev
+
+
+class Simulation:
+    """Whole-domain driver owning exactly three device buffers per species."""
+
+    def __init__(self, setup, cfl_fraction=0.9, dt=None, corrections=True,
+                 schedule="velocity-major", sigma=DEFAULT_SIGMA, *, device=None, exact=False,
+                 use_graphs=True):
+        if schedule not in ("velocity-major", "position-major", "free"):
+            raise ValueError(f"unknown schedule {schedule!r}")
+        self.device = require_cuda(device)
+        self.species = tuple(setup.species)
+        self.grids = tuple(f.grid for f in setup.dists)
+        self.cfl_fraction = cfl_fraction
+        self.fixed_dt = dt
+        self.corrections = corrections
+        self.schedule = schedule
+        self.sigma = sigma
+        self.exact = exact
+        self.use_graphs = use_graphs
+        self._names = [f.species for f in setup.dists]
+        f0, self.frozen = [], []
+        for f in setup.dists:
+            data, frozen = _host_filled(f)
+            f0.append(torch.from_numpy(data).to(self.device))
+            self.frozen.append(frozen)
+        # velocity ghosts are frozen: all three buffers start as the filled t=0 array
+        self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
+        self.tables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
+        self.fields = FieldSolver(self.grids, self.species, self.device)
+        base = _lib.VPFV_EXACT if exact else 0
+        self.flags = [base | wrap_flags(g) for g in self.grids]
+        S = len(self.species)
+        self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
+        self._flags_host = torch.empty((4, S), dtype=torch.int64, pin_memory=True)
+        self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._graphs = {}
+        self._last_E = None
+        self._timing = False
+        self._events = None
+        self._stage_ms = [0.0] * 4
+
+    # -- state access --------------------------------------------------------
+    @property
+    def t(self):
+        return self.ctx.t
+
+    @property
+    def step_count(self):
+        return self.ctx.step
+
+    def persistent_buffers(self):
+        return (self.ctx.f0, self.ctx.f1, self.ctx.fout)
+
+    # -- the stage protocol (timestepping.py:69-84 calls this) ---------------
+    def _stage(self, dest, A, B, src, ca, cb, cd, cL, t, *, dt_dev=None, cL_div=1.0, slot=None):
+        stream = stream_handle(self.device)
+        E = self.fields.solve(src, stream=stream)
+        self._last_E = E
+        for s, tab in enumerate(self.tables):
+            tab.update(E, stream)
+            nf = None if slot is None else self.nonfinite[slot, s:s + 1]
+            timed = self._timing and slot is not None
+            if timed:
+                self._events[slot][s][0].record()
+            tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
+                       dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf)
+            if timed:
+                self._events[slot][s][1].record()
+
+    def _step_body(self, f0, f1, fout):
+        bufs = {"f0": f0, "f1": f1, "fout": fout}
+        self.nonfinite.fill_(-1)
+        for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
+            self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, None,
+                        dt_dev=self.dt_dev, cL_div=div, slot=slot)
+
+    # -- in-step timing of the fused stage kernel (bench roofline) -----------
+    def enable_stage_timing(self, on=True):
+        """Record CUDA events around every stage-kernel launch of ``advance``
+        (captured into the step graph as external event nodes)."""
+        import torch as _t
+
+        self._timing = bool(on)
+        self._stage_ms = [0.0] * 4
+        if on and self._events is None:
+            S = len(self.species)
+            self._events = [[(_t.cuda.Event(enable_timing=True, external=True),
+                              _t.cuda.Event(enable_timing=True, external=True)) for _ in range(S)]
+                            for _ in range(4)]
+
+    def stage_kernel_ms(self):
+        return list(self._stage_ms)
+
+    def _accumulate_timing(self):
+        if self._timing:
+            for slot in range(4):
+                for a, b in self._events[slot]:
+                    self._stage_ms[slot] += a.elapsed_time(b)
+
+    def launches_per_step(self):
+        """libvpfv kernels launched per RK4 step."""
+        S = len(self.species)
+        poisson = 1 if self.grids[0].d == 1 else 3
+        return 4 * (S + 1 + poisson + 2 * S)
+
+    def _graph_for(self, bufs):
+        key = (self._timing,) + tuple(tuple(a.data_ptr() for a in b) for b in bufs)
+        g = self._graphs.get(key)
+        if g is None:
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):  # warm-up: first launches outside capture
+                self._step_body(*bufs)
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._step_body(*bufs)
+            self._graphs[key] = g
+        return g
+
+    def launch_step(self, dt):
+        """Enqueue one RK4 step (no host sync, no rotate)."""
+        self.dt_dev.fill_(float(dt))
+        bufs = (self.ctx.f0, self.ctx.f1, self.ctx.fout)
+        if self.use_graphs:
+            self._graph_for(bufs).replay()
+        else:
+            self._step_body(*bufs)
+
+    # -- timestep control -----------------------------------------------------
+    def _E_host(self, arrays):
+        E = self.fields.solve(arrays)
+        return {k: v.cpu().numpy() for k, v in E.items()}
+
+    def max_dt(self):
+        return stable_dt(self.grids, self.species, self._E_host(self.ctx.f0), self.sigma)
+
+    def current_dt(self):
+        if self.fixed_dt is not None:
+            return self.fixed_dt
+        bound = self.max_dt()
+        if not math.isfinite(bound):
+            raise RunDiverged("stability bound is not finite (empty flow?)")
+        return bound * self.cfl_fraction
+
+    # -- stepping ---------------------------------------------------------------
+    def advance(self, dt):
+        self.launch_step(dt)
+        self._flags_host.copy_(self.nonfinite, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        self._accumulate_timing()
+        self.ctx.t = self.ctx.t + dt
+        self.ctx.rotate()
+        bad = self._flags_host[3].numpy().astype(np.uint64)
+        for s in range(len(self.species)):
+            if bad[s] != np.uint64(_lib.VPFV_FINITE):
+                self.ctx.f0, self.ctx.fout = self.ctx.fout, self.ctx.f0
+                self.ctx.t -= dt
+                self.ctx.step -= 1
+                raise RunDiverged(f"species {self._names[s]} non-finite")
+
+    def interiors(self):
+        return [a[g.interior_slices()].cpu().numpy().copy() for a, g in zip(self.ctx.f0, self.grids)]
+
+    def _host_state(self):
+        datas = []
+        for a, g, fr in zip(self.ctx.f0, self.grids, self.frozen):
+            h = a.cpu().numpy().copy()
+            fill_local_ghosts(DistField(g, data=h), fr)
+            datas.append(h)
+        return datas
+
+    def state(self):
+        from .fields import FieldState
+
+        dists = [DistField(g, n, d) for g, n, d in zip(self.grids, self._names, self._host_state())]
+        return FieldState.solve(dists, self.species, self.schedule)
+
+    def diagnostics_row(self, dt):
+        E = self._E_host(self.ctx.f0)
+        return conserved_quantities(self._host_state(), self.grids, self.species, E, self.ctx.t, dt)
+
+    def field_amplitude(self):
+        from .diagnostics import field_amplitude
+
+        return field_amplitude(self._E_host(self.ctx.f0), self.grids[0])
+
+    def run(self, t_end, cadence=10, max_steps=10 ** 7, on_row=None):
+        rows = [self.diagnostics_row(0.0)]
+        if on_row:
+            on_row(rows[0])
+        while self.ctx.t < t_end - 1e-12 and self.ctx.step < max_steps:
+            dt = min(self.current_dt(), t_end - self.ctx.t)
+            self.advance(dt)
+            if self.ctx.step % cadence == 0 or self.ctx.t >= t_end - 1e-12:
+                row = self.diagnostics_row(dt)
+                rows.append(row)
+                if on_row:
+                    on_row(row)
+        return rows

@@ -1,0 +1,311 @@
+"""GPU parity tests: the sm_100a library against the oracle / reference fixtures.
+
+Everything calls through the C ABI (libvpfv.so via ctypes).  Bars:
+* exact mode: bitwise equal to the reference fused kernels;
+* fast mode and full steps: relative L2 on f <= 1e-12 per step (north star);
+* physics: Landau damping and two-stream rates vs the reference's frozen
+  dispersion roots (/root/reference/pkg/tests/test_dispersion.py:185-212,
+  :497-508).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as G
+from oracle import vpfv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2410_12155_b200 import _lib, fields as F, kernels as K, problems as P, runner as R  # noqa: E402
+from paper_2410_12155_b200.grid import make_grid  # noqa: E402
+
+
+def pgrid(g):
+    return make_grid(g.d, g.v, g.N, g.lo, g.hi, periodic=g.periodic)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+# ---------------------------------------------------------------------------
+# fused stage
+
+
+@pytest.mark.parametrize("name", G.STAGE_NAMES)
+def test_stage_exact_bitwise_host_buffers(name):
+    c = G.stage_case(name)
+    g = pgrid(c["grid"])
+    for (ca, cb, cd, cL), want in zip(c["coefs"], c["out"]):
+        dest = c["dest"].copy()
+        K.fused_stage(dest, c["A"], c["B"], c["src"], ca, cb, cd, cL, g, c["species"], c["E"])
+        assert np.array_equal(dest[g.interior_slices()], want)
+
+
+@pytest.mark.parametrize("name", G.STAGE_NAMES)
+def test_stage_exact_bitwise_device_buffers(name):
+    c = G.stage_case(name)
+    g = pgrid(c["grid"])
+    dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    A, B, src = dev(c["A"]), dev(c["B"]), dev(c["src"])
+    E = {k: dev(v) for k, v in c["E"].items()}
+    for (ca, cb, cd, cL), want in zip(c["coefs"], c["out"]):
+        dest = dev(c["dest"].copy())
+        K.fused_stage(dest, A, B, src, ca, cb, cd, cL, g, c["species"], E)
+        assert np.array_equal(dest[g.interior_slices()].cpu().numpy(), want)
+        # ghosts untouched
+        d0 = c["dest"].copy()
+        d0[g.interior_slices()] = want
+        assert np.array_equal(dest.cpu().numpy(), d0)
+
+
+@pytest.mark.parametrize("name", G.STAGE_NAMES)
+def test_stage_fast_close(name):
+    c = G.stage_case(name)
+    g = pgrid(c["grid"])
+    for (ca, cb, cd, cL), want in zip(c["coefs"], c["out"]):
+        dest = c["dest"].copy()
+        K.fused_stage(dest, c["A"], c["B"], c["src"], ca, cb, cd, cL, g, c["species"], c["E"], exact=False)
+        got = dest[g.interior_slices()]
+        assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_stage_aliasing_patterns_of_rk4(exact):
+    """The four RK stages alias A/B/dest with src and each other
+    (timestepping.py:80-83); device results equal the oracle on the same
+    aliasing."""
+    c = G.stage_case("stage_2d2v_frozen")
+    g = pgrid(c["grid"])
+    og, sp = c["grid"], c["species"]
+    f0, f1 = c["src"].copy(), c["A"].copy()
+    O.fill_ghosts(f1, og, O.capture_frozen(f0, og))
+    fout = c["B"].copy()
+    for (dn, an, bn, sn, ca, cb, cd, cL) in [("f1", "f0", "f0", "f0", 1.0, 0.0, 0.0, 0.01),
+                                              ("fout", "f0", "f1", "f1", 2.0, -1.0, 0.0, 0.03),
+                                              ("f1", "fout", "fout", "fout", -1.0, 0.0, 2.0, 0.03),
+                                              ("fout", "f0", "f1", "f1", -0.125, 0.375, 0.75, 0.00375)]:
+        host = {"f0": f0.copy(), "f1": f1.copy(), "fout": fout.copy()}
+        O.fused_stage(host[dn], host[an], host[bn], host[sn], ca, cb, cd, cL, og, sp, c["E"], check=False)
+        devb = {k: torch.from_numpy(v.copy()).cuda() for k, v in (("f0", f0), ("f1", f1), ("fout", fout))}
+        K.fused_stage(devb[dn], devb[an], devb[bn], devb[sn], ca, cb, cd, cL, g, sp, c["E"], exact=exact)
+        got = devb[dn][g.interior_slices()].cpu().numpy()
+        want = host[dn][og.inner()]
+        if exact:
+            assert np.array_equal(got, want)
+        else:
+            assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want))
+
+
+def test_alias_rejected_and_nonfinite_index():
+    c = G.stage_case("stage_1d2v_periodic")
+    g = pgrid(c["grid"])
+    src = torch.from_numpy(c["src"]).cuda()
+    with pytest.raises(ValueError):
+        K.fused_stage(src, src, src, src, 0, 0, 0, 1.0, g, c["species"], c["E"])
+    bad = c["src"].copy()
+    bad[8, 7, 9] = np.inf
+    with pytest.raises(FloatingPointError) as ei:
+        K.fused_stage(np.zeros(g.padded_shape), bad, bad, bad, 0, 0, 0, 1.0, g, c["species"], c["E"])
+    host = np.zeros(g.padded_shape)
+    with pytest.raises(FloatingPointError) as eo:
+        O.fused_stage(host, bad, bad, bad, 0, 0, 0, 1.0, c["grid"], c["species"], c["E"])
+    assert str(ei.value) == str(eo.value)
+
+
+def test_unsupported_dimensionality():
+    from paper_2410_12155_b200.grid import PhaseSpaceGrid
+
+    g = PhaseSpaceGrid(2, 3, (8,) * 5, (0.0,) * 5, (1.0,) * 5, (True,) * 5)
+    with pytest.raises(ValueError):
+        K.fused_stage(np.zeros(1), np.zeros(1), np.zeros(1), np.ones(1), 0, 0, 0, 1.0, g, None, {})
+
+
+def test_constant_field_is_steady_all_periodic():
+    """Constant f on a torus: every face difference and diagonal vanishes."""
+    g = make_grid(2, 2, [8, 8, 8, 8], [0, 0, -1, -1], [1, 1, 1, 1], periodic=(True,) * 4)
+    from paper_2410_12155_b200.fvm import SpeciesConfig
+
+    f = torch.full(g.padded_shape, 1.7, dtype=torch.float64, device="cuda")
+    dest = torch.zeros_like(f)
+    E = {"Ex": np.full((8, 8), 0.3), "Ey": np.full((8, 8), -0.2)}
+    K.fused_stage(dest, f, f, f, 1.0, 0.0, 0.0, 0.1, g, SpeciesConfig(kappa_c=0.5, Bz=1.0), E, exact=False)
+    assert torch.equal(dest[g.interior_slices()], f[g.interior_slices()])
+
+
+# ---------------------------------------------------------------------------
+# moments and Poisson
+
+
+@pytest.mark.parametrize("name", G.MOMENT_NAMES)
+def test_moment_bitwise(name):
+    from paper_2410_12155_b200.grid import DistField
+
+    g, data, want = G.moment_case(name + ".npz")
+    got = F.zeroth_moment(DistField(pgrid(g), data=data))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("nv", [(32, 32), (128, 128), (64, 1024), (12, 10), (33, 17), (1024,)])
+def test_moment_bitwise_shapes(nv):
+    from paper_2410_12155_b200.grid import DistField
+
+    if len(nv) == 1:
+        og = O.Grid(1, 1, (8,) + nv, (0.0, -1.0), (1.0, 1.0))
+    else:
+        og = O.Grid(1, 2, (8,) + nv, (0.0, -1.0, -2.0), (1.0, 1.0, 2.0))
+    data = np.random.default_rng(5).random(og.padded_shape)
+    got = F.zeroth_moment(DistField(pgrid(og), data=data))
+    assert np.array_equal(got, O.zeroth_moment(data, og))
+
+
+@pytest.mark.parametrize("name", G.POISSON_NAMES)
+def test_poisson_vs_reference(name):
+    g, arr = G.poisson_case(name + ".npz")
+    phi, E = F.poisson_solve(arr["rho"], pgrid(g))
+    for k, v in E.items():
+        assert np.max(np.abs(v - arr[k])) <= 1e-13 * max(1.0, np.max(np.abs(arr[k])))
+    assert np.max(np.abs(phi - arr["phi"])) <= 1e-13 * max(1.0, np.max(np.abs(arr["phi"])))
+
+
+@pytest.mark.parametrize("n", [(128,), (1024,), (100,), (128, 128), (64, 32), (24, 20)])
+def test_poisson_eigen_and_oracle(n):
+    rng = np.random.default_rng(len(n) * 1000 + n[0])
+    if len(n) == 1:
+        og = O.Grid(1, 1, (n[0], 8), (0.0, -1.0), (2 * np.pi, 1.0))
+    else:
+        og = O.Grid(2, 2, (n[0], n[1], 8, 8), (0.0, 0.0, -1, -1), (4 * np.pi, 2 * np.pi, 1, 1))
+    rho = rng.standard_normal(n)
+    rho -= rho.mean()
+    _, want = O.poisson_solve(rho, og)
+    _, got = F.poisson_solve(rho, pgrid(og))
+    for k in want:
+        assert np.max(np.abs(got[k] - want[k])) <= 1e-13 * np.max(np.abs(want[k]))
+
+
+# ---------------------------------------------------------------------------
+# full steps through the Simulation driver
+
+
+@pytest.mark.parametrize("name", G.STEP_NAMES)
+@pytest.mark.parametrize("exact", [False, True])
+def test_simulation_steps_vs_reference(name, exact):
+    c = G.step_case(name)
+    mk = {
+        "landau1d": lambda: P.make_landau_1d(P.landau_spec(alpha=0.01), 16, 16),
+        "twostream": lambda: P.make_problem(P.ProblemSpec("two-stream"), 16, 16),
+        "dgh": lambda: P.make_problem(P.ProblemSpec("dgh"), 8, 8),
+        "lhdi": lambda: P.make_problem(P.ProblemSpec("lhdi"), 8, 8),
+        "bimax1d2v": lambda: P.make_bimaxwellian_1d2v(8, 8, 10),
+        "landau2d": lambda: P.make_problem(P.landau_spec(), 8, 8),
+    }[name]
+    sim = R.Simulation(mk(), dt=c["dt"], exact=exact)
+    for k in range(3):
+        sim.advance(c["dt"])
+        if k in (0, 2):
+            for s, a in enumerate(sim.interiors()):
+                want = c["out"][f"step{k + 1}_f{s}"]
+                assert rel_l2(a, want) <= 1e-12, (name, k, s, rel_l2(a, want))
+
+
+def test_graph_replay_equals_eager():
+    a = R.Simulation(P.make_problem(P.landau_spec(), 8, 8), dt=0.05, use_graphs=True)
+    b = R.Simulation(P.make_problem(P.landau_spec(), 8, 8), dt=0.05, use_graphs=False)
+    for _ in range(4):
+        a.advance(0.05)
+        b.advance(0.05)
+    assert np.array_equal(a.interiors()[0], b.interiors()[0])
+
+
+def test_protocol_stage_equals_advance():
+    """rk4_38_low_storage_step(ctx, dt, sim._stage) == sim.advance(dt)."""
+    from paper_2410_12155_b200.timestepping import rk4_38_low_storage_step
+
+    a = R.Simulation(P.make_problem(P.ProblemSpec("lhdi"), 8, 8), dt=0.002)
+    b = R.Simulation(P.make_problem(P.ProblemSpec("lhdi"), 8, 8), dt=0.002)
+    a.advance(0.002)
+    rk4_38_low_storage_step(b.ctx, 0.002, b._stage)
+    b.ctx.rotate()
+    for x, y in zip(a.interiors(), b.interiors()):
+        assert np.array_equal(x, y)
+
+
+def test_three_persistent_buffers_and_divergence():
+    sim = R.Simulation(P.make_problem(P.ProblemSpec("two-stream"), 16, 16), dt=1e-3)
+    ids = {id(b[0]) for b in sim.persistent_buffers()}
+    ptrs = {b[0].data_ptr() for b in sim.persistent_buffers()}
+    for _ in range(5):
+        sim.advance(sim.current_dt())
+    assert {id(b[0]) for b in sim.persistent_buffers()} == ids
+    assert {b[0].data_ptr() for b in sim.persistent_buffers()} == ptrs
+    good = sim.interiors()[0]
+    sim.ctx.f0[0][8, 8] = math.nan
+    with pytest.raises(R.RunDiverged):
+        for _ in range(60):
+            sim.advance(sim.current_dt())
+    assert np.all(np.isfinite(sim.interiors()[0]))
+    assert sim.step_count >= 5 and good.shape == sim.interiors()[0].shape
+
+
+def test_cfl_dt_matches_oracle():
+    c = G.step_case("twostream")
+    sim = R.Simulation(P.make_problem(P.ProblemSpec("two-stream"), 16, 16))
+    ref = O.OracleSimulation(c["grids"], c["species"], c["init"])
+    assert sim.current_dt() == pytest.approx(ref.current_dt(), rel=1e-12)
+
+
+@pytest.mark.parametrize("maker,N", [("landau2d", 32), ("bimax", 32), ("ep", 16)])
+def test_medium_step_vs_c_oracle(maker, N):
+    """One step at a size where the threaded C oracle still takes seconds."""
+    from oracle import cbackend as C
+
+    mk = {"landau2d": lambda: P.make_problem(P.landau_spec(), N, N),
+          "bimax": lambda: P.make_bimaxwellian_1d2v(N, N, N),
+          "ep": lambda: P.make_electron_proton_2d2v(N, N)}[maker]
+    setup = mk()
+    dt = 0.9 * R.Simulation(mk()).max_dt()
+    sim = R.Simulation(setup, dt=dt)
+    ref = C.CSimulation([f.grid for f in setup.dists], setup.species, [f.data for f in mk().dists], dt=dt)
+    for _ in range(2):
+        sim.advance(dt)
+        ref.advance(dt)
+    for a, b in zip(sim.interiors(), ref.interiors()):
+        assert rel_l2(a, b) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# physics rates (north star: Landau-damping and two-stream rates must match)
+
+
+def _amplitude_history(sim, t_end):
+    ts, amps = [0.0], [sim.field_amplitude()]
+    while sim.t < t_end - 1e-12:
+        sim.advance(min(sim.current_dt(), t_end - sim.t))
+        ts.append(sim.t)
+        amps.append(sim.field_amplitude())
+    return np.array(ts), np.array(amps)
+
+
+def test_landau_damping_rate():
+    from paper_2410_12155_b200.diagnostics import fit_growth_rate
+
+    sim = R.Simulation(P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128))
+    ts, amps = _amplitude_history(sim, 20.0)
+    gamma = fit_growth_rate(ts, amps, peaks=True)
+    root = -0.15335946690960492  # test_dispersion.py:497-508 (k = 0.5)
+    assert abs(gamma - root) <= 0.02 * abs(root), gamma
+    assert abs(gamma - (-0.15416)) <= 2e-3  # CPU oracle fit at 128^2
+
+
+def test_two_stream_growth_rate():
+    from paper_2410_12155_b200.diagnostics import fit_growth_rate
+
+    sim = R.Simulation(P.make_problem(P.ProblemSpec("two-stream"), 256, 256))
+    ts, amps = _amplitude_history(sim, 25.0)
+    gamma = fit_growth_rate(ts, amps, t_min=10.0, t_max=25.0)
+    root = 0.2931724221224933  # test_dispersion.py:185-212 table, k = 0.6, v_T^2 = 0.1
+    assert abs(gamma - root) <= 0.01 * root, gamma
+    assert abs(gamma - 0.29312) <= 1e-3  # CPU oracle fit at 256^2

@@ -1,0 +1,147 @@
+"""CPU-side tests: the C ABI library, host API mirror and set-ups (no GPU)."""
+
+import math
+import re
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from paper_2410_12155_b200 import _lib, grid as GR, problems as P, timestepping as TS
+from paper_2410_12155_b200.fvm import SpeciesConfig, correction_coeffs
+from paper_2410_12155_b200.grid import DistField, FrozenGhosts, fill_local_ghosts, make_grid
+
+
+def header_symbols():
+    import os
+
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "vpfv.h")).read()
+    return sorted(set(re.findall(r"\b(vpfv_[a-z0-9_]+)\s*\(", hdr)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+    assert lib.vpfv_version() >= 100
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(8|9)\d", out)
+
+
+@pytest.mark.parametrize("name", G.STEP_NAMES)
+def test_problem_setups_bitwise_vs_reference(name):
+    c = G.step_case(name)
+    mk = {
+        "landau1d": lambda: P.make_landau_1d(P.landau_spec(alpha=0.01), 16, 16),
+        "twostream": lambda: P.make_problem(P.ProblemSpec("two-stream"), 16, 16),
+        "dgh": lambda: P.make_problem(P.ProblemSpec("dgh"), 8, 8),
+        "lhdi": lambda: P.make_problem(P.ProblemSpec("lhdi"), 8, 8),
+        "bimax1d2v": lambda: P.make_bimaxwellian_1d2v(8, 8, 10),
+        "landau2d": lambda: P.make_problem(P.landau_spec(), 8, 8),
+    }[name]
+    setup = mk()
+    assert len(setup.dists) == len(c["init"])
+    for f, want, gm, sm in zip(setup.dists, c["init"], c["meta"]["grids"], c["meta"]["species"]):
+        assert np.array_equal(f.data, want)
+        assert f.grid.N == tuple(gm["N"]) and f.grid.lo == tuple(gm["lo"]) and f.grid.hi == tuple(gm["hi"])
+    for sp, sm in zip(setup.species, c["meta"]["species"]):
+        assert (sp.q, sp.m, sp.kappa2, sp.kappa_c, sp.Bz) == (sm["q"], sm["m"], sm["kappa2"], sm["kappa_c"], sm["Bz"])
+
+
+@pytest.mark.parametrize("name", G.STAGE_NAMES)
+def test_host_correction_coeffs_bitwise(name):
+    c = G.stage_case(name)
+    g = c["grid"]
+    pg = make_grid(g.d, g.v, g.N, g.lo, g.hi, periodic=g.periodic)
+    s = c["species"]
+    sp = SpeciesConfig(s.name, s.q, s.m, s.kappa2, s.kappa_c, s.Bz, s.G)
+    for k, v in correction_coeffs(pg, sp, c["E"]).items():
+        assert np.array_equal(np.asarray(v), c["arrays"]["coef_" + k])
+
+
+class TestGrid:
+    def test_validation(self):
+        with pytest.raises(ValueError):
+            make_grid(2, 1, [8] * 3, [0] * 3, [1] * 3)
+        with pytest.raises(ValueError):
+            make_grid(1, 1, [7, 8], [0, 0], [1, 1])
+        with pytest.raises(ValueError):
+            make_grid(1, 1, [8, 8], [0, 1], [1, 1])
+
+    def test_flat_index_round_trip(self):
+        g = make_grid(1, 2, [8, 9, 10], [0, -1, -1], [1, 1, 1])
+        for mi in [(-3, -3, -3), (0, 0, 0), (7, 8, 9), (10, 11, 12), (3, -1, 4)]:
+            assert GR.unflatten(g, GR.flat_index(g, mi)) == mi
+
+    def test_ghost_fill_matches_oracle(self):
+        from oracle import vpfv_oracle as O
+
+        g = make_grid(1, 2, [8, 9, 10], [0, -1, -1], [1, 1, 1])
+        rng = np.random.default_rng(3)
+        a = rng.random(g.padded_shape)
+        b = a.copy()
+        fr = FrozenGhosts.capture(DistField(g, data=a))
+        fill_local_ghosts(DistField(g, data=a), fr)
+        og = O.grid_from(g)
+        O.fill_ghosts(b, og, O.capture_frozen(b, og))
+        assert np.array_equal(a, b)
+
+    def test_float64_enforced(self):
+        g = make_grid(1, 1, [8, 8], [0, -1], [1, 1])
+        with pytest.raises(TypeError):
+            DistField(g, data=np.zeros(g.padded_shape, dtype=np.float32))
+
+
+class TestStageProtocol:
+    @pytest.mark.parametrize("z", [-0.5, -2.0, 0.3, -1.0 + 1.2j, 2.5j])
+    def test_low_storage_quartic(self, z):
+        dt = 0.7
+        lam = z / dt
+
+        def stage(dest, A, B, src, ca, cb, cd, cL, t):
+            dest[...] = ca * A + cb * B + cd * dest + cL * (lam * src)
+
+        ctx = TS.StepContext(f0=np.asarray(1.0 + 0j), f1=np.zeros((), complex), fout=np.zeros((), complex))
+        TS.rk4_38_low_storage_step(ctx, dt, stage)
+        R = 1 + z + z ** 2 / 2 + z ** 3 / 6 + z ** 4 / 24
+        assert abs(ctx.fout - R) <= 1e-13 * abs(R)
+
+    def test_stage_table_matches_reference_calls(self):
+        calls = []
+        ctx = TS.StepContext(f0="a", f1="b", fout="c", t=1.0)
+        TS.rk4_38_low_storage_step(ctx, 0.3, lambda *a: calls.append(a))
+        assert [c[:8] for c in calls] == [
+            ("b", "a", "a", "a", 1.0, 0.0, 0.0, 0.3 / 3.0),
+            ("c", "a", "b", "b", 2.0, -1.0, 0.0, 0.3),
+            ("b", "c", "c", "c", -1.0, 0.0, 2.0, 0.3),
+            ("c", "a", "b", "b", -0.125, 0.375, 0.75, 0.3 / 8.0),
+        ]
+        assert [c[8] for c in calls] == [1.0, 1.0 + 0.3 / 3.0, 1.0 + 2.0 * 0.3 / 3.0, 1.0 + 0.3]
+        assert ctx.t == 1.3
+
+    def test_max_stable_dt(self):
+        assert TS.max_stable_dt([[1.0, 1.0]], [1.0, 1.0], sigma=1.73) == pytest.approx(0.865)
+        assert TS.max_stable_dt([[0.0, 0.0]], [1.0, 1.0]) == math.inf
+        with pytest.raises(ValueError):
+            TS.max_stable_dt([[1.0]], [1.0, 1.0])
+
+
+def test_synthetic_setups_shapes():
+    s3 = P.make_bimaxwellian_1d2v(8, 8, 8)
+    g = s3.dists[0].grid
+    assert (g.d, g.v) == (1, 2) and g.h[1] != g.h[2]
+    c = correction_coeffs(g, s3.species[0], {"Ex": np.zeros(8)})
+    assert c["c2"] != 0.0
+    s5 = P.make_electron_proton_2d2v(8, 8)
+    assert [sp.name for sp in s5.species] == ["i", "e"]
+    assert s5.species[1].m == pytest.approx(1 / 1836.0)
+    assert s5.dists[0].grid.N[:2] == s5.dists[1].grid.N[:2]
