@@ -172,7 +172,7 @@ def fused_stage(dest, A, B, src, ca, cb, cd, cL, grid, species, E, check=True, e
     flags = _lib.VPFV_EXACT if exact else 0
     tables.launch(d_dest, d_A, d_B, d_src, ca, cb, cd, cL, flags, stream, nonfinite=flag)
     if not isinstance(dest, torch.Tensor):
-        inner = grid.interior_slices()
+        inner = tuple(slice(3, 3 + n) for n in grid.N)
         dest[inner] = d_dest[inner].cpu().numpy()
     if check:
         v = int(flag.item()) & 0xFFFFFFFFFFFFFFFF

@@ -129,7 +129,7 @@ def test_constant_field_is_steady_all_periodic():
     g = make_grid(2, 2, [8, 8, 8, 8], [0, 0, -1, -1], [1, 1, 1, 1], periodic=(True,) * 4)
     from paper_2410_12155_b200.fvm import SpeciesConfig
 
-    f = torch.full(g.padded_shape, 1.7, dtype=torch.float64, device="cuda")
+    f = torch.full(g.padded_shape, 1.0, dtype=torch.float64, device="cuda")
     dest = torch.zeros_like(f)
     E = {"Ex": np.full((8, 8), 0.3), "Ey": np.full((8, 8), -0.2)}
     K.fused_stage(dest, f, f, f, 1.0, 0.0, 0.0, 0.1, g, SpeciesConfig(kappa_c=0.5, Bz=1.0), E, exact=False)
