@@ -79,6 +79,42 @@ int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double
                     unsigned flags, const double *dt_dev, double cL_div,
                     unsigned long long *nonfinite, void *stream);
 
+/* 2D-2V stage with the fused velocity-moment epilogue: as vpfv_stage_2d2v,
+ * and when moment_partials is non-NULL the kernel also writes, for every new
+ * dest cell row (x, y, vx) and every aligned 32-wide vy chunk c, the
+ * fold-tree subtree sum  moment_partials[((x*Ny + y)*Nvx + vx)*(Nvy/32) + c]
+ * (finish with vpfv_moment_partials).  Runs the TMA-tiled x-marching kernel
+ * (requires the fast path, stored velocity ghosts, Ny%4 == Nvx%8 == Nvy%32
+ * == 0); otherwise falls back to the generic kernel (and rejects a non-NULL
+ * moment_partials with VPFV_EARG).  xsegments <= 0 picks a split of the x
+ * march automatically.  vpfv_stage_2d2v == this with moment_partials NULL. */
+int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const double *src,
+                          double ca, double cb, double cd, double cL,
+                          const double *vxc, const double *vyc, const double *evx,
+                          const double *evy, double cB, const double *c1, double c2,
+                          const double *c3, const double *c4, const double *c5,
+                          double hx, double hy, double hvx, double hvy,
+                          int Nx, int Ny, int Nvx, int Nvy,
+                          unsigned flags, const double *dt_dev, double cL_div,
+                          unsigned long long *nonfinite, double *moment_partials,
+                          int xsegments, void *stream);
+
+/* The untiled one-thread-per-cell 2D-2V kernel (exact or fast), always. */
+int vpfv_stage_2d2v_generic(double *dest, const double *A, const double *B, const double *src,
+                            double ca, double cb, double cd, double cL,
+                            const double *vxc, const double *vyc, const double *evx,
+                            const double *evy, double cB, const double *c1, double c2,
+                            const double *c3, const double *c4, const double *c5,
+                            double hx, double hy, double hvx, double hvy,
+                            int Nx, int Ny, int Nvx, int Nvy,
+                            unsigned flags, const double *dt_dev, double cL_div,
+                            unsigned long long *nonfinite, void *stream);
+
+/* Finish the fused moment: n[p] = fold(fold over chunks per vx row, then
+ * over vx) * vol -- bitwise the reference fold tree when Nvy % 32 == 0. */
+int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,
+                         double vol, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Velocity moment.  n[p] = fold_tree(f[p, :]) * vol over the velocity dims,
  * fastest axis first, adjacent pairs with the odd tail carried -- bitwise

@@ -282,6 +282,9 @@ static Update make_update(double *dest, const double *A, const double *B, const 
     return u;
 }
 
+struct Stage22;
+bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
+
 }  // namespace vpfv
 
 using namespace vpfv;
@@ -325,6 +328,16 @@ extern "C" int vpfv_stage_1d2v(double *dest, const double *A, const double *B, c
     return check_launch("stage_1d2v");
 }
 
+extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B,
+                                     const double *src, double ca, double cb, double cd, double cL,
+                                     const double *vxc, const double *vyc, const double *evx,
+                                     const double *evy, double cB, const double *c1, double c2,
+                                     const double *c3, const double *c4, const double *c5, double hx,
+                                     double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
+                                     int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                                     unsigned long long *nonfinite, double *moment_partials,
+                                     int xsegments, void *stream);
+
 extern "C" int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double *src,
                                double ca, double cb, double cd, double cL, const double *vxc,
                                const double *vyc, const double *evx, const double *evy, double cB,
@@ -333,6 +346,19 @@ extern "C" int vpfv_stage_2d2v(double *dest, const double *A, const double *B, c
                                int Nx, int Ny, int Nvx, int Nvy, unsigned flags,
                                const double *dt_dev, double cL_div,
                                unsigned long long *nonfinite, void *stream) {
+    return vpfv_stage_2d2v_fused(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3,
+                                 c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev, cL_div,
+                                 nonfinite, nullptr, 0, stream);
+}
+
+extern "C" int vpfv_stage_2d2v_generic(double *dest, const double *A, const double *B,
+                                       const double *src, double ca, double cb, double cd, double cL,
+                                       const double *vxc, const double *vyc, const double *evx,
+                                       const double *evy, double cB, const double *c1, double c2,
+                                       const double *c3, const double *c4, const double *c5,
+                                       double hx, double hy, double hvx, double hvy, int Nx, int Ny,
+                                       int Nvx, int Nvy, unsigned flags, const double *dt_dev,
+                                       double cL_div, unsigned long long *nonfinite, void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
     if (Nx < 1 || Ny < 1 || Nvx < 1 || Nvy < 1) return set_error(VPFV_EARG, "bad extents");
     if ((long long)Nx * Ny > 65535) return set_error(VPFV_EARG, "Nx*Ny > 65535 unsupported");

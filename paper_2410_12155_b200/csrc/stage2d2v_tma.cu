@@ -1,0 +1,588 @@
+// 2D-2V fused stage, x-marching with TMA-staged halo tiles (sm_100a, fast path).
+//
+// Same operator as stage_2d2v (/root/reference/pkg/src/vpfv/_kernels.py:254-317)
+// with the fast arithmetic policy.  Organisation:
+//
+//  * A CTA owns a (y, vx, vy) = (BJ, BK, BL) block of columns and marches
+//    along x (the slowest dim) over planes p = i0-3 .. i1+2.
+//  * Every plane's (BJ+6, BK+6, BL+8) halo tile is copied global -> shared by
+//    the Tensor Memory Accelerator (cp.async.bulk.tensor.4d, one core box plus
+//    two 3-row y-halo boxes so periodic y wraps cost nothing), NSTAGE deep,
+//    completion tracked by mbarrier transaction counts.
+//  * Each thread keeps, per column, 7 register accumulators for the cells
+//    p-3..p+3 currently "in flight" along x.  When plane p lands, it adds
+//      - its x-stencil contribution (a_x/(60 h_x) * w_o * s(p)) to cells p-o,
+//      - the in-plane part T(p): y/vx/vy fluxes + (y,vy),(vx,vy),(y,vx)
+//        corrections, all read from shared memory with immediate offsets,
+//      - the x-coupled corrections through D(p) = s[k-1]-s[k+1] and
+//        G(p) = s[l-1]-s[l+1]:  c1(q)(D(q+1)-D(q-1)) - c5(q)(G(q+1)-G(q-1)),
+//    then finalises cell p-3 with the RK4 stage combination and streams it
+//    to HBM (coalesced 256 B warp rows).
+//  * Optionally the epilogue also emits the velocity-moment partials of the
+//    new dest: a warp-shuffle fold-tree subtree over each aligned 32-wide vy
+//    chunk (bitwise the reference fold tree's first five levels), finished by
+//    vpfv_moment_from_partials.  This saves the separate moment pass over f.
+//
+// Requirements (checked by the launcher, else the generic kernel runs):
+// Ny % BJ == 0, Nvx % BK == 0, Nvy % BL == 0, even Nvy (16 B TMA strides),
+// periodic-or-halo x/y, stored (frozen) velocity ghosts.
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace vpfv {
+
+namespace tma {
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void load4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                       int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace tma
+
+struct Stage22 {
+    double *dest;
+    const double *A, *B;
+    double ca, cb, cd, cL;
+    const double *dt_dev;
+    double cL_div;
+    int a_is_src, b_is_src;
+    unsigned long long *nonfinite;
+    // tables (T22 in stage.cu)
+    const double *vxc, *vyc, *evx, *evy, *c1, *c3, *c4, *c5;
+    double cB, c2, mhx, mhy, mhvx, mhvy;
+    int Nx, Ny, Nvx, Nvy;
+    int wrap_x, wrap_y;
+    int i0, i1;        // x range of cells this launch updates (interior indices)
+    int nseg, seglen;  // x segments per column block
+    double *partials;  // moment partials [Nx][Ny][Nvx][Nvy/BL] or nullptr
+};
+
+template <int BJ, int BK, int BL, int NSTAGE>
+struct Tile {
+    static constexpr int J = BJ + 6, K = BK + 6, L = BL + 8;
+    static constexpr int KL = K * L;
+    static constexpr int ELEMS = J * K * L;
+    static constexpr int BYTES = ELEMS * 8;
+    static constexpr int THREADS = BJ * (BK / 2) * BL;
+    static constexpr int SMEM = NSTAGE * BYTES + 64;
+};
+
+// x stencil weights (face difference * 60), offsets o = -3..3
+__device__ __forceinline__ double wpos(int o) {
+    return o == -3 ? -2.0 : o == -2 ? 15.0 : o == -1 ? -60.0 : o == 0 ? 20.0 : o == 1 ? 30.0 : o == 2 ? -3.0 : 0.0;
+}
+__device__ __forceinline__ double wneg(int o) {
+    return o == -3 ? 0.0 : o == -2 ? 3.0 : o == -1 ? -30.0 : o == 0 ? -20.0 : o == 1 ? 60.0 : o == 2 ? -15.0 : 2.0;
+}
+
+// upwinded 7-point weighted sum along one in-tile direction (stride ST)
+template <int ST>
+__device__ __forceinline__ double wsum(const double *c, bool pos) {
+    double t = (pos ? -2.0 : 0.0) * c[-3 * ST];
+    t = fma(pos ? 15.0 : 3.0, c[-2 * ST], t);
+    t = fma(pos ? -60.0 : -30.0, c[-ST], t);
+    t = fma(pos ? 20.0 : -20.0, c[0], t);
+    t = fma(pos ? 30.0 : 60.0, c[ST], t);
+    t = fma(pos ? -3.0 : -15.0, c[2 * ST], t);
+    t = fma(pos ? 0.0 : 2.0, c[3 * ST], t);
+    return t;
+}
+
+template <int SA, int SB>
+__device__ __forceinline__ double dsum(const double *c) {
+    // s[+a,-b] + s[-a,+b] - s[+a,+b] - s[-a,-b]
+    return ((c[SA - SB] + c[-SA + SB]) - c[SA + SB]) - c[-SA - SB];
+}
+
+__device__ __forceinline__ double warp_tree_sum(double x) {
+    for (int off = 1; off < 32; off <<= 1) x = __dadd_rn(x, __shfl_down_sync(0xffffffffu, x, off));
+    return x;
+}
+
+template <int BJ, int BK, int BL, int NSTAGE>
+__global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
+    stage2d2v_tma_kernel(const __grid_constant__ CUtensorMap tm_core,
+                         const __grid_constant__ CUtensorMap tm_halo,
+                         const double *__restrict__ src, const Stage22 P) {
+    using TL = Tile<BJ, BK, BL, NSTAGE>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *tiles = reinterpret_cast<double *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::BYTES);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // column block of this CTA
+    const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
+    int b = blockIdx.x;
+    const int seg = b % P.nseg;
+    b /= P.nseg;
+    const int lt = b % nlt;
+    b /= nlt;
+    const int kt = b % nkt;
+    const int jt = b / nkt;
+    const int j0 = jt * BJ, k0 = kt * BK, l0 = lt * BL;
+    const int i0 = P.i0 + seg * P.seglen;
+    const int i1 = min(P.i1, i0 + P.seglen);
+    if (i0 >= i1) return;
+    (void)njt;
+
+    // thread -> cells (a, b0) and (a, b0 + BK/2), lane over l
+    const int a = warp / (BK / 2);
+    const int b0 = warp % (BK / 2);
+    const int jj = j0 + a;
+    const int kk[2] = {k0 + b0, k0 + b0 + BK / 2};
+    const int ll = l0 + lane;
+
+    // y-halo coordinates in padded storage
+    int yl = j0 - 3, yh = j0 + BJ;
+    if (P.wrap_y) {
+        if (yl < 0) yl += P.Ny;
+        if (yh >= P.Ny) yh -= P.Ny;
+    }
+    const int cy_lo = yl + NG, cy_core = j0 + NG, cy_hi = yh + NG;
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) tma::mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int p_first = i0 - 3, p_last = i1 + 2;  // planes streamed
+    const int nplanes = p_last - p_first + 1;
+    auto plane_coord = [&](int p) {
+        if (P.wrap_x) {
+            int q = p % P.Nx;
+            if (q < 0) q += P.Nx;
+            return q + NG;
+        }
+        return p + NG;
+    };
+    auto issue = [&](int n) {  // plane number n (0-based) into stage n % NSTAGE
+        const int s = n % NSTAGE;
+        double *dst = tiles + s * TL::ELEMS;
+        const int cx = plane_coord(p_first + n);
+        tma::mbar_expect_tx(&bars[s], TL::BYTES);
+        tma::load4d(dst, &tm_halo, &bars[s], l0 - 1, k0, cy_lo, cx);
+        tma::load4d(dst + 3 * TL::KL, &tm_core, &bars[s], l0 - 1, k0, cy_core, cx);
+        tma::load4d(dst + (3 + BJ) * TL::KL, &tm_halo, &bars[s], l0 - 1, k0, cy_hi, cx);
+    };
+    if (tid == 0) {
+        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n) issue(n);
+    }
+
+    // per-thread constants
+    const double vx[2] = {__ldg(P.vxc + kk[0]), __ldg(P.vxc + kk[1])};
+    const double vy = __ldg(P.vyc + ll);
+    const double ay_s = vy * P.mhy;  // y speed times -1/(60 h_y)
+    const bool ypos = vy > 0.0;
+    const bool xpos[2] = {vx[0] > 0.0, vx[1] > 0.0};
+    const double ax_s[2] = {vx[0] * P.mhx, vx[1] * P.mhx};
+    const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
+
+    // smem offsets of this thread's cells inside a tile
+    const int off0 = ((a + 3) * TL::K + (b0 + 3)) * TL::L + (lane + 4);
+    const int off1 = off0 + (BK / 2) * TL::L;
+
+    // padded global offsets of the two cells at x-interior index 0
+    const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
+                    P1 = (long long)(P.Ny + 2 * NG) * P2;
+    const long long g0 = (long long)(jj + NG) * P2 + (long long)(kk[0] + NG) * P3 + (ll + NG);
+    const long long g1 = g0 + (long long)(BK / 2) * P3;
+
+    double acc0[7], acc1[7];
+#pragma unroll
+    for (int m = 0; m < 7; ++m) acc0[m] = acc1[m] = 0.0;
+
+    for (int n = 0; n < nplanes; ++n) {
+        const int p = p_first + n;
+        // refill: the stage consumed in iteration n-1 is free after the barrier
+        if (tid == 0 && n + NSTAGE - 1 < nplanes) {
+            tma::fence_proxy_async();
+            issue(n + NSTAGE - 1);
+        }
+        const int s = n % NSTAGE;
+        tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
+        const double *tile = tiles + s * TL::ELEMS;
+
+        int pw = p;  // table index of plane p (wrapped)
+        if (P.wrap_x) {
+            pw = p % P.Nx;
+            if (pw < 0) pw += P.Nx;
+        }
+        const bool in_T = (p >= i0 && p < i1);
+        // tables of plane p and of its x neighbours (cells p-1, p+1)
+        double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
+        if (in_T) {
+            const long long e = (long long)pw * P.Ny + jj;
+            evx = __ldg(P.evx + e);
+            evy = __ldg(P.evy + e);
+            c3 = __ldg(P.c3 + e);
+            c4 = __ldg(P.c4 + e);
+        }
+        if (p - 1 >= i0 && p - 1 < i1) {
+            int q = P.wrap_x ? (pw == 0 ? P.Nx - 1 : pw - 1) : p - 1;
+            c1m = __ldg(P.c1 + (long long)q * P.Ny + jj);
+            c5m = __ldg(P.c5 + (long long)q * P.Ny + jj);
+        }
+        if (p + 1 >= i0 && p + 1 < i1) {
+            int q = P.wrap_x ? (pw == P.Nx - 1 ? 0 : pw + 1) : p + 1;
+            c1p = __ldg(P.c1 + (long long)q * P.Ny + jj);
+            c5p = __ldg(P.c5 + (long long)q * P.Ny + jj);
+        }
+        const double avx_s = fma(P.cB, vy, evx) * P.mhvx;
+        const bool vxpos = fma(P.cB, vy, evx) > 0.0;
+
+#pragma unroll
+        for (int cidx = 0; cidx < 2; ++cidx) {
+            double *acc = cidx ? acc1 : acc0;
+            const double *c = tile + (cidx ? off1 : off0);
+            const double s0 = c[0];
+            // x stencil contributions of s(p) to cells p-o (acc index 3-o)
+            const double t = ax_s[cidx] * s0;
+            if (xpos[cidx]) {
+                acc[6] = fma(-2.0, t, acc[6]);
+                acc[5] = fma(15.0, t, acc[5]);
+                acc[4] = fma(-60.0, t, acc[4]);
+                acc[3] = fma(20.0, t, acc[3]);
+                acc[2] = fma(30.0, t, acc[2]);
+                acc[1] = fma(-3.0, t, acc[1]);
+            } else {
+                acc[5] = fma(3.0, t, acc[5]);
+                acc[4] = fma(-30.0, t, acc[4]);
+                acc[3] = fma(-20.0, t, acc[3]);
+                acc[2] = fma(60.0, t, acc[2]);
+                acc[1] = fma(-15.0, t, acc[1]);
+                acc[0] = fma(2.0, t, acc[0]);
+            }
+            // x-coupled corrections through D(p), G(p) (cells p-1 and p+1)
+            const double D = c[-TL::L] - c[TL::L];
+            const double G = c[-1] - c[1];
+            acc[2] = fma(c1m, D, acc[2]);
+            acc[2] = fma(-c5m, G, acc[2]);
+            acc[4] = fma(-c1p, D, acc[4]);
+            acc[4] = fma(c5p, G, acc[4]);
+            if (in_T) {
+                const double avy = fma(-P.cB, vx[cidx], evy);
+                double T = ay_s * wsum<TL::KL>(c, ypos);
+                T = fma(avx_s, wsum<TL::L>(c, vxpos), T);
+                T = fma(avy * P.mhvy, wsum<1>(c, avy > 0.0), T);
+                T = fma(c4, dsum<TL::KL, 1>(c), T);
+                T = fma(-P.c2, dsum<TL::L, 1>(c), T);
+                T = fma(-c3, dsum<TL::KL, TL::L>(c), T);
+                acc[3] += T;
+            }
+        }
+
+        // finalize cell q = p - 3
+        const int q = p - 3;
+        if (q >= i0 && q < i1) {
+#pragma unroll
+            for (int cidx = 0; cidx < 2; ++cidx) {
+                const double rhs = cidx ? acc1[0] : acc0[0];
+                const long long g = (long long)(q + NG) * P1 + (cidx ? g1 : g0);
+                double out = cL * rhs;
+                if (P.cd != 0.0) out = fma(P.cd, P.dest[g], out);
+                double sv = 0.0;
+                if (P.a_is_src | P.b_is_src) sv = __ldg(src + g);
+                if (P.cb != 0.0) out = fma(P.cb, P.b_is_src ? sv : __ldg(P.B + g), out);
+                if (P.ca != 0.0) out = fma(P.ca, P.a_is_src ? sv : __ldg(P.A + g), out);
+                P.dest[g] = out;
+                if (P.nonfinite && !isfinite(out)) {
+                    const unsigned long long flat =
+                        (((unsigned long long)q * P.Ny + jj) * P.Nvx + kk[cidx]) * P.Nvy + ll;
+                    atomicMin(P.nonfinite, flat);
+                }
+                if (P.partials) {
+                    const double sub = warp_tree_sum(out);
+                    if (lane == 0)
+                        P.partials[(((long long)q * P.Ny + jj) * P.Nvx + kk[cidx]) * nlt + lt] = sub;
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+            acc0[m] = acc0[m + 1];
+            acc1[m] = acc1[m + 1];
+        }
+        acc0[6] = acc1[6] = 0.0;
+        __syncthreads();  // everyone is done with stage s before it is refilled
+    }
+}
+
+// ---------------------------------------------------------------------------
+// moment from partials: per physical cell, fold over the vy chunks of every
+// vx row (chunk sums are exact 32-wide subtrees), then over vx, times vol.
+
+__device__ double fold_small(double *x, int n) {  // single thread, in place
+    while (n > 1) {
+        int m = n >> 1;
+        for (int t = 0; t < m; ++t) x[t] = __dadd_rn(x[2 * t], x[2 * t + 1]);
+        if (n & 1) {
+            x[m] = x[n - 1];
+            n = m + 1;
+        } else {
+            n = m;
+        }
+    }
+    return x[0];
+}
+
+__global__ void moment_partials_kernel(const double *__restrict__ part, double *__restrict__ n,
+                                       int nphys, int nvx, int nlt, double vol) {
+    extern __shared__ double sm[];  // per warp: two buffers of nvx
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int p = blockIdx.x * wpb + warp;
+    if (p >= nphys) return;
+    double *bufA = sm + (size_t)warp * 2 * nvx, *bufB = bufA + nvx;
+    const double *src = part + (size_t)p * nvx * nlt;
+    for (int k = lane; k < nvx; k += 32) {
+        double tmp[8];
+        for (int t = 0; t < nlt; ++t) tmp[t] = src[(size_t)k * nlt + t];
+        bufA[k] = fold_small(tmp, nlt);
+    }
+    __syncwarp();
+    int len = nvx;
+    double *a = bufA, *b = bufB;
+    while (len > 1) {
+        const int m = len >> 1;
+        for (int t = lane; t < m; t += 32) b[t] = __dadd_rn(a[2 * t], a[2 * t + 1]);
+        if ((len & 1) && lane == 0) b[m] = a[len - 1];
+        __syncwarp();
+        len = m + (len & 1);
+        double *tmp = a;
+        a = b;
+        b = tmp;
+    }
+    if (lane == 0) n[p] = __dmul_rn(a[0], vol);
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps and launch
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+struct MapKey {
+    const void *ptr;
+    int n[4];
+    int box[4];
+    bool operator==(const MapKey &o) const {
+        if (ptr != o.ptr) return false;
+        for (int i = 0; i < 4; ++i)
+            if (n[i] != o.n[i] || box[i] != o.box[i]) return false;
+        return true;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey &k) const {
+        size_t h = reinterpret_cast<size_t>(k.ptr);
+        for (int i = 0; i < 4; ++i) h = h * 1000003u ^ (size_t)(k.n[i] * 131 + k.box[i]);
+        return h;
+    }
+};
+
+static bool get_map(const double *src, const int Npad[4] /* x,y,vx,vy */, const int box[4] /* l,k,j,i */,
+                    CUtensorMap *out) {
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    MapKey key{src, {Npad[0], Npad[1], Npad[2], Npad[3]}, {box[0], box[1], box[2], box[3]}};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)Npad[3], (cuuint64_t)Npad[2], (cuuint64_t)Npad[1], (cuuint64_t)Npad[0]};
+    cuuint64_t strides[3] = {(cuuint64_t)Npad[3] * 8, (cuuint64_t)Npad[3] * Npad[2] * 8,
+                             (cuuint64_t)Npad[3] * Npad[2] * Npad[1] * 8};
+    cuuint32_t bdim[4] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2], (cuuint32_t)box[3]};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUtensorMap m;
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(src), dims, strides, bdim,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    if (cache.size() > 256) cache.clear();
+    cache.emplace(key, m);
+    *out = m;
+    return true;
+}
+
+constexpr int TBJ = 4, TBK = 8, TBL = 32, TNS = 3;
+using TileCfg = Tile<TBJ, TBK, TBL, TNS>;
+
+bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
+    if (flags & VPFV_EXACT) return false;
+    if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
+    if (Ny % TBJ || Nvx % TBK || Nvy % TBL || (Nvy & 1)) return false;
+    if (Nx < 1 || Ny < 3 + TBJ) return false;
+    return encode_fn() != nullptr;
+}
+
+int launch_tma_2d2v(const double *src, Stage22 P, unsigned flags, int nseg, cudaStream_t s) {
+    const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
+    const int box_core[4] = {TBL + 8, TBK + 6, TBJ, 1};
+    const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
+    CUtensorMap mc, mh;
+    if (!get_map(src, Npad, box_core, &mc) || !get_map(src, Npad, box_halo, &mh))
+        return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
+    P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
+    P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
+    P.i0 = 0;
+    P.i1 = P.Nx;
+    P.nseg = nseg < 1 ? 1 : nseg;
+    P.seglen = (P.Nx + P.nseg - 1) / P.nseg;
+    static bool attr = false;
+    auto kern = stage2d2v_tma_kernel<TBJ, TBK, TBL, TNS>;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg::SMEM);
+        attr = true;
+    }
+    const int nblocks = (P.Ny / TBJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
+    kern<<<nblocks, TileCfg::THREADS, TileCfg::SMEM, s>>>(mc, mh, src, P);
+    return check_launch("stage_2d2v_tma");
+}
+
+int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
+                                cudaStream_t s) {
+    if (nlt > 8) return set_error(VPFV_EARG, "moment partials: at most 8 vy chunks");
+    const int wpb = 4;
+    size_t smem = sizeof(double) * (size_t)wpb * 2 * nvx;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(moment_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    moment_partials_kernel<<<(nphys + wpb - 1) / wpb, 32 * wpb, smem, s>>>(part, n, nphys, nvx, nlt, vol);
+    return check_launch("moment_from_partials");
+}
+
+}  // namespace vpfv
+
+using namespace vpfv;
+
+extern "C" int vpfv_stage_2d2v_generic(double *, const double *, const double *, const double *, double,
+                                       double, double, double, const double *, const double *,
+                                       const double *, const double *, double, const double *, double,
+                                       const double *, const double *, const double *, double, double,
+                                       double, double, int, int, int, int, unsigned, const double *,
+                                       double, unsigned long long *, void *);
+
+extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B,
+                                     const double *src, double ca, double cb, double cd, double cL,
+                                     const double *vxc, const double *vyc, const double *evx,
+                                     const double *evy, double cB, const double *c1, double c2,
+                                     const double *c3, const double *c4, const double *c5, double hx,
+                                     double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
+                                     int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                                     unsigned long long *nonfinite, double *moment_partials,
+                                     int xsegments, void *stream) {
+    if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
+    if (!tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags)) {
+        if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 2D-2V path");
+        return vpfv_stage_2d2v_generic(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2,
+                                       c3, c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev,
+                                       cL_div, nonfinite, stream);
+    }
+    Stage22 P{};
+    P.dest = dest;
+    P.A = A;
+    P.B = B;
+    P.ca = ca;
+    P.cb = cb;
+    P.cd = cd;
+    P.cL = cL;
+    P.dt_dev = dt_dev;
+    P.cL_div = cL_div;
+    P.a_is_src = (A == src);
+    P.b_is_src = (B == src);
+    P.nonfinite = nonfinite;
+    P.vxc = vxc;
+    P.vyc = vyc;
+    P.evx = evx;
+    P.evy = evy;
+    P.c1 = c1;
+    P.c3 = c3;
+    P.c4 = c4;
+    P.c5 = c5;
+    P.cB = cB;
+    P.c2 = c2;
+    P.mhx = -1.0 / (60.0 * hx);
+    P.mhy = -1.0 / (60.0 * hy);
+    P.mhvx = -1.0 / (60.0 * hvx);
+    P.mhvy = -1.0 / (60.0 * hvy);
+    P.Nx = Nx;
+    P.Ny = Ny;
+    P.Nvx = Nvx;
+    P.Nvy = Nvy;
+    P.partials = moment_partials;
+    int nseg = xsegments;
+    if (nseg <= 0) {  // enough column blocks for >= 4 waves of one CTA per SM
+        const int cols = (Ny / TBJ) * (Nvx / TBK) * (Nvy / TBL);
+        nseg = (4 * 148 + cols - 1) / cols;
+        if (nseg > Nx / 16) nseg = Nx / 16;
+        if (nseg < 1) nseg = 1;
+    }
+    return launch_tma_2d2v(src, P, flags, nseg, (cudaStream_t)stream);
+}
+
+extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,
+                                    double vol, void *stream) {
+    return launch_moment_from_partials(partials, n, nphys, Nvx, nchunks, vol, (cudaStream_t)stream);
+}

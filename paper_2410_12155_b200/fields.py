@@ -90,6 +90,21 @@ class FieldSolver:
                       self.N_arrays[s], self.vols[s], stream)
         return self.n
 
+    def moments_from_partials(self, partials, stream=None):
+        """n_s from the fused-epilogue partials of each species' last stage."""
+        stream = stream_handle(self.device) if stream is None else stream
+        for s, (g, part) in enumerate(zip(self.grids, partials)):
+            if part is None:
+                raise ValueError("species without fused moment partials")
+            _lib.call("vpfv_moment_partials", part.data_ptr(), self.n[s].data_ptr(), self.nphys,
+                      g.N[2], part.shape[-1], self.vols[s], stream)
+        return self.n
+
+    def solve_from_partials(self, partials, stream=None):
+        self.moments_from_partials(partials, stream)
+        self.charge(stream)
+        return self.poisson(self.rho, False, stream)
+
     def poisson(self, rho, with_phi=False, stream=None):
         stream = stream_handle(self.device) if stream is None else stream
         phi = self.phi.data_ptr() if with_phi else None

@@ -81,6 +81,20 @@ class StageTables:
             self.c2 = 0.0
         self.nphys = nphys
 
+    def fused_moment_ok(self, flags):
+        """True when the TMA-tiled 2D-2V kernel (and its fused moment) applies."""
+        g = self.grid
+        if (g.d, g.v) != (2, 2) or flags & _lib.VPFV_EXACT:
+            return False
+        if flags & (_lib.VPFV_WRAP(2) | _lib.VPFV_WRAP(3)):
+            return False
+        N = g.N
+        return N[1] % 4 == 0 and N[1] >= 7 and N[2] % 8 == 0 and N[3] % 32 == 0 and N[3] // 32 <= 8
+
+    def partials_shape(self):
+        g = self.grid
+        return (g.N[0], g.N[1], g.N[2], g.N[3] // 32)
+
     # -- per-stage tables from E (device arrays on the physical grid) ---------
     def update(self, E, stream):
         g = self.grid
@@ -102,7 +116,7 @@ class StageTables:
 
     # -- launch ---------------------------------------------------------------
     def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
-               nonfinite=None):
+               nonfinite=None, partials=None):
         g, h, N = self.grid, self.grid.h, self.grid.N
         common_tail = (flags, _ptr(dt_dev), float(cL_div), _ptr(nonfinite), stream)
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
@@ -115,10 +129,14 @@ class StageTables:
                       self.e.data_ptr(), self.avy.data_ptr(), self.c1.data_ptr(), self.c2,
                       h[0], h[1], h[2], N[0], N[1], N[2], *common_tail)
         else:
-            _lib.call("vpfv_stage_2d2v", *head, self.vxc.data_ptr(), self.vyc.data_ptr(),
-                      self.evx.data_ptr(), self.evy.data_ptr(), self.cB, self.c1.data_ptr(),
-                      self.c2, self.c3.data_ptr(), self.c4.data_ptr(), self.c5.data_ptr(),
-                      h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3], *common_tail)
+            args = (*head, self.vxc.data_ptr(), self.vyc.data_ptr(), self.evx.data_ptr(),
+                    self.evy.data_ptr(), self.cB, self.c1.data_ptr(), self.c2, self.c3.data_ptr(),
+                    self.c4.data_ptr(), self.c5.data_ptr(), h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3])
+            if partials is not None:
+                _lib.call("vpfv_stage_2d2v_fused", *args, flags, _ptr(dt_dev), float(cL_div),
+                          _ptr(nonfinite), partials.data_ptr(), 0, stream)
+            else:
+                _lib.call("vpfv_stage_2d2v", *args, *common_tail)
 
 
 def wrap_flags(grid, dims=None):

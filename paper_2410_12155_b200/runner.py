@@ -99,6 +99,13 @@ class Simulation:
         self._flags_host = torch.empty((4, S), dtype=torch.int64, pin_memory=True)
         self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._graphs = {}
+        self._launches = {}
+        # fused velocity moment: stages 1-3 emit the moment partials of their
+        # dest, which is the next stage's src (stage 1 of a step always runs
+        # the standalone moment, so external edits of f0 are honoured)
+        self.fuse_moment = all(t.fused_moment_ok(f) for t, f in zip(self.tables, self.flags))
+        self.partials = ([torch.empty(t.partials_shape(), dtype=torch.float64, device=self.device)
+                          for t in self.tables] if self.fuse_moment else None)
         self._last_E = None
         self._timing = False
         self._events = None
@@ -119,7 +126,12 @@ class Simulation:
     # -- the stage protocol (timestepping.py:69-84 calls this) ---------------
     def _stage(self, dest, A, B, src, ca, cb, cd, cL, t, *, dt_dev=None, cL_div=1.0, slot=None):
         stream = stream_handle(self.device)
-        E = self.fields.solve(src, stream=stream)
+        use_partials = self.fuse_moment and slot is not None and slot > 0
+        emit_partials = self.fuse_moment and slot is not None and slot < 3
+        if use_partials:
+            E = self.fields.solve_from_partials(self.partials, stream=stream)
+        else:
+            E = self.fields.solve(src, stream=stream)
         self._last_E = E
         for s, tab in enumerate(self.tables):
             tab.update(E, stream)
@@ -128,16 +140,19 @@ class Simulation:
             if timed:
                 self._events[slot][s][0].record()
             tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
-                       dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf)
+                       dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
+                       partials=self.partials[s] if emit_partials else None)
             if timed:
                 self._events[slot][s][1].record()
 
     def _step_body(self, f0, f1, fout):
         bufs = {"f0": f0, "f1": f1, "fout": fout}
+        start = _lib.launch_counter[0]
         self.nonfinite.fill_(-1)
         for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, None,
                         dt_dev=self.dt_dev, cL_div=div, slot=slot)
+        self._launches["step"] = _lib.launch_counter[0] - start
 
     # -- in-step timing of the fused stage kernel (bench roofline) -----------
     def enable_stage_timing(self, on=True):
@@ -163,10 +178,8 @@ class Simulation:
                     self._stage_ms[slot] += a.elapsed_time(b)
 
     def launches_per_step(self):
-        """libvpfv kernels launched per RK4 step."""
-        S = len(self.species)
-        poisson = 1 if self.grids[0].d == 1 else 3
-        return 4 * (S + 1 + poisson + 2 * S)
+        """libvpfv kernels launched per RK4 step (counted while capturing/running it)."""
+        return self._launches.get("step", 0)
 
     def _graph_for(self, bufs):
         key = (self._timing,) + tuple(tuple(a.data_ptr() for a in b) for b in bufs)
