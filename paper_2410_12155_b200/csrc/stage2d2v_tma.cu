@@ -5,7 +5,8 @@
 //
 //  * A CTA owns a (y, vx, vy) = (BJ, BK, BL) block of columns and marches
 //    along x (the slowest dim) over planes p = i0-3 .. i1+2.
-//  * Every plane's (BJ+6, BK+6, BL+8) halo tile is copied global -> shared by
+//  * Every plane's (BJ+6, BK+6, BL+8) halo tile (the vy box starts at the
+//    16 B-aligned padded column l0 -- TMA requires an aligned inner start) is copied global -> shared by
 //    the Tensor Memory Accelerator (cp.async.bulk.tensor.4d, one core box plus
 //    two 3-row y-halo boxes so periodic y wraps cost nothing), NSTAGE deep,
 //    completion tracked by mbarrier transaction counts.
@@ -104,6 +105,7 @@ struct Tile {
     static constexpr int BYTES = ELEMS * 8;
     static constexpr int THREADS = BJ * (BK / 2) * BL;
     static constexpr int SMEM = NSTAGE * BYTES + 64;
+    static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ;
 };
 
 // x stencil weights (face difference * 60), offsets o = -3..3
@@ -136,6 +138,26 @@ __device__ __forceinline__ double dsum(const double *c) {
 __device__ __forceinline__ double warp_tree_sum(double x) {
     for (int off = 1; off < 32; off <<= 1) x = __dadd_rn(x, __shfl_down_sync(0xffffffffu, x, off));
     return x;
+}
+
+template <class TL>
+__device__ __forceinline__ void issue_plane(double *tiles, uint64_t *bars, const CUtensorMap *pm_core,
+                                            const CUtensorMap *pm_halo, int n, int p_first,
+                                            const Stage22 &P, int l0, int k0, int cy_lo, int cy_core,
+                                            int cy_hi) {
+    constexpr int NS = TL::NSTAGE_;
+    const int s = n % NS;
+    double *dst = tiles + s * TL::ELEMS;
+    int p = p_first + n;
+    if (P.wrap_x) {
+        p %= P.Nx;
+        if (p < 0) p += P.Nx;
+    }
+    const int cx = p + NG;
+    tma::mbar_expect_tx(&bars[s], TL::BYTES);
+    tma::load4d(dst, pm_halo, &bars[s], l0, k0, cy_lo, cx);
+    tma::load4d(dst + 3 * TL::KL, pm_core, &bars[s], l0, k0, cy_core, cx);
+    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, pm_halo, &bars[s], l0, k0, cy_hi, cx);
 }
 
 template <int BJ, int BK, int BL, int NSTAGE>
@@ -187,25 +209,11 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
 
     const int p_first = i0 - 3, p_last = i1 + 2;  // planes streamed
     const int nplanes = p_last - p_first + 1;
-    auto plane_coord = [&](int p) {
-        if (P.wrap_x) {
-            int q = p % P.Nx;
-            if (q < 0) q += P.Nx;
-            return q + NG;
-        }
-        return p + NG;
-    };
-    auto issue = [&](int n) {  // plane number n (0-based) into stage n % NSTAGE
-        const int s = n % NSTAGE;
-        double *dst = tiles + s * TL::ELEMS;
-        const int cx = plane_coord(p_first + n);
-        tma::mbar_expect_tx(&bars[s], TL::BYTES);
-        tma::load4d(dst, &tm_halo, &bars[s], l0 - 1, k0, cy_lo, cx);
-        tma::load4d(dst + 3 * TL::KL, &tm_core, &bars[s], l0 - 1, k0, cy_core, cx);
-        tma::load4d(dst + (3 + BJ) * TL::KL, &tm_halo, &bars[s], l0 - 1, k0, cy_hi, cx);
-    };
+    const CUtensorMap *pm_core = &tm_core;
+    const CUtensorMap *pm_halo = &tm_halo;
     if (tid == 0) {
-        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n) issue(n);
+        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
+            issue_plane<TL>(tiles, bars, pm_core, pm_halo, n, p_first, P, l0, k0, cy_lo, cy_core, cy_hi);
     }
 
     // per-thread constants
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
 
     // smem offsets of this thread's cells inside a tile
-    const int off0 = ((a + 3) * TL::K + (b0 + 3)) * TL::L + (lane + 4);
+    const int off0 = ((a + 3) * TL::K + (b0 + 3)) * TL::L + (lane + 3);
     const int off1 = off0 + (BK / 2) * TL::L;
 
     // padded global offsets of the two cells at x-interior index 0
@@ -236,7 +244,8 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
         // refill: the stage consumed in iteration n-1 is free after the barrier
         if (tid == 0 && n + NSTAGE - 1 < nplanes) {
             tma::fence_proxy_async();
-            issue(n + NSTAGE - 1);
+            issue_plane<TL>(tiles, bars, pm_core, pm_halo, n + NSTAGE - 1, p_first, P, l0, k0, cy_lo,
+                            cy_core, cy_hi);
         }
         const int s = n % NSTAGE;
         tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
