@@ -29,6 +29,8 @@
 // periodic-or-halo x/y, stored (frozen) velocity ghosts.
 #include <cuda.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -116,17 +118,21 @@ __device__ __forceinline__ double wneg(int o) {
     return o == -3 ? 0.0 : o == -2 ? 3.0 : o == -1 ? -30.0 : o == 0 ? -20.0 : o == 1 ? 60.0 : o == 2 ? -15.0 : 2.0;
 }
 
-// upwinded 7-point weighted sum along one in-tile direction (stride ST)
+// upwinded 6-point weighted sum (face difference * 60) along one in-tile
+// direction of stride ST; the sign test is warp-uniform in practice, and the
+// sum is evaluated as three independent pairs for ILP.
 template <int ST>
 __device__ __forceinline__ double wsum(const double *c, bool pos) {
-    double t = (pos ? -2.0 : 0.0) * c[-3 * ST];
-    t = fma(pos ? 15.0 : 3.0, c[-2 * ST], t);
-    t = fma(pos ? -60.0 : -30.0, c[-ST], t);
-    t = fma(pos ? 20.0 : -20.0, c[0], t);
-    t = fma(pos ? 30.0 : 60.0, c[ST], t);
-    t = fma(pos ? -3.0 : -15.0, c[2 * ST], t);
-    t = fma(pos ? 0.0 : 2.0, c[3 * ST], t);
-    return t;
+    if (pos) {
+        const double t1 = fma(15.0, c[-2 * ST], -2.0 * c[-3 * ST]);
+        const double t2 = fma(20.0, c[0], -60.0 * c[-ST]);
+        const double t3 = fma(-3.0, c[2 * ST], 30.0 * c[ST]);
+        return (t1 + t2) + t3;
+    }
+    const double t1 = fma(-30.0, c[-ST], 3.0 * c[-2 * ST]);
+    const double t2 = fma(60.0, c[ST], -20.0 * c[0]);
+    const double t3 = fma(2.0, c[3 * ST], -15.0 * c[2 * ST]);
+    return (t1 + t2) + t3;
 }
 
 template <int SA, int SB>
@@ -173,9 +179,11 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // column block of this CTA
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
-    int b = blockIdx.x;
-    const int seg = b % P.nseg;
-    b /= P.nseg;
+    // x segment outermost: the CTAs resident at once cover neighbouring column
+    // blocks of the same x range, so their overlapping halos hit in L2
+    const int ncols = nlt * nkt * njt;
+    int b = blockIdx.x % ncols;
+    const int seg = blockIdx.x / ncols;
     const int lt = b % nlt;
     b /= nlt;
     const int kt = b % nkt;
@@ -184,7 +192,6 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
-    (void)njt;
 
     // thread -> cells (a, b0) and (a, b0 + BK/2), lane over l
     const int a = warp / (BK / 2);
@@ -247,17 +254,14 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
             issue_plane<TL>(tiles, bars, pm_core, pm_halo, n + NSTAGE - 1, p_first, P, l0, k0, cy_lo,
                             cy_core, cy_hi);
         }
-        const int s = n % NSTAGE;
-        tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
-        const double *tile = tiles + s * TL::ELEMS;
-
         int pw = p;  // table index of plane p (wrapped)
         if (P.wrap_x) {
             pw = p % P.Nx;
             if (pw < 0) pw += P.Nx;
         }
         const bool in_T = (p >= i0 && p < i1);
-        // tables of plane p and of its x neighbours (cells p-1, p+1)
+        // tables of plane p and of its x neighbours (cells p-1, p+1): issued
+        // before the TMA wait so their latency overlaps it
         double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
         if (in_T) {
             const long long e = (long long)pw * P.Ny + jj;
@@ -276,6 +280,26 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
             c1p = __ldg(P.c1 + (long long)q * P.Ny + jj);
             c5p = __ldg(P.c5 + (long long)q * P.Ny + jj);
         }
+        // RK operands of the cell finalised this iteration (q = p - 3)
+        const int q = p - 3;
+        const bool fin = (q >= i0 && q < i1);
+        double rk[2] = {0.0, 0.0};
+        if (fin) {
+#pragma unroll
+            for (int cidx = 0; cidx < 2; ++cidx) {
+                const long long g = (long long)(q + NG) * P1 + (cidx ? g1 : g0);
+                double acc_rk = 0.0, sv = 0.0;
+                if (P.a_is_src | P.b_is_src) sv = __ldg(src + g);
+                if (P.cd != 0.0) acc_rk = P.cd * P.dest[g];
+                if (P.cb != 0.0) acc_rk = fma(P.cb, P.b_is_src ? sv : __ldg(P.B + g), acc_rk);
+                if (P.ca != 0.0) acc_rk = fma(P.ca, P.a_is_src ? sv : __ldg(P.A + g), acc_rk);
+                rk[cidx] = acc_rk;
+            }
+        }
+        const int s = n % NSTAGE;
+        tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
+        const double *tile = tiles + s * TL::ELEMS;
+
         const double avx_s = fma(P.cB, vy, evx) * P.mhvx;
         const bool vxpos = fma(P.cB, vy, evx) > 0.0;
 
@@ -321,18 +345,12 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
         }
 
         // finalize cell q = p - 3
-        const int q = p - 3;
-        if (q >= i0 && q < i1) {
+        if (fin) {
 #pragma unroll
             for (int cidx = 0; cidx < 2; ++cidx) {
                 const double rhs = cidx ? acc1[0] : acc0[0];
                 const long long g = (long long)(q + NG) * P1 + (cidx ? g1 : g0);
-                double out = cL * rhs;
-                if (P.cd != 0.0) out = fma(P.cd, P.dest[g], out);
-                double sv = 0.0;
-                if (P.a_is_src | P.b_is_src) sv = __ldg(src + g);
-                if (P.cb != 0.0) out = fma(P.cb, P.b_is_src ? sv : __ldg(P.B + g), out);
-                if (P.ca != 0.0) out = fma(P.ca, P.a_is_src ? sv : __ldg(P.A + g), out);
+                const double out = fma(cL, rhs, rk[cidx]);
                 P.dest[g] = out;
                 if (P.nonfinite && !isfinite(out)) {
                     const unsigned long long flat =
@@ -582,10 +600,21 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
     P.Nvy = Nvy;
     P.partials = moment_partials;
     int nseg = xsegments;
-    if (nseg <= 0) {  // enough column blocks for >= 4 waves of one CTA per SM
+    static int env_seg = -1;
+    if (env_seg < 0) {
+        const char *e = getenv("VPFV_XSEG");
+        env_seg = e ? atoi(e) : 0;
+    }
+    if (nseg <= 0 && env_seg > 0) nseg = env_seg;
+    if (nseg <= 0) {
+        // x segments of ~32 planes: a wave of resident CTAs then touches a
+        // slab small enough for L2 to keep the halos its neighbours re-read;
+        // and at least ~4 waves of work
         const int cols = (Ny / TBJ) * (Nvx / TBK) * (Nvy / TBL);
-        nseg = (4 * 148 + cols - 1) / cols;
-        if (nseg > Nx / 16) nseg = Nx / 16;
+        nseg = Nx / 32;
+        const int waves = (4 * 148 + cols - 1) / cols;
+        if (nseg < waves) nseg = waves;
+        if (nseg > Nx / 8) nseg = Nx / 8;
         if (nseg < 1) nseg = 1;
     }
     return launch_tma_2d2v(src, P, flags, nseg, (cudaStream_t)stream);
