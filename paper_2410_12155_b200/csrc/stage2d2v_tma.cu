@@ -242,135 +242,159 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     const long long g0 = (long long)(jj + NG) * P2 + (long long)(kk[0] + NG) * P3 + (ll + NG);
     const long long g1 = g0 + (long long)(BK / 2) * P3;
 
+    // Accumulator ring: cell c = p_first + m lives in slot m % 7.  The plane
+    // loop is unrolled by 7 so every slot index is a compile-time constant
+    // (no register shuffling between planes).
     double acc0[7], acc1[7];
 #pragma unroll
     for (int m = 0; m < 7; ++m) acc0[m] = acc1[m] = 0.0;
 
-    for (int n = 0; n < nplanes; ++n) {
-        const int p = p_first + n;
-        // refill: the stage consumed in iteration n-1 is free after the barrier
-        if (tid == 0 && n + NSTAGE - 1 < nplanes) {
-            tma::fence_proxy_async();
-            issue_plane<TL>(tiles, bars, pm_core, pm_halo, n + NSTAGE - 1, p_first, P, l0, k0, cy_lo,
-                            cy_core, cy_hi);
-        }
-        int pw = p;  // table index of plane p (wrapped)
-        if (P.wrap_x) {
-            pw = p % P.Nx;
-            if (pw < 0) pw += P.Nx;
-        }
-        const bool in_T = (p >= i0 && p < i1);
-        // tables of plane p and of its x neighbours (cells p-1, p+1): issued
-        // before the TMA wait so their latency overlaps it
-        double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
-        if (in_T) {
-            const long long e = (long long)pw * P.Ny + jj;
-            evx = __ldg(P.evx + e);
-            evy = __ldg(P.evy + e);
-            c3 = __ldg(P.c3 + e);
-            c4 = __ldg(P.c4 + e);
-        }
-        if (p - 1 >= i0 && p - 1 < i1) {
-            int q = P.wrap_x ? (pw == 0 ? P.Nx - 1 : pw - 1) : p - 1;
-            c1m = __ldg(P.c1 + (long long)q * P.Ny + jj);
-            c5m = __ldg(P.c5 + (long long)q * P.Ny + jj);
-        }
-        if (p + 1 >= i0 && p + 1 < i1) {
-            int q = P.wrap_x ? (pw == P.Nx - 1 ? 0 : pw + 1) : p + 1;
-            c1p = __ldg(P.c1 + (long long)q * P.Ny + jj);
-            c5p = __ldg(P.c5 + (long long)q * P.Ny + jj);
-        }
-        // RK operands of the cell finalised this iteration (q = p - 3)
-        const int q = p - 3;
-        const bool fin = (q >= i0 && q < i1);
-        double rk[2] = {0.0, 0.0};
-        if (fin) {
-#pragma unroll
-            for (int cidx = 0; cidx < 2; ++cidx) {
-                const long long g = (long long)(q + NG) * P1 + (cidx ? g1 : g0);
-                double acc_rk = 0.0, sv = 0.0;
-                if (P.a_is_src | P.b_is_src) sv = __ldg(src + g);
-                if (P.cd != 0.0) acc_rk = P.cd * P.dest[g];
-                if (P.cb != 0.0) acc_rk = fma(P.cb, P.b_is_src ? sv : __ldg(P.B + g), acc_rk);
-                if (P.ca != 0.0) acc_rk = fma(P.ca, P.a_is_src ? sv : __ldg(P.A + g), acc_rk);
-                rk[cidx] = acc_rk;
-            }
-        }
-        const int s = n % NSTAGE;
-        tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
-        const double *tile = tiles + s * TL::ELEMS;
+    // running plane state
+    int pw = p_first;  // wrapped table index of plane p
+    if (P.wrap_x) {
+        pw %= P.Nx;
+        if (pw < 0) pw += P.Nx;
+    }
+    const double *srcq = src + (long long)(p_first - 3 + NG) * P1;  // row base of cell q = p - 3
+    double *destq = P.dest + (long long)(p_first - 3 + NG) * P1;
+    const double *Aq = P.A + (long long)(p_first - 3 + NG) * P1;
+    const double *Bq = P.B + (long long)(p_first - 3 + NG) * P1;
+    const bool use_sv = P.a_is_src | P.b_is_src;
 
-        const double avx_s = fma(P.cB, vy, evx) * P.mhvx;
-        const bool vxpos = fma(P.cB, vy, evx) > 0.0;
-
+    for (int blk = 0; blk < nplanes; blk += 7) {
 #pragma unroll
-        for (int cidx = 0; cidx < 2; ++cidx) {
-            double *acc = cidx ? acc1 : acc0;
-            const double *c = tile + (cidx ? off1 : off0);
-            const double s0 = c[0];
-            // x stencil contributions of s(p) to cells p-o (acc index 3-o)
-            const double t = ax_s[cidx] * s0;
-            if (xpos[cidx]) {
-                acc[6] = fma(-2.0, t, acc[6]);
-                acc[5] = fma(15.0, t, acc[5]);
-                acc[4] = fma(-60.0, t, acc[4]);
-                acc[3] = fma(20.0, t, acc[3]);
-                acc[2] = fma(30.0, t, acc[2]);
-                acc[1] = fma(-3.0, t, acc[1]);
-            } else {
-                acc[5] = fma(3.0, t, acc[5]);
-                acc[4] = fma(-30.0, t, acc[4]);
-                acc[3] = fma(-20.0, t, acc[3]);
-                acc[2] = fma(60.0, t, acc[2]);
-                acc[1] = fma(-15.0, t, acc[1]);
-                acc[0] = fma(2.0, t, acc[0]);
+        for (int r = 0; r < 7; ++r) {
+            const int n = blk + r;
+            if (n >= nplanes) break;
+            const int p = p_first + n;
+            if (tid == 0 && n + NSTAGE - 1 < nplanes) {
+                tma::fence_proxy_async();
+                issue_plane<TL>(tiles, bars, pm_core, pm_halo, n + NSTAGE - 1, p_first, P, l0, k0, cy_lo,
+                                cy_core, cy_hi);
             }
-            // x-coupled corrections through D(p), G(p) (cells p-1 and p+1)
-            const double D = c[-TL::L] - c[TL::L];
-            const double G = c[-1] - c[1];
-            acc[2] = fma(c1m, D, acc[2]);
-            acc[2] = fma(-c5m, G, acc[2]);
-            acc[4] = fma(-c1p, D, acc[4]);
-            acc[4] = fma(c5p, G, acc[4]);
+            const bool in_T = (p >= i0 && p < i1);
+            const bool has_m = (p - 1 >= i0 && p - 1 < i1);
+            const bool has_p = (p + 1 >= i0 && p + 1 < i1);
+            const int pwm = pw == 0 ? P.Nx - 1 : pw - 1;
+            const int pwp = pw == P.Nx - 1 ? 0 : pw + 1;
+            const int tm_ = P.wrap_x ? pwm : p - 1;
+            const int tp_ = P.wrap_x ? pwp : p + 1;
+            // tables (issued before the TMA wait so their latency overlaps it)
+            double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
             if (in_T) {
-                const double avy = fma(-P.cB, vx[cidx], evy);
-                double T = ay_s * wsum<TL::KL>(c, ypos);
-                T = fma(avx_s, wsum<TL::L>(c, vxpos), T);
-                T = fma(avy * P.mhvy, wsum<1>(c, avy > 0.0), T);
-                T = fma(c4, dsum<TL::KL, 1>(c), T);
-                T = fma(-P.c2, dsum<TL::L, 1>(c), T);
-                T = fma(-c3, dsum<TL::KL, TL::L>(c), T);
-                acc[3] += T;
+                const int e = pw * P.Ny + jj;
+                evx = __ldg(P.evx + e);
+                evy = __ldg(P.evy + e);
+                c3 = __ldg(P.c3 + e);
+                c4 = __ldg(P.c4 + e);
             }
-        }
+            if (has_m) {
+                const int e = tm_ * P.Ny + jj;
+                c1m = __ldg(P.c1 + e);
+                c5m = __ldg(P.c5 + e);
+            }
+            if (has_p) {
+                const int e = tp_ * P.Ny + jj;
+                c1p = __ldg(P.c1 + e);
+                c5p = __ldg(P.c5 + e);
+            }
+            // RK operands of the cell finalised at this plane (q = p - 3)
+            const int q = p - 3;
+            const bool fin = (q >= i0 && q < i1);
+            double rk0 = 0.0, rk1 = 0.0;
+            if (fin) {
+                double sv0 = 0.0, sv1 = 0.0;
+                if (use_sv) {
+                    sv0 = __ldg(srcq + g0);
+                    sv1 = __ldg(srcq + g1);
+                }
+                if (P.cd != 0.0) {
+                    rk0 = P.cd * destq[g0];
+                    rk1 = P.cd * destq[g1];
+                }
+                if (P.cb != 0.0) {
+                    rk0 = fma(P.cb, P.b_is_src ? sv0 : __ldg(Bq + g0), rk0);
+                    rk1 = fma(P.cb, P.b_is_src ? sv1 : __ldg(Bq + g1), rk1);
+                }
+                if (P.ca != 0.0) {
+                    rk0 = fma(P.ca, P.a_is_src ? sv0 : __ldg(Aq + g0), rk0);
+                    rk1 = fma(P.ca, P.a_is_src ? sv1 : __ldg(Aq + g1), rk1);
+                }
+            }
+            const int s = n % NSTAGE;
+            tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
+            const double *tile = tiles + s * TL::ELEMS;
 
-        // finalize cell q = p - 3
-        if (fin) {
+            const double avx0 = fma(P.cB, vy, evx);
+            const double avx_s = avx0 * P.mhvx;
+            const bool vxpos = avx0 > 0.0;
 #pragma unroll
             for (int cidx = 0; cidx < 2; ++cidx) {
-                const double rhs = cidx ? acc1[0] : acc0[0];
-                const long long g = (long long)(q + NG) * P1 + (cidx ? g1 : g0);
-                const double out = fma(cL, rhs, rk[cidx]);
-                P.dest[g] = out;
-                if (P.nonfinite && !isfinite(out)) {
-                    const unsigned long long flat =
-                        (((unsigned long long)q * P.Ny + jj) * P.Nvx + kk[cidx]) * P.Nvy + ll;
-                    atomicMin(P.nonfinite, flat);
+                double *acc = cidx ? acc1 : acc0;
+                const double *c = tile + (cidx ? off1 : off0);
+                // x-stencil contribution of s(p) to cell p - o: slot (r - o) mod 7
+                const double t = ax_s[cidx] * c[0];
+                if (xpos[cidx]) {
+                    acc[(r + 10) % 7] = fma(-2.0, t, acc[(r + 10) % 7]);
+                    acc[(r + 9) % 7] = fma(15.0, t, acc[(r + 9) % 7]);
+                    acc[(r + 8) % 7] = fma(-60.0, t, acc[(r + 8) % 7]);
+                    acc[r] = fma(20.0, t, acc[r]);
+                    acc[(r + 6) % 7] = fma(30.0, t, acc[(r + 6) % 7]);
+                    acc[(r + 5) % 7] = fma(-3.0, t, acc[(r + 5) % 7]);
+                } else {
+                    acc[(r + 9) % 7] = fma(3.0, t, acc[(r + 9) % 7]);
+                    acc[(r + 8) % 7] = fma(-30.0, t, acc[(r + 8) % 7]);
+                    acc[r] = fma(-20.0, t, acc[r]);
+                    acc[(r + 6) % 7] = fma(60.0, t, acc[(r + 6) % 7]);
+                    acc[(r + 5) % 7] = fma(-15.0, t, acc[(r + 5) % 7]);
+                    acc[(r + 4) % 7] = fma(2.0, t, acc[(r + 4) % 7]);
+                }
+                // x-coupled corrections through D(p), G(p) to cells p-1, p+1
+                const double D = c[-TL::L] - c[TL::L];
+                const double G = c[-1] - c[1];
+                acc[(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[(r + 6) % 7]));
+                acc[(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[(r + 1) % 7]));
+                if (in_T) {
+                    const double avy = fma(-P.cB, vx[cidx], evy);
+                    const double Ty = ay_s * wsum<TL::KL>(c, ypos);
+                    const double Tvx = avx_s * wsum<TL::L>(c, vxpos);
+                    const double Tvy = (avy * P.mhvy) * wsum<1>(c, avy > 0.0);
+                    const double Tc = fma(c4, dsum<TL::KL, 1>(c),
+                                          fma(-P.c2, dsum<TL::L, 1>(c), -c3 * dsum<TL::KL, TL::L>(c)));
+                    acc[r] += ((Ty + Tvx) + (Tvy + Tc));
+                }
+            }
+            // finalise cell q = p - 3 (slot (r + 4) % 7) and recycle the slot
+            if (fin) {
+                const double out0 = fma(cL, acc0[(r + 4) % 7], rk0);
+                const double out1 = fma(cL, acc1[(r + 4) % 7], rk1);
+                destq[g0] = out0;
+                destq[g1] = out1;
+                if (P.nonfinite && !(isfinite(out0) && isfinite(out1))) {
+                    const unsigned long long base = ((unsigned long long)q * P.Ny + jj) * P.Nvx;
+                    if (!isfinite(out0)) atomicMin(P.nonfinite, (base + kk[0]) * P.Nvy + ll);
+                    if (!isfinite(out1)) atomicMin(P.nonfinite, (base + kk[1]) * P.Nvy + ll);
                 }
                 if (P.partials) {
-                    const double sub = warp_tree_sum(out);
-                    if (lane == 0)
-                        P.partials[(((long long)q * P.Ny + jj) * P.Nvx + kk[cidx]) * nlt + lt] = sub;
+                    const double s0 = warp_tree_sum(out0);
+                    const double s1 = warp_tree_sum(out1);
+                    if (lane == 0) {
+                        const long long pb = ((long long)q * P.Ny + jj) * P.Nvx;
+                        P.partials[(pb + kk[0]) * nlt + lt] = s0;
+                        P.partials[(pb + kk[1]) * nlt + lt] = s1;
+                    }
                 }
             }
+            acc0[(r + 4) % 7] = 0.0;
+            acc1[(r + 4) % 7] = 0.0;
+            // advance the running state
+            pw = pwp;
+            srcq += P1;
+            destq += P1;
+            Aq += P1;
+            Bq += P1;
+            __syncthreads();  // everyone is done with stage s before it is refilled
         }
-#pragma unroll
-        for (int m = 0; m < 6; ++m) {
-            acc0[m] = acc0[m + 1];
-            acc1[m] = acc1[m + 1];
-        }
-        acc0[6] = acc1[6] = 0.0;
-        __syncthreads();  // everyone is done with stage s before it is refilled
     }
 }
 
