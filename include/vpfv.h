@@ -99,6 +99,10 @@ int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const 
                           unsigned long long *nonfinite, double *moment_partials,
                           int xsegments, void *stream);
 
+/* 1 when vpfv_stage_2d2v_fused would take the tiled path (and so accepts
+ * moment_partials) for these extents and flags, else 0. */
+int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
+
 /* The untiled one-thread-per-cell 2D-2V kernel (exact or fast), always. */
 int vpfv_stage_2d2v_generic(double *dest, const double *A, const double *B, const double *src,
                             double ca, double cb, double cd, double cL,

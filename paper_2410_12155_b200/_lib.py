@@ -46,6 +46,7 @@ SIGNATURES = {
     "vpfv_stage_2d2v_generic": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d, _p, _d] + [_p] * 3
                                 + [_d] * 4 + [_i] * 4 + [_u, _p, _d, _p, _p]),
     "vpfv_moment_partials": (_i, [_p, _p, _i, _i, _i, _d, _p]),
+    "vpfv_stage_2d2v_tiled_ok": (_i, [_i, _i, _i, _i, _u]),
     "vpfv_moment": (_i, [_p, _p, _i, _i, _p, _d, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
     "vpfv_poisson_1d": (_i, [_p, _p, _p, _i, _p, _p, _p, _p]),
@@ -96,7 +97,7 @@ def check_device(dev: int):
 
 # kernels launched per entry-point call (for launch accounting); default 1
 KERNELS_PER_CALL = {"vpfv_poisson_2d": 3, "vpfv_version": 0, "vpfv_check_device": 0,
-                    "vpfv_last_error": 0}
+                    "vpfv_last_error": 0, "vpfv_stage_2d2v_tiled_ok": 0}
 launch_counter = [0]
 
 

@@ -166,21 +166,21 @@ __device__ __forceinline__ void issue_plane(double *tiles, uint64_t *bars, const
     tma::load4d(dst + (3 + TL::BJ_) * TL::KL, pm_halo, &bars[s], l0, k0, cy_hi, cx);
 }
 
-template <int BJ, int BK, int BL, int NSTAGE>
-__global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
+template <int BJ, int BK, int BL, int NSTAGE, int CK>
+__global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     stage2d2v_tma_kernel(const __grid_constant__ CUtensorMap tm_core,
                          const __grid_constant__ CUtensorMap tm_halo,
                          const double *__restrict__ src, const Stage22 P) {
     using TL = Tile<BJ, BK, BL, NSTAGE>;
+    constexpr int L = TL::L, KL = TL::KL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *tiles = reinterpret_cast<double *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::BYTES);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // column block of this CTA
+    // column block of this CTA; x segment outermost so the CTAs resident at
+    // once cover neighbouring column blocks of the same x range
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
-    // x segment outermost: the CTAs resident at once cover neighbouring column
-    // blocks of the same x range, so their overlapping halos hit in L2
     const int ncols = nlt * nkt * njt;
     int b = blockIdx.x % ncols;
     const int seg = blockIdx.x / ncols;
@@ -193,14 +193,13 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    // thread -> cells (a, b0) and (a, b0 + BK/2), lane over l
-    const int a = warp / (BK / 2);
-    const int b0 = warp % (BK / 2);
+    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at lane's vy
+    const int a = warp / (BK / CK);
+    const int kb = (warp % (BK / CK)) * CK;
     const int jj = j0 + a;
-    const int kk[2] = {k0 + b0, k0 + b0 + BK / 2};
+    const int kfirst = k0 + kb;
     const int ll = l0 + lane;
 
-    // y-halo coordinates in padded storage
     int yl = j0 - 3, yh = j0 + BJ;
     if (P.wrap_y) {
         if (yl < 0) yl += P.Ny;
@@ -214,7 +213,7 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     }
     __syncthreads();
 
-    const int p_first = i0 - 3, p_last = i1 + 2;  // planes streamed
+    const int p_first = i0 - 3, p_last = i1 + 2;
     const int nplanes = p_last - p_first + 1;
     const CUtensorMap *pm_core = &tm_core;
     const CUtensorMap *pm_halo = &tm_halo;
@@ -224,42 +223,43 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
     }
 
     // per-thread constants
-    const double vx[2] = {__ldg(P.vxc + kk[0]), __ldg(P.vxc + kk[1])};
+    double ax_s[CK];
+    bool xpos[CK];
+    double bvx[CK];  // -cB * vx (for a_vy = evy - cB vx)
+#pragma unroll
+    for (int i = 0; i < CK; ++i) {
+        const double v = __ldg(P.vxc + kfirst + i);
+        ax_s[i] = v * P.mhx;
+        xpos[i] = v > 0.0;
+        bvx[i] = -P.cB * v;
+    }
     const double vy = __ldg(P.vyc + ll);
-    const double ay_s = vy * P.mhy;  // y speed times -1/(60 h_y)
+    const double ay_s = vy * P.mhy;
     const bool ypos = vy > 0.0;
-    const bool xpos[2] = {vx[0] > 0.0, vx[1] > 0.0};
-    const double ax_s[2] = {vx[0] * P.mhx, vx[1] * P.mhx};
+    const double cBvy = P.cB * vy;
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
+    const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
 
-    // smem offsets of this thread's cells inside a tile
-    const int off0 = ((a + 3) * TL::K + (b0 + 3)) * TL::L + (lane + 3);
-    const int off1 = off0 + (BK / 2) * TL::L;
+    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);  // first cell, in tile
 
-    // padded global offsets of the two cells at x-interior index 0
     const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
                     P1 = (long long)(P.Ny + 2 * NG) * P2;
-    const long long g0 = (long long)(jj + NG) * P2 + (long long)(kk[0] + NG) * P3 + (ll + NG);
-    const long long g1 = g0 + (long long)(BK / 2) * P3;
+    const long long g0 = (long long)(jj + NG) * P2 + (long long)(kfirst + NG) * P3 + (ll + NG);
 
-    // Accumulator ring: cell c = p_first + m lives in slot m % 7.  The plane
-    // loop is unrolled by 7 so every slot index is a compile-time constant
-    // (no register shuffling between planes).
-    double acc0[7], acc1[7];
+    double acc[CK][7];
 #pragma unroll
-    for (int m = 0; m < 7; ++m) acc0[m] = acc1[m] = 0.0;
+    for (int i = 0; i < CK; ++i)
+#pragma unroll
+        for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
 
-    // running plane state
-    int pw = p_first;  // wrapped table index of plane p
+    int pw = p_first;
     if (P.wrap_x) {
         pw %= P.Nx;
         if (pw < 0) pw += P.Nx;
     }
-    const double *srcq = src + (long long)(p_first - 3 + NG) * P1;  // row base of cell q = p - 3
-    double *destq = P.dest + (long long)(p_first - 3 + NG) * P1;
-    const double *Aq = P.A + (long long)(p_first - 3 + NG) * P1;
-    const double *Bq = P.B + (long long)(p_first - 3 + NG) * P1;
+    long long gq = (long long)(p_first - 3 + NG) * P1 + g0;  // cell q = p - 3, first k
     const bool use_sv = P.a_is_src | P.b_is_src;
+    const double ca = P.ca, cb = P.cb, cd = P.cd;
 
     for (int blk = 0; blk < nplanes; blk += 7) {
 #pragma unroll
@@ -277,9 +277,6 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
             const bool has_p = (p + 1 >= i0 && p + 1 < i1);
             const int pwm = pw == 0 ? P.Nx - 1 : pw - 1;
             const int pwp = pw == P.Nx - 1 ? 0 : pw + 1;
-            const int tm_ = P.wrap_x ? pwm : p - 1;
-            const int tp_ = P.wrap_x ? pwp : p + 1;
-            // tables (issued before the TMA wait so their latency overlaps it)
             double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
             if (in_T) {
                 const int e = pw * P.Ny + jj;
@@ -289,111 +286,137 @@ __global__ void __launch_bounds__(Tile<BJ, BK, BL, NSTAGE>::THREADS, 1)
                 c4 = __ldg(P.c4 + e);
             }
             if (has_m) {
-                const int e = tm_ * P.Ny + jj;
+                const int e = (P.wrap_x ? pwm : p - 1) * P.Ny + jj;
                 c1m = __ldg(P.c1 + e);
                 c5m = __ldg(P.c5 + e);
             }
             if (has_p) {
-                const int e = tp_ * P.Ny + jj;
+                const int e = (P.wrap_x ? pwp : p + 1) * P.Ny + jj;
                 c1p = __ldg(P.c1 + e);
                 c5p = __ldg(P.c5 + e);
             }
-            // RK operands of the cell finalised at this plane (q = p - 3)
+            // RK operands of the cells finalised at this plane (q = p - 3)
             const int q = p - 3;
             const bool fin = (q >= i0 && q < i1);
-            double rk0 = 0.0, rk1 = 0.0;
+            double rk[CK];
+#pragma unroll
+            for (int i = 0; i < CK; ++i) rk[i] = 0.0;
             if (fin) {
-                double sv0 = 0.0, sv1 = 0.0;
-                if (use_sv) {
-                    sv0 = __ldg(srcq + g0);
-                    sv1 = __ldg(srcq + g1);
-                }
-                if (P.cd != 0.0) {
-                    rk0 = P.cd * destq[g0];
-                    rk1 = P.cd * destq[g1];
-                }
-                if (P.cb != 0.0) {
-                    rk0 = fma(P.cb, P.b_is_src ? sv0 : __ldg(Bq + g0), rk0);
-                    rk1 = fma(P.cb, P.b_is_src ? sv1 : __ldg(Bq + g1), rk1);
-                }
-                if (P.ca != 0.0) {
-                    rk0 = fma(P.ca, P.a_is_src ? sv0 : __ldg(Aq + g0), rk0);
-                    rk1 = fma(P.ca, P.a_is_src ? sv1 : __ldg(Aq + g1), rk1);
+#pragma unroll
+                for (int i = 0; i < CK; ++i) {
+                    const long long g = gq + i * P3;
+                    const double sv = use_sv ? __ldg(src + g) : 0.0;
+                    double v = 0.0;
+                    if (cd != 0.0) v = cd * P.dest[g];
+                    if (cb != 0.0) v = fma(cb, P.b_is_src ? sv : __ldg(P.B + g), v);
+                    if (ca != 0.0) v = fma(ca, P.a_is_src ? sv : __ldg(P.A + g), v);
+                    rk[i] = v;
                 }
             }
             const int s = n % NSTAGE;
             tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
-            const double *tile = tiles + s * TL::ELEMS;
+            const double *c0 = tiles + s * TL::ELEMS + off;  // cell (a, kb, lane)
 
-            const double avx0 = fma(P.cB, vy, evx);
-            const double avx_s = avx0 * P.mhvx;
-            const bool vxpos = avx0 > 0.0;
+            // vx column at (j, l): k = kb-3 .. kb+CK+2
+            double col[CK + 6];
 #pragma unroll
-            for (int cidx = 0; cidx < 2; ++cidx) {
-                double *acc = cidx ? acc1 : acc0;
-                const double *c = tile + (cidx ? off1 : off0);
-                // x-stencil contribution of s(p) to cell p - o: slot (r - o) mod 7
-                const double t = ax_s[cidx] * c[0];
-                if (xpos[cidx]) {
-                    acc[(r + 10) % 7] = fma(-2.0, t, acc[(r + 10) % 7]);
-                    acc[(r + 9) % 7] = fma(15.0, t, acc[(r + 9) % 7]);
-                    acc[(r + 8) % 7] = fma(-60.0, t, acc[(r + 8) % 7]);
-                    acc[r] = fma(20.0, t, acc[r]);
-                    acc[(r + 6) % 7] = fma(30.0, t, acc[(r + 6) % 7]);
-                    acc[(r + 5) % 7] = fma(-3.0, t, acc[(r + 5) % 7]);
+            for (int m = 0; m < CK + 6; ++m) col[m] = c0[(m - 3) * L];
+
+            const double avx = evx + cBvy;
+            const double avx_s = avx * mhvx;
+            const bool vxpos = avx > 0.0;
+
+#pragma unroll
+            for (int i = 0; i < CK; ++i) {
+                const double *c = c0 + i * L;
+                // x-stencil contribution of s(p) to cells p - o: slot (r - o) mod 7
+                const double t = ax_s[i] * col[i + 3];
+                if (xpos[i]) {
+                    acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
+                    acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
+                    acc[i][(r + 8) % 7] = fma(-60.0, t, acc[i][(r + 8) % 7]);
+                    acc[i][r] = fma(20.0, t, acc[i][r]);
+                    acc[i][(r + 6) % 7] = fma(30.0, t, acc[i][(r + 6) % 7]);
+                    acc[i][(r + 5) % 7] = fma(-3.0, t, acc[i][(r + 5) % 7]);
                 } else {
-                    acc[(r + 9) % 7] = fma(3.0, t, acc[(r + 9) % 7]);
-                    acc[(r + 8) % 7] = fma(-30.0, t, acc[(r + 8) % 7]);
-                    acc[r] = fma(-20.0, t, acc[r]);
-                    acc[(r + 6) % 7] = fma(60.0, t, acc[(r + 6) % 7]);
-                    acc[(r + 5) % 7] = fma(-15.0, t, acc[(r + 5) % 7]);
-                    acc[(r + 4) % 7] = fma(2.0, t, acc[(r + 4) % 7]);
+                    acc[i][(r + 9) % 7] = fma(3.0, t, acc[i][(r + 9) % 7]);
+                    acc[i][(r + 8) % 7] = fma(-30.0, t, acc[i][(r + 8) % 7]);
+                    acc[i][r] = fma(-20.0, t, acc[i][r]);
+                    acc[i][(r + 6) % 7] = fma(60.0, t, acc[i][(r + 6) % 7]);
+                    acc[i][(r + 5) % 7] = fma(-15.0, t, acc[i][(r + 5) % 7]);
+                    acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
                 }
-                // x-coupled corrections through D(p), G(p) to cells p-1, p+1
-                const double D = c[-TL::L] - c[TL::L];
+                // x-coupled corrections: D(p) = s[k-1]-s[k+1], G(p) = s[l-1]-s[l+1]
+                const double D = col[i + 2] - col[i + 4];
                 const double G = c[-1] - c[1];
-                acc[(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[(r + 6) % 7]));
-                acc[(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[(r + 1) % 7]));
+                acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
+                acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
                 if (in_T) {
-                    const double avy = fma(-P.cB, vx[cidx], evy);
-                    const double Ty = ay_s * wsum<TL::KL>(c, ypos);
-                    const double Tvx = avx_s * wsum<TL::L>(c, vxpos);
-                    const double Tvy = (avy * P.mhvy) * wsum<1>(c, avy > 0.0);
-                    const double Tc = fma(c4, dsum<TL::KL, 1>(c),
-                                          fma(-P.c2, dsum<TL::L, 1>(c), -c3 * dsum<TL::KL, TL::L>(c)));
-                    acc[r] += ((Ty + Tvx) + (Tvy + Tc));
+                    // vx flux from the column, vy and y fluxes from the tile
+                    double wvx;
+                    if (vxpos)
+                        wvx = fma(-3.0, col[i + 5], fma(30.0, col[i + 4], fma(20.0, col[i + 3],
+                              fma(-60.0, col[i + 2], fma(15.0, col[i + 1], -2.0 * col[i])))));
+                    else
+                        wvx = fma(2.0, col[i + 6], fma(-15.0, col[i + 5], fma(60.0, col[i + 4],
+                              fma(-20.0, col[i + 3], fma(-30.0, col[i + 2], 3.0 * col[i + 1])))));
+                    const double avy = evy + bvx[i];
+                    double wvy;
+                    if (avy > 0.0)
+                        wvy = fma(-3.0, c[2], fma(30.0, c[1], fma(20.0, c[0], fma(-60.0, c[-1],
+                              fma(15.0, c[-2], -2.0 * c[-3])))));
+                    else
+                        wvy = fma(2.0, c[3], fma(-15.0, c[2], fma(60.0, c[1], fma(-20.0, c[0],
+                              fma(-30.0, c[-1], 3.0 * c[-2])))));
+                    double wy;
+                    if (ypos)
+                        wy = fma(-3.0, c[2 * KL], fma(30.0, c[KL], fma(20.0, c[0], fma(-60.0, c[-KL],
+                             fma(15.0, c[-2 * KL], -2.0 * c[-3 * KL])))));
+                    else
+                        wy = fma(2.0, c[3 * KL], fma(-15.0, c[2 * KL], fma(60.0, c[KL], fma(-20.0, c[0],
+                             fma(-30.0, c[-KL], 3.0 * c[-2 * KL])))));
+                    // (y,vy), (vx,vy), (y,vx) diagonals
+                    const double dyvy = ((c[KL - 1] + c[-KL + 1]) - c[KL + 1]) - c[-KL - 1];
+                    const double dvxvy = ((c[L - 1] + c[-L + 1]) - c[L + 1]) - c[-L - 1];
+                    const double dyvx = ((c[KL - L] + c[-KL + L]) - c[KL + L]) - c[-KL - L];
+                    double T = ay_s * wy;
+                    T = fma(avx_s, wvx, T);
+                    T = fma(avy * mhvy, wvy, T);
+                    T = fma(c4, dyvy, T);
+                    T = fma(mc2, dvxvy, T);
+                    T = fma(-c3, dyvx, T);
+                    acc[i][r] += T;
                 }
             }
-            // finalise cell q = p - 3 (slot (r + 4) % 7) and recycle the slot
+            // finalise cells q = p - 3 (slot (r + 4) % 7) and recycle the slot
             if (fin) {
-                const double out0 = fma(cL, acc0[(r + 4) % 7], rk0);
-                const double out1 = fma(cL, acc1[(r + 4) % 7], rk1);
-                destq[g0] = out0;
-                destq[g1] = out1;
-                if (P.nonfinite && !(isfinite(out0) && isfinite(out1))) {
-                    const unsigned long long base = ((unsigned long long)q * P.Ny + jj) * P.Nvx;
-                    if (!isfinite(out0)) atomicMin(P.nonfinite, (base + kk[0]) * P.Nvy + ll);
-                    if (!isfinite(out1)) atomicMin(P.nonfinite, (base + kk[1]) * P.Nvy + ll);
+                double out[CK];
+#pragma unroll
+                for (int i = 0; i < CK; ++i) {
+                    out[i] = fma(cL, acc[i][(r + 4) % 7], rk[i]);
+                    P.dest[gq + i * P3] = out[i];
+                }
+                if (P.nonfinite) {
+#pragma unroll
+                    for (int i = 0; i < CK; ++i)
+                        if (!isfinite(out[i]))
+                            atomicMin(P.nonfinite,
+                                      (((unsigned long long)q * P.Ny + jj) * P.Nvx + kfirst + i) * P.Nvy + ll);
                 }
                 if (P.partials) {
-                    const double s0 = warp_tree_sum(out0);
-                    const double s1 = warp_tree_sum(out1);
-                    if (lane == 0) {
-                        const long long pb = ((long long)q * P.Ny + jj) * P.Nvx;
-                        P.partials[(pb + kk[0]) * nlt + lt] = s0;
-                        P.partials[(pb + kk[1]) * nlt + lt] = s1;
+                    const long long pb = ((long long)q * P.Ny + jj) * P.Nvx + kfirst;
+#pragma unroll
+                    for (int i = 0; i < CK; ++i) {
+                        const double sub = warp_tree_sum(out[i]);
+                        if (lane == 0) P.partials[(pb + i) * nlt + lt] = sub;
                     }
                 }
             }
-            acc0[(r + 4) % 7] = 0.0;
-            acc1[(r + 4) % 7] = 0.0;
-            // advance the running state
+#pragma unroll
+            for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
             pw = pwp;
-            srcq += P1;
-            destq += P1;
-            Aq += P1;
-            Bq += P1;
-            __syncthreads();  // everyone is done with stage s before it is refilled
+            gq += P1;
+            __syncthreads();
         }
     }
 }
@@ -515,20 +538,52 @@ static bool get_map(const double *src, const int Npad[4] /* x,y,vx,vy */, const 
     return true;
 }
 
-constexpr int TBJ = 4, TBK = 8, TBL = 32, TNS = 3;
-using TileCfg = Tile<TBJ, TBK, TBL, TNS>;
+// Tile configurations: (BJ, NSTAGE, CK) with BK = 8, BL = 32.  Chosen at run
+// time (VPFV_TCFG=0/1/2 overrides; default 0).
+constexpr int TBK = 8, TBL = 32;
+struct TCfg {
+    int bj, ns, ck;
+};
+static const TCfg kCfgs[] = {{4, 3, 4}, {4, 3, 2}, {8, 3, 4}};
+
+static int tile_cfg() {
+    static int c = -1;
+    if (c < 0) {
+        const char *e = getenv("VPFV_TCFG");
+        c = e ? atoi(e) : 0;
+        if (c < 0 || c > 2) c = 0;
+    }
+    return c;
+}
 
 bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
+    const TCfg &c = kCfgs[tile_cfg()];
     if (flags & VPFV_EXACT) return false;
     if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
-    if (Ny % TBJ || Nvx % TBK || Nvy % TBL || (Nvy & 1)) return false;
-    if (Nx < 1 || Ny < 3 + TBJ) return false;
+    if (Ny % c.bj || Nvx % TBK || Nvy % TBL || (Nvy & 1)) return false;
+    if (Nx < 1 || Ny < 3 + c.bj) return false;
     return encode_fn() != nullptr;
 }
 
+template <int BJ, int NS, int CK>
+static int launch_cfg(const CUtensorMap &mc, const CUtensorMap &mh, const double *src, const Stage22 &P,
+                      cudaStream_t s) {
+    using TL = Tile<BJ, TBK, TBL, NS>;
+    auto kern = stage2d2v_tma_kernel<BJ, TBK, TBL, NS, CK>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM);
+        attr = true;
+    }
+    const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
+    kern<<<nblocks, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(mc, mh, src, P);
+    return check_launch("stage_2d2v_tma");
+}
+
 int launch_tma_2d2v(const double *src, Stage22 P, unsigned flags, int nseg, cudaStream_t s) {
+    const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
-    const int box_core[4] = {TBL + 8, TBK + 6, TBJ, 1};
+    const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
     const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
     CUtensorMap mc, mh;
     if (!get_map(src, Npad, box_core, &mc) || !get_map(src, Npad, box_halo, &mh))
@@ -539,16 +594,14 @@ int launch_tma_2d2v(const double *src, Stage22 P, unsigned flags, int nseg, cuda
     P.i1 = P.Nx;
     P.nseg = nseg < 1 ? 1 : nseg;
     P.seglen = (P.Nx + P.nseg - 1) / P.nseg;
-    static bool attr = false;
-    auto kern = stage2d2v_tma_kernel<TBJ, TBK, TBL, TNS>;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg::SMEM);
-        attr = true;
+    switch (tile_cfg()) {
+        case 1: return launch_cfg<4, 3, 2>(mc, mh, src, P, s);
+        case 2: return launch_cfg<8, 3, 4>(mc, mh, src, P, s);
+        default: return launch_cfg<4, 3, 4>(mc, mh, src, P, s);
     }
-    const int nblocks = (P.Ny / TBJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
-    kern<<<nblocks, TileCfg::THREADS, TileCfg::SMEM, s>>>(mc, mh, src, P);
-    return check_launch("stage_2d2v_tma");
 }
+
+int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / kCfgs[tile_cfg()].bj) * (Nvx / TBK) * (Nvy / TBL); }
 
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
                                 cudaStream_t s) {
@@ -634,7 +687,7 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
         // x segments of ~32 planes: a wave of resident CTAs then touches a
         // slab small enough for L2 to keep the halos its neighbours re-read;
         // and at least ~4 waves of work
-        const int cols = (Ny / TBJ) * (Nvx / TBK) * (Nvy / TBL);
+        const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
         nseg = Nx / 32;
         const int waves = (4 * 148 + cols - 1) / cols;
         if (nseg < waves) nseg = waves;
@@ -647,4 +700,8 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,
                                     double vol, void *stream) {
     return launch_moment_from_partials(partials, n, nphys, Nvx, nchunks, vol, (cudaStream_t)stream);
+}
+
+extern "C" int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
+    return tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) && Nvy / 32 <= 8 ? 1 : 0;
 }

@@ -88,8 +88,7 @@ class StageTables:
             return False
         if flags & (_lib.VPFV_WRAP(2) | _lib.VPFV_WRAP(3)):
             return False
-        N = g.N
-        return N[1] % 4 == 0 and N[1] >= 7 and N[2] % 8 == 0 and N[3] % 32 == 0 and N[3] // 32 <= 8
+        return bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*g.N, flags))
 
     def partials_shape(self):
         g = self.grid
