@@ -83,13 +83,12 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 struct Stage22 {
     double *dest;
-    const double *A, *B;
-    double ca, cb, cd, cL;
+    double cL;
     const double *dt_dev;
     double cL_div;
-    int a_is_src, b_is_src;
+    int nops;          // RK operands staged by TMA (A, B, dest as needed)
+    double opc[3];     // their coefficients
     unsigned long long *nonfinite;
-    // tables (T22 in stage.cu)
     const double *vxc, *vyc, *evx, *evy, *c1, *c3, *c4, *c5;
     double cB, c2, mhx, mhy, mhvx, mhvy;
     int Nx, Ny, Nvx, Nvy;
@@ -103,24 +102,23 @@ template <int BJ, int BK, int BL, int NSTAGE>
 struct Tile {
     static constexpr int J = BJ + 6, K = BK + 6, L = BL + 8;
     static constexpr int KL = K * L;
-    static constexpr int ELEMS = J * K * L;
-    static constexpr int BYTES = ELEMS * 8;
-    static constexpr int THREADS = BJ * (BK / 2) * BL;
-    static constexpr int SMEM = NSTAGE * BYTES + 64;
-    static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ;
+    static constexpr int ELEMS = J * K * L;              // src halo tile
+    static constexpr int OL = BL + 2;                     // operand row (16 B aligned start)
+    static constexpr int OELEMS = BJ * BK * OL;           // one RK operand core tile
+    static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS;
+    static constexpr int HALO_BYTES = ELEMS * 8, OP_BYTES = OELEMS * 8;
+    static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
+    static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ, BK_ = BK, BL_ = BL;
+    static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
 };
 
-// x stencil weights (face difference * 60), offsets o = -3..3
-__device__ __forceinline__ double wpos(int o) {
-    return o == -3 ? -2.0 : o == -2 ? 15.0 : o == -1 ? -60.0 : o == 0 ? 20.0 : o == 1 ? 30.0 : o == 2 ? -3.0 : 0.0;
-}
-__device__ __forceinline__ double wneg(int o) {
-    return o == -3 ? 0.0 : o == -2 ? 3.0 : o == -1 ? -30.0 : o == 0 ? -20.0 : o == 1 ? 60.0 : o == 2 ? -15.0 : 2.0;
-}
+struct Maps {
+    CUtensorMap core, halo, op[3];
+};
 
-// upwinded 6-point weighted sum (face difference * 60) along one in-tile
-// direction of stride ST; the sign test is warp-uniform in practice, and the
-// sum is evaluated as three independent pairs for ILP.
+// upwinded 6-point weighted sum (face difference * 60) along an in-tile
+// direction of stride ST, evaluated as three independent pairs (ILP); the
+// sign test is warp-uniform in practice.
 template <int ST>
 __device__ __forceinline__ double wsum(const double *c, bool pos) {
     if (pos) {
@@ -136,9 +134,8 @@ __device__ __forceinline__ double wsum(const double *c, bool pos) {
 }
 
 template <int SA, int SB>
-__device__ __forceinline__ double dsum(const double *c) {
-    // s[+a,-b] + s[-a,+b] - s[+a,+b] - s[-a,-b]
-    return ((c[SA - SB] + c[-SA + SB]) - c[SA + SB]) - c[-SA - SB];
+__device__ __forceinline__ double dsum(const double *c) {  // s[+a,-b]+s[-a,+b]-s[+a,+b]-s[-a,-b]
+    return (c[SA - SB] + c[-SA + SB]) - (c[SA + SB] + c[-SA - SB]);
 }
 
 __device__ __forceinline__ double warp_tree_sum(double x) {
@@ -146,40 +143,46 @@ __device__ __forceinline__ double warp_tree_sum(double x) {
     return x;
 }
 
+// Plane n: the src halo tile of plane p = p_first + n, and the RK operand core
+// tiles of cell-plane q = p - 3 when q is updated by this CTA.
 template <class TL>
-__device__ __forceinline__ void issue_plane(double *tiles, uint64_t *bars, const CUtensorMap *pm_core,
-                                            const CUtensorMap *pm_halo, int n, int p_first,
-                                            const Stage22 &P, int l0, int k0, int cy_lo, int cy_core,
-                                            int cy_hi) {
-    constexpr int NS = TL::NSTAGE_;
-    const int s = n % NS;
-    double *dst = tiles + s * TL::ELEMS;
-    int p = p_first + n;
+__device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, const Maps *M, int n,
+                                            int p_first, int i0, int i1, const Stage22 &P, int l0,
+                                            int k0, int j0, int cy_lo, int cy_core, int cy_hi) {
+    const int s = n % TL::NSTAGE_;
+    double *dst = stages + s * TL::STAGE_ELEMS;
+    const int p = p_first + n;
+    int px = p;
     if (P.wrap_x) {
-        p %= P.Nx;
-        if (p < 0) p += P.Nx;
+        px %= P.Nx;
+        if (px < 0) px += P.Nx;
     }
-    const int cx = p + NG;
-    tma::mbar_expect_tx(&bars[s], TL::BYTES);
-    tma::load4d(dst, pm_halo, &bars[s], l0, k0, cy_lo, cx);
-    tma::load4d(dst + 3 * TL::KL, pm_core, &bars[s], l0, k0, cy_core, cx);
-    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, pm_halo, &bars[s], l0, k0, cy_hi, cx);
+    const int q = p - 3;
+    const bool ops = (q >= i0 && q < i1);
+    tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
+    const int cx = px + NG;
+    tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
+    tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx);
+    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
+    if (ops) {
+        for (int o = 0; o < P.nops; ++o)
+            tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
+                        q + NG);
+    }
 }
 
 template <int BJ, int BK, int BL, int NSTAGE, int CK>
 __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
-    stage2d2v_tma_kernel(const __grid_constant__ CUtensorMap tm_core,
-                         const __grid_constant__ CUtensorMap tm_halo,
-                         const double *__restrict__ src, const Stage22 P) {
+    stage2d2v_tma_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using TL = Tile<BJ, BK, BL, NSTAGE>;
     constexpr int L = TL::L, KL = TL::KL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *tiles = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::BYTES);
+    double *stages = reinterpret_cast<double *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::STAGE_ELEMS * 8);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // column block of this CTA; x segment outermost so the CTAs resident at
-    // once cover neighbouring column blocks of the same x range
+    // column block; x segment outermost so the CTAs resident at once cover
+    // neighbouring column blocks of the same x range (halo reuse in L2)
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
     const int ncols = nlt * nkt * njt;
     int b = blockIdx.x % ncols;
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at lane's vy
+    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at the lane's vy
     const int a = warp / (BK / CK);
     const int kb = (warp % (BK / CK)) * CK;
     const int jj = j0 + a;
@@ -215,17 +218,14 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
 
     const int p_first = i0 - 3, p_last = i1 + 2;
     const int nplanes = p_last - p_first + 1;
-    const CUtensorMap *pm_core = &tm_core;
-    const CUtensorMap *pm_halo = &tm_halo;
+    const Maps *M = &maps;
     if (tid == 0) {
         for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
-            issue_plane<TL>(tiles, bars, pm_core, pm_halo, n, p_first, P, l0, k0, cy_lo, cy_core, cy_hi);
+            issue_plane<TL>(stages, bars, M, n, p_first, i0, i1, P, l0, k0, j0, cy_lo, cy_core, cy_hi);
     }
 
-    // per-thread constants
-    double ax_s[CK];
+    double ax_s[CK], bvx[CK];
     bool xpos[CK];
-    double bvx[CK];  // -cB * vx (for a_vy = evy - cB vx)
 #pragma unroll
     for (int i = 0; i < CK; ++i) {
         const double v = __ldg(P.vxc + kfirst + i);
@@ -239,12 +239,16 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     const double cBvy = P.cB * vy;
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
     const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
+    const int nops = P.nops;
+    const double oc0 = P.opc[0], oc1 = P.opc[1], oc2 = P.opc[2];
 
-    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);  // first cell, in tile
+    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);   // first cell in the halo tile
+    const int ooff = TL::ELEMS + (a * BK + kb) * TL::OL + lane + 1;  // first cell in operand tile 0
 
     const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
                     P1 = (long long)(P.Ny + 2 * NG) * P2;
-    const long long g0 = (long long)(jj + NG) * P2 + (long long)(kfirst + NG) * P3 + (ll + NG);
+    long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(jj + NG) * P2 +
+                   (long long)(kfirst + NG) * P3 + (ll + NG);  // cell q = p - 3
 
     double acc[CK][7];
 #pragma unroll
@@ -252,15 +256,14 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
 #pragma unroll
         for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
 
-    int pw = p_first;
+    int pw = p_first;  // wrapped table row of plane p
     if (P.wrap_x) {
         pw %= P.Nx;
         if (pw < 0) pw += P.Nx;
     }
-    long long gq = (long long)(p_first - 3 + NG) * P1 + g0;  // cell q = p - 3, first k
-    const bool use_sv = P.a_is_src | P.b_is_src;
-    const double ca = P.ca, cb = P.cb, cd = P.cd;
 
+    // Accumulator ring: cell c = p_first + m lives in slot m % 7; the plane
+    // loop is unrolled by 7 so every slot index is a compile-time constant.
     for (int blk = 0; blk < nplanes; blk += 7) {
 #pragma unroll
         for (int r = 0; r < 7; ++r) {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             const int p = p_first + n;
             if (tid == 0 && n + NSTAGE - 1 < nplanes) {
                 tma::fence_proxy_async();
-                issue_plane<TL>(tiles, bars, pm_core, pm_halo, n + NSTAGE - 1, p_first, P, l0, k0, cy_lo,
+                issue_plane<TL>(stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
                                 cy_core, cy_hi);
             }
             const bool in_T = (p >= i0 && p < i1);
@@ -295,42 +298,19 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                 c1p = __ldg(P.c1 + e);
                 c5p = __ldg(P.c5 + e);
             }
-            // RK operands of the cells finalised at this plane (q = p - 3)
-            const int q = p - 3;
-            const bool fin = (q >= i0 && q < i1);
-            double rk[CK];
-#pragma unroll
-            for (int i = 0; i < CK; ++i) rk[i] = 0.0;
-            if (fin) {
-#pragma unroll
-                for (int i = 0; i < CK; ++i) {
-                    const long long g = gq + i * P3;
-                    const double sv = use_sv ? __ldg(src + g) : 0.0;
-                    double v = 0.0;
-                    if (cd != 0.0) v = cd * P.dest[g];
-                    if (cb != 0.0) v = fma(cb, P.b_is_src ? sv : __ldg(P.B + g), v);
-                    if (ca != 0.0) v = fma(ca, P.a_is_src ? sv : __ldg(P.A + g), v);
-                    rk[i] = v;
-                }
-            }
             const int s = n % NSTAGE;
             tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
-            const double *c0 = tiles + s * TL::ELEMS + off;  // cell (a, kb, lane)
-
-            // vx column at (j, l): k = kb-3 .. kb+CK+2
-            double col[CK + 6];
-#pragma unroll
-            for (int m = 0; m < CK + 6; ++m) col[m] = c0[(m - 3) * L];
+            const double *stage = stages + s * TL::STAGE_ELEMS;
+            const double *c0 = stage + off;
 
             const double avx = evx + cBvy;
             const double avx_s = avx * mhvx;
             const bool vxpos = avx > 0.0;
-
 #pragma unroll
             for (int i = 0; i < CK; ++i) {
                 const double *c = c0 + i * L;
                 // x-stencil contribution of s(p) to cells p - o: slot (r - o) mod 7
-                const double t = ax_s[i] * col[i + 3];
+                const double t = ax_s[i] * c[0];
                 if (xpos[i]) {
                     acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
                     acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
@@ -347,53 +327,30 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                     acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
                 }
                 // x-coupled corrections: D(p) = s[k-1]-s[k+1], G(p) = s[l-1]-s[l+1]
-                const double D = col[i + 2] - col[i + 4];
+                const double D = c[-L] - c[L];
                 const double G = c[-1] - c[1];
                 acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
                 acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
                 if (in_T) {
-                    // vx flux from the column, vy and y fluxes from the tile
-                    double wvx;
-                    if (vxpos)
-                        wvx = fma(-3.0, col[i + 5], fma(30.0, col[i + 4], fma(20.0, col[i + 3],
-                              fma(-60.0, col[i + 2], fma(15.0, col[i + 1], -2.0 * col[i])))));
-                    else
-                        wvx = fma(2.0, col[i + 6], fma(-15.0, col[i + 5], fma(60.0, col[i + 4],
-                              fma(-20.0, col[i + 3], fma(-30.0, col[i + 2], 3.0 * col[i + 1])))));
                     const double avy = evy + bvx[i];
-                    double wvy;
-                    if (avy > 0.0)
-                        wvy = fma(-3.0, c[2], fma(30.0, c[1], fma(20.0, c[0], fma(-60.0, c[-1],
-                              fma(15.0, c[-2], -2.0 * c[-3])))));
-                    else
-                        wvy = fma(2.0, c[3], fma(-15.0, c[2], fma(60.0, c[1], fma(-20.0, c[0],
-                              fma(-30.0, c[-1], 3.0 * c[-2])))));
-                    double wy;
-                    if (ypos)
-                        wy = fma(-3.0, c[2 * KL], fma(30.0, c[KL], fma(20.0, c[0], fma(-60.0, c[-KL],
-                             fma(15.0, c[-2 * KL], -2.0 * c[-3 * KL])))));
-                    else
-                        wy = fma(2.0, c[3 * KL], fma(-15.0, c[2 * KL], fma(60.0, c[KL], fma(-20.0, c[0],
-                             fma(-30.0, c[-KL], 3.0 * c[-2 * KL])))));
-                    // (y,vy), (vx,vy), (y,vx) diagonals
-                    const double dyvy = ((c[KL - 1] + c[-KL + 1]) - c[KL + 1]) - c[-KL - 1];
-                    const double dvxvy = ((c[L - 1] + c[-L + 1]) - c[L + 1]) - c[-L - 1];
-                    const double dyvx = ((c[KL - L] + c[-KL + L]) - c[KL + L]) - c[-KL - L];
-                    double T = ay_s * wy;
-                    T = fma(avx_s, wvx, T);
-                    T = fma(avy * mhvy, wvy, T);
-                    T = fma(c4, dyvy, T);
-                    T = fma(mc2, dvxvy, T);
-                    T = fma(-c3, dyvx, T);
-                    acc[i][r] += T;
+                    const double Ty = ay_s * wsum<KL>(c, ypos);
+                    const double Tvx = avx_s * wsum<L>(c, vxpos);
+                    const double Tvy = (avy * mhvy) * wsum<1>(c, avy > 0.0);
+                    const double Tc = fma(c4, dsum<KL, 1>(c), fma(mc2, dsum<L, 1>(c), -c3 * dsum<KL, L>(c)));
+                    acc[i][r] += (Ty + Tvx) + (Tvy + Tc);
                 }
             }
-            // finalise cells q = p - 3 (slot (r + 4) % 7) and recycle the slot
-            if (fin) {
+            // finalise cells q = p - 3 (slot (r + 4) % 7) from the staged RK operands
+            const int q = p - 3;
+            if (q >= i0 && q < i1) {
+                const double *op = stage + ooff;
                 double out[CK];
 #pragma unroll
                 for (int i = 0; i < CK; ++i) {
-                    out[i] = fma(cL, acc[i][(r + 4) % 7], rk[i]);
+                    double rk = oc0 * op[i * TL::OL];
+                    if (nops > 1) rk = fma(oc1, op[TL::OELEMS + i * TL::OL], rk);
+                    if (nops > 2) rk = fma(oc2, op[2 * TL::OELEMS + i * TL::OL], rk);
+                    out[i] = fma(cL, acc[i][(r + 4) % 7], rk);
                     P.dest[gq + i * P3] = out[i];
                 }
                 if (P.nonfinite) {
@@ -416,7 +373,7 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
             pw = pwp;
             gq += P1;
-            __syncthreads();
+            __syncthreads();  // stage s is free for the next refill
         }
     }
 }
@@ -539,12 +496,12 @@ static bool get_map(const double *src, const int Npad[4] /* x,y,vx,vy */, const 
 }
 
 // Tile configurations: (BJ, NSTAGE, CK) with BK = 8, BL = 32.  Chosen at run
-// time (VPFV_TCFG=0/1/2 overrides; default 0).
+// time (VPFV_TCFG overrides; default 0).
 constexpr int TBK = 8, TBL = 32;
 struct TCfg {
     int bj, ns, ck;
 };
-static const TCfg kCfgs[] = {{4, 3, 4}, {4, 3, 2}, {8, 3, 4}};
+static const TCfg kCfgs[] = {{4, 3, 2}, {4, 3, 4}, {4, 2, 2}};
 
 static int tile_cfg() {
     static int c = -1;
@@ -565,9 +522,10 @@ bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
     return encode_fn() != nullptr;
 }
 
+int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / kCfgs[tile_cfg()].bj) * (Nvx / TBK) * (Nvy / TBL); }
+
 template <int BJ, int NS, int CK>
-static int launch_cfg(const CUtensorMap &mc, const CUtensorMap &mh, const double *src, const Stage22 &P,
-                      cudaStream_t s) {
+static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
     using TL = Tile<BJ, TBK, TBL, NS>;
     auto kern = stage2d2v_tma_kernel<BJ, TBK, TBL, NS, CK>;
     static bool attr = false;
@@ -576,18 +534,24 @@ static int launch_cfg(const CUtensorMap &mc, const CUtensorMap &mh, const double
         attr = true;
     }
     const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
-    kern<<<nblocks, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(mc, mh, src, P);
+    kern<<<nblocks, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
 }
 
-int launch_tma_2d2v(const double *src, Stage22 P, unsigned flags, int nseg, cudaStream_t s) {
+// ops: up to three (coefficient, array) RK operands, already de-duplicated
+int launch_tma_2d2v(const double *src, const double *const ops[3], Stage22 P, unsigned flags, int nseg,
+                    cudaStream_t s) {
     const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
     const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
     const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
-    CUtensorMap mc, mh;
-    if (!get_map(src, Npad, box_core, &mc) || !get_map(src, Npad, box_halo, &mh))
+    const int box_op[4] = {TBL + 2, TBK, c.bj, 1};
+    Maps maps;
+    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_halo, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
+    for (int o = 0; o < P.nops; ++o)
+        if (!get_map(ops[o], Npad, box_op, &maps.op[o])) return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
+    for (int o = P.nops; o < 3; ++o) maps.op[o] = maps.core;
     P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
     P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
     P.i0 = 0;
@@ -595,13 +559,11 @@ int launch_tma_2d2v(const double *src, Stage22 P, unsigned flags, int nseg, cuda
     P.nseg = nseg < 1 ? 1 : nseg;
     P.seglen = (P.Nx + P.nseg - 1) / P.nseg;
     switch (tile_cfg()) {
-        case 1: return launch_cfg<4, 3, 2>(mc, mh, src, P, s);
-        case 2: return launch_cfg<8, 3, 4>(mc, mh, src, P, s);
-        default: return launch_cfg<4, 3, 4>(mc, mh, src, P, s);
+        case 1: return launch_cfg<4, 3, 4>(maps, P, s);
+        case 2: return launch_cfg<4, 2, 2>(maps, P, s);
+        default: return launch_cfg<4, 3, 2>(maps, P, s);
     }
 }
-
-int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / kCfgs[tile_cfg()].bj) * (Nvx / TBK) * (Nvy / TBL); }
 
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
                                 cudaStream_t s) {
@@ -646,16 +608,29 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
     }
     Stage22 P{};
     P.dest = dest;
-    P.A = A;
-    P.B = B;
-    P.ca = ca;
-    P.cb = cb;
-    P.cd = cd;
     P.cL = cL;
     P.dt_dev = dt_dev;
     P.cL_div = cL_div;
-    P.a_is_src = (A == src);
-    P.b_is_src = (B == src);
+    // RK operands: ca*A + cb*B + cd*dest, merging B into A when they alias
+    const double *ops[3] = {nullptr, nullptr, nullptr};
+    int nops = 0;
+    if (ca != 0.0 || (cb != 0.0 && B == A)) {
+        ops[nops] = A;
+        P.opc[nops++] = (B == A) ? ca + cb : ca;
+    }
+    if (cb != 0.0 && B != A) {
+        ops[nops] = B;
+        P.opc[nops++] = cb;
+    }
+    if (cd != 0.0) {
+        ops[nops] = dest;
+        P.opc[nops++] = cd;
+    }
+    if (nops == 0) {  // pure RHS: one zero-weighted operand keeps the code path uniform
+        ops[nops] = src;
+        P.opc[nops++] = 0.0;
+    }
+    P.nops = nops;
     P.nonfinite = nonfinite;
     P.vxc = vxc;
     P.vyc = vyc;
@@ -683,18 +658,13 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
         env_seg = e ? atoi(e) : 0;
     }
     if (nseg <= 0 && env_seg > 0) nseg = env_seg;
-    if (nseg <= 0) {
-        // x segments of ~32 planes: a wave of resident CTAs then touches a
-        // slab small enough for L2 to keep the halos its neighbours re-read;
-        // and at least ~4 waves of work
+    if (nseg <= 0) {  // at least ~4 waves of one CTA per SM, segments >= 8 planes
         const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
-        nseg = Nx / 32;
-        const int waves = (4 * 148 + cols - 1) / cols;
-        if (nseg < waves) nseg = waves;
+        nseg = (4 * 148 + cols - 1) / cols;
         if (nseg > Nx / 8) nseg = Nx / 8;
         if (nseg < 1) nseg = 1;
     }
-    return launch_tma_2d2v(src, P, flags, nseg, (cudaStream_t)stream);
+    return launch_tma_2d2v(src, ops, P, flags, nseg, (cudaStream_t)stream);
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,
