@@ -86,8 +86,10 @@ int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double
  * (finish with vpfv_moment_partials).  Runs the TMA-tiled x-marching kernel
  * (requires the fast path, stored velocity ghosts, Ny%4 == Nvx%8 == Nvy%32
  * == 0); otherwise falls back to the generic kernel (and rejects a non-NULL
- * moment_partials with VPFV_EARG).  xsegments <= 0 picks a split of the x
- * march automatically.  vpfv_stage_2d2v == this with moment_partials NULL. */
+ * moment_partials with VPFV_EARG).  The tiled path reads the E tables from
+ * packed_tables (vpfv_tables_2d_packed); with packed_tables NULL the generic
+ * kernel runs.  xsegments <= 0 picks a split of the x march automatically.
+ * vpfv_stage_2d2v == this with packed_tables and moment_partials NULL. */
 int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const double *src,
                           double ca, double cb, double cd, double cL,
                           const double *vxc, const double *vyc, const double *evx,
@@ -96,8 +98,8 @@ int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const 
                           double hx, double hy, double hvx, double hvy,
                           int Nx, int Ny, int Nvx, int Nvy,
                           unsigned flags, const double *dt_dev, double cL_div,
-                          unsigned long long *nonfinite, double *moment_partials,
-                          int xsegments, void *stream);
+                          unsigned long long *nonfinite, const double *packed_tables,
+                          double *moment_partials, int xsegments, void *stream);
 
 /* 1 when vpfv_stage_2d2v_fused would take the tiled path (and so accepts
  * moment_partials) for these extents and flags, else 0. */
@@ -157,6 +159,13 @@ int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, double *evy,
                    double *c1, double *c3, double *c4, double *c5, int Nx, int Ny,
                    double qmk2, double nqmk2, double gx, double gy,
                    double t1, double t4, double denx, double deny, void *stream);
+
+/* The same 2D tables packed for the tiled kernel: packed[(Nx+2)][Ny][8] =
+ * (evx, evy, c1, c3, c4, c5, 0, 0) with x rows shifted by one and periodic
+ * ghost rows 0 (= x Nx-1) and Nx+1 (= x 0). */
+int vpfv_tables_2d_packed(const double *Ex, const double *Ey, double *packed, int Nx, int Ny,
+                          double qmk2, double nqmk2, double gx, double gy,
+                          double t1, double t4, double denx, double deny, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Ghost fill of the periodic dims named in dims_mask (bit k = dim k), whole

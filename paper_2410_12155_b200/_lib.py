@@ -42,7 +42,7 @@ SIGNATURES = {
     "vpfv_stage_2d2v": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d, _p, _d] + [_p] * 3 + [_d] * 4
                         + [_i] * 4 + [_u, _p, _d, _p, _p]),
     "vpfv_stage_2d2v_fused": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d, _p, _d] + [_p] * 3
-                              + [_d] * 4 + [_i] * 4 + [_u, _p, _d, _p, _p, _i, _p]),
+                              + [_d] * 4 + [_i] * 4 + [_u, _p, _d, _p, _p, _p, _i, _p]),
     "vpfv_stage_2d2v_generic": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d, _p, _d] + [_p] * 3
                                 + [_d] * 4 + [_i] * 4 + [_u, _p, _d, _p, _p]),
     "vpfv_moment_partials": (_i, [_p, _p, _i, _i, _i, _d, _p]),
@@ -53,6 +53,7 @@ SIGNATURES = {
     "vpfv_poisson_2d": (_i, [_p] * 4 + [_i, _i] + [_p] * 7 + [_p]),
     "vpfv_tables_1d": (_i, [_p, _p, _p, _i, _d, _d, _d, _d, _p]),
     "vpfv_tables_2d": (_i, [_p] * 8 + [_i, _i] + [_d] * 8 + [_p]),
+    "vpfv_tables_2d_packed": (_i, [_p] * 3 + [_i, _i] + [_d] * 8 + [_p]),
     "vpfv_wrap_fill": (_i, [_p, _i, _p, _u, _p]),
     "vpfv_box_copy": (_i, [_p, _p, _p, _p, _p, _p, _i, _p, _p]),
     "vpfv_version": (_i, []),

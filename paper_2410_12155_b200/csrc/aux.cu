@@ -60,6 +60,31 @@ __global__ void tables2d_kernel(const double *__restrict__ Ex, const double *__r
     c5[p] = __ddiv_rn(__dmul_rn(nqmk2, dEy_x), deny);
 }
 
+// packed layout for the tiled 2D-2V kernel: tab[(Nx+2)][Ny][8] =
+// (evx, evy, c1, c3, c4, c5, 0, 0), x rows shifted by one with periodic ghost
+// rows 0 and Nx+1, so one TMA box brings planes p-1, p, p+1.
+__global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const double *__restrict__ Ey,
+                                       double *__restrict__ tab, int nx, int ny, double qmk2,
+                                       double nqmk2, double gx, double gy, double t1, double t4,
+                                       double denx, double deny) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (nx + 2) * ny) return;
+    const int row = t / ny, j = t - row * ny;
+    const int i = row == 0 ? nx - 1 : (row == nx + 1 ? 0 : row - 1);
+    const int p = i * ny + j;
+    const int ip = (i + 1 < nx ? i + 1 : 0) * ny + j, im = (i > 0 ? i - 1 : nx - 1) * ny + j;
+    const int jp = i * ny + (j + 1 < ny ? j + 1 : 0), jm = i * ny + (j > 0 ? j - 1 : ny - 1);
+    double *o = tab + (size_t)t * 8;
+    o[0] = __dadd_rn(__dmul_rn(qmk2, Ex[p]), gx);
+    o[1] = __dadd_rn(__dmul_rn(qmk2, Ey[p]), gy);
+    o[2] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ex[ip], Ex[im])), denx));
+    o[3] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ex[jp], Ex[jm])), denx);
+    o[4] = __dadd_rn(t4, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ey[jp], Ey[jm])), deny));
+    o[5] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ey[ip], Ey[im])), deny);
+    o[6] = 0.0;
+    o[7] = 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // charge density: rho = sum_s q_s n_s - mean (one CTA, fixed-order sums)
 
@@ -139,6 +164,15 @@ extern "C" int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, d
     tables2d_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
         Ex, Ey, evx, evy, c1, c3, c4, c5, Nx, Ny, qmk2, nqmk2, gx, gy, t1, t4, denx, deny);
     return check_launch("tables_2d");
+}
+
+extern "C" int vpfv_tables_2d_packed(const double *Ex, const double *Ey, double *packed, int Nx, int Ny,
+                                     double qmk2, double nqmk2, double gx, double gy, double t1,
+                                     double t4, double denx, double deny, void *stream) {
+    int n = (Nx + 2) * Ny;
+    tables2d_packed_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        Ex, Ey, packed, Nx, Ny, qmk2, nqmk2, gx, gy, t1, t4, denx, deny);
+    return check_launch("tables_2d_packed");
 }
 
 extern "C" int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,

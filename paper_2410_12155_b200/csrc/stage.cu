@@ -335,8 +335,8 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
                                      const double *c3, const double *c4, const double *c5, double hx,
                                      double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
                                      int Nvy, unsigned flags, const double *dt_dev, double cL_div,
-                                     unsigned long long *nonfinite, double *moment_partials,
-                                     int xsegments, void *stream);
+                                     unsigned long long *nonfinite, const double *packed_tables,
+                                     double *moment_partials, int xsegments, void *stream);
 
 extern "C" int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double *src,
                                double ca, double cb, double cd, double cL, const double *vxc,
@@ -348,7 +348,7 @@ extern "C" int vpfv_stage_2d2v(double *dest, const double *A, const double *B, c
                                unsigned long long *nonfinite, void *stream) {
     return vpfv_stage_2d2v_fused(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3,
                                  c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev, cL_div,
-                                 nonfinite, nullptr, 0, stream);
+                                 nonfinite, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int vpfv_stage_2d2v_generic(double *dest, const double *A, const double *B,

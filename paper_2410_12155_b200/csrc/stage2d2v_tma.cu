@@ -75,6 +75,15 @@ __device__ __forceinline__ void load4d(void *dst, const CUtensorMap *map, uint64
         : "memory");
 }
 
+__device__ __forceinline__ void load3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                       int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -105,7 +114,9 @@ struct Tile {
     static constexpr int ELEMS = J * K * L;              // src halo tile
     static constexpr int OL = BL + 2;                     // operand row (16 B aligned start)
     static constexpr int OELEMS = BJ * BK * OL;           // one RK operand core tile
-    static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS;
+    static constexpr int TELEMS = 3 * BJ * 8;              // packed E tables, planes p-1..p+1
+    static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS + TELEMS;
+    static constexpr int TAB_BYTES = TELEMS * 8;
     static constexpr int HALO_BYTES = ELEMS * 8, OP_BYTES = OELEMS * 8;
     static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
     static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ, BK_ = BK, BL_ = BL;
@@ -113,7 +124,7 @@ struct Tile {
 };
 
 struct Maps {
-    CUtensorMap core, halo, op[3];
+    CUtensorMap core, halo, op[3], tab;
 };
 
 // upwinded 6-point weighted sum (face difference * 60) along an in-tile
@@ -159,8 +170,10 @@ __device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, cons
     }
     const int q = p - 3;
     const bool ops = (q >= i0 && q < i1);
-    tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
+    tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + TL::TAB_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
     const int cx = px + NG;
+    // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
+    tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
     tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
     tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx);
     tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
@@ -256,12 +269,6 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
 #pragma unroll
         for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
 
-    int pw = p_first;  // wrapped table row of plane p
-    if (P.wrap_x) {
-        pw %= P.Nx;
-        if (pw < 0) pw += P.Nx;
-    }
-
     // Accumulator ring: cell c = p_first + m lives in slot m % 7; the plane
     // loop is unrolled by 7 so every slot index is a compile-time constant.
     for (int blk = 0; blk < nplanes; blk += 7) {
@@ -278,30 +285,15 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             const bool in_T = (p >= i0 && p < i1);
             const bool has_m = (p - 1 >= i0 && p - 1 < i1);
             const bool has_p = (p + 1 >= i0 && p + 1 < i1);
-            const int pwm = pw == 0 ? P.Nx - 1 : pw - 1;
-            const int pwp = pw == P.Nx - 1 ? 0 : pw + 1;
-            double evx = 0, evy = 0, c3 = 0, c4 = 0, c1m = 0, c1p = 0, c5m = 0, c5p = 0;
-            if (in_T) {
-                const int e = pw * P.Ny + jj;
-                evx = __ldg(P.evx + e);
-                evy = __ldg(P.evy + e);
-                c3 = __ldg(P.c3 + e);
-                c4 = __ldg(P.c4 + e);
-            }
-            if (has_m) {
-                const int e = (P.wrap_x ? pwm : p - 1) * P.Ny + jj;
-                c1m = __ldg(P.c1 + e);
-                c5m = __ldg(P.c5 + e);
-            }
-            if (has_p) {
-                const int e = (P.wrap_x ? pwp : p + 1) * P.Ny + jj;
-                c1p = __ldg(P.c1 + e);
-                c5p = __ldg(P.c5 + e);
-            }
             const int s = n % NSTAGE;
             tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
             const double *stage = stages + s * TL::STAGE_ELEMS;
             const double *c0 = stage + off;
+            const double *tb = stage + TL::ELEMS + 3 * TL::OELEMS + a * 8;  // row p-1, this j
+            const double evx = tb[BJ * 8 + 0], evy = tb[BJ * 8 + 1];
+            const double c3 = in_T ? tb[BJ * 8 + 3] : 0.0, c4 = in_T ? tb[BJ * 8 + 4] : 0.0;
+            const double c1m = has_m ? tb[2] : 0.0, c5m = has_m ? tb[5] : 0.0;
+            const double c1p = has_p ? tb[2 * BJ * 8 + 2] : 0.0, c5p = has_p ? tb[2 * BJ * 8 + 5] : 0.0;
 
             const double avx = evx + cBvy;
             const double avx_s = avx * mhvx;
@@ -371,7 +363,6 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             }
 #pragma unroll
             for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
-            pw = pwp;
             gq += P1;
             __syncthreads();  // stage s is free for the next refill
         }
@@ -539,8 +530,35 @@ static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
 }
 
 // ops: up to three (coefficient, array) RK operands, already de-duplicated
-int launch_tma_2d2v(const double *src, const double *const ops[3], Stage22 P, unsigned flags, int nseg,
-                    cudaStream_t s) {
+static bool get_tab_map(const double *tab, int Nx, int Ny, int bj, CUtensorMap *out) {
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    MapKey key{tab, {Nx, Ny, 8, -1}, {8, bj, 3, -1}};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {8, (cuuint64_t)Ny, (cuuint64_t)Nx + 2};
+    cuuint64_t strides[2] = {64, (cuuint64_t)Ny * 64};
+    cuuint32_t bdim[3] = {8, (cuuint32_t)bj, 3};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(tab), dims, strides, bdim, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cache.size() > 256) cache.clear();
+    cache.emplace(key, m);
+    *out = m;
+    return true;
+}
+
+int launch_tma_2d2v(const double *src, const double *const ops[3], const double *tab, Stage22 P,
+                    unsigned flags, int nseg, cudaStream_t s) {
     const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
     const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
@@ -552,6 +570,7 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], Stage22 P, un
     for (int o = 0; o < P.nops; ++o)
         if (!get_map(ops[o], Npad, box_op, &maps.op[o])) return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
     for (int o = P.nops; o < 3; ++o) maps.op[o] = maps.core;
+    if (!get_tab_map(tab, P.Nx, P.Ny, c.bj, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
     P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
     P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
     P.i0 = 0;
@@ -597,10 +616,10 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
                                      const double *c3, const double *c4, const double *c5, double hx,
                                      double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
                                      int Nvy, unsigned flags, const double *dt_dev, double cL_div,
-                                     unsigned long long *nonfinite, double *moment_partials,
-                                     int xsegments, void *stream) {
+                                     unsigned long long *nonfinite, const double *packed_tables,
+                                     double *moment_partials, int xsegments, void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
-    if (!tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags)) {
+    if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags)) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 2D-2V path");
         return vpfv_stage_2d2v_generic(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2,
                                        c3, c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev,
@@ -664,7 +683,7 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
         if (nseg > Nx / 8) nseg = Nx / 8;
         if (nseg < 1) nseg = 1;
     }
-    return launch_tma_2d2v(src, ops, P, flags, nseg, (cudaStream_t)stream);
+    return launch_tma_2d2v(src, ops, packed_tables, P, flags, nseg, (cudaStream_t)stream);
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,

@@ -77,6 +77,8 @@ class StageTables:
             self.denx, self.deny = 96.0 * h[2], 96.0 * h[3]
             mk = lambda: torch.empty(phys_shape, dtype=torch.float64, device=device)  # noqa: E731
             self.evx, self.evy, self.c1, self.c3, self.c4, self.c5 = (mk() for _ in range(6))
+            # packed (evx, evy, c1, c3, c4, c5) rows with periodic x ghost rows, for the tiled kernel
+            self.packed = torch.zeros((g.N[0] + 2, g.N[1], 8), dtype=torch.float64, device=device)
         if not corrections:
             self.c2 = 0.0
         self.nphys = nphys
@@ -95,7 +97,9 @@ class StageTables:
         return (g.N[0], g.N[1], g.N[2], g.N[3] // 32)
 
     # -- per-stage tables from E (device arrays on the physical grid) ---------
-    def update(self, E, stream):
+    def update(self, E, stream, packed=False):
+        """Recompute the E-dependent tables; ``packed`` builds the layout the
+        tiled 2D-2V kernel streams (instead of the separate arrays)."""
         g = self.grid
         if g.d == 1:
             Ex = E["Ex"]
@@ -104,18 +108,24 @@ class StageTables:
             if not self.corrections:
                 self.c1.zero_()
         else:
-            _lib.call("vpfv_tables_2d", E["Ex"].data_ptr(), E["Ey"].data_ptr(),
-                      self.evx.data_ptr(), self.evy.data_ptr(), self.c1.data_ptr(),
-                      self.c3.data_ptr(), self.c4.data_ptr(), self.c5.data_ptr(), g.N[0], g.N[1],
-                      self.qmk2, self.nqmk2, self.gx, self.gy, self.t1, self.t4, self.denx,
-                      self.deny, stream)
-            if not self.corrections:
-                for c in (self.c1, self.c3, self.c4, self.c5):
-                    c.zero_()
+            common = (g.N[0], g.N[1], self.qmk2, self.nqmk2, self.gx, self.gy, self.t1, self.t4,
+                      self.denx, self.deny, stream)
+            if packed:
+                _lib.call("vpfv_tables_2d_packed", E["Ex"].data_ptr(), E["Ey"].data_ptr(),
+                          self.packed.data_ptr(), *common)
+                if not self.corrections:
+                    self.packed[:, :, 2:6].zero_()
+            else:
+                _lib.call("vpfv_tables_2d", E["Ex"].data_ptr(), E["Ey"].data_ptr(),
+                          self.evx.data_ptr(), self.evy.data_ptr(), self.c1.data_ptr(),
+                          self.c3.data_ptr(), self.c4.data_ptr(), self.c5.data_ptr(), *common)
+                if not self.corrections:
+                    for c in (self.c1, self.c3, self.c4, self.c5):
+                        c.zero_()
 
     # -- launch ---------------------------------------------------------------
     def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
-               nonfinite=None, partials=None):
+               nonfinite=None, partials=None, packed=False):
         g, h, N = self.grid, self.grid.h, self.grid.N
         common_tail = (flags, _ptr(dt_dev), float(cL_div), _ptr(nonfinite), stream)
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
@@ -131,9 +141,10 @@ class StageTables:
             args = (*head, self.vxc.data_ptr(), self.vyc.data_ptr(), self.evx.data_ptr(),
                     self.evy.data_ptr(), self.cB, self.c1.data_ptr(), self.c2, self.c3.data_ptr(),
                     self.c4.data_ptr(), self.c5.data_ptr(), h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3])
-            if partials is not None:
+            if packed or partials is not None:
                 _lib.call("vpfv_stage_2d2v_fused", *args, flags, _ptr(dt_dev), float(cL_div),
-                          _ptr(nonfinite), partials.data_ptr(), 0, stream)
+                          _ptr(nonfinite), self.packed.data_ptr() if packed else None,
+                          _ptr(partials), 0, stream)
             else:
                 _lib.call("vpfv_stage_2d2v", *args, *common_tail)
 
@@ -182,12 +193,13 @@ def fused_stage(dest, A, B, src, ca, cb, cd, cL, grid, species, E, check=True, e
     E_dev = {k: _to_device(v, device, cache) for k, v in E.items()}
     tables = StageTables(grid, species, device)
     stream = stream_handle(device)
-    tables.update(E_dev, stream)
+    flags = _lib.VPFV_EXACT if exact else 0
+    tiled = tables.fused_moment_ok(flags)
+    tables.update(E_dev, stream, packed=tiled)
     flag = None
     if check:
         flag = torch.full((1,), -1, dtype=torch.int64, device=device)
-    flags = _lib.VPFV_EXACT if exact else 0
-    tables.launch(d_dest, d_A, d_B, d_src, ca, cb, cd, cL, flags, stream, nonfinite=flag)
+    tables.launch(d_dest, d_A, d_B, d_src, ca, cb, cd, cL, flags, stream, nonfinite=flag, packed=tiled)
     if not isinstance(dest, torch.Tensor):
         inner = tuple(slice(3, 3 + n) for n in grid.N)
         dest[inner] = d_dest[inner].cpu().numpy()

@@ -103,7 +103,8 @@ class Simulation:
         # fused velocity moment: stages 1-3 emit the moment partials of their
         # dest, which is the next stage's src (stage 1 of a step always runs
         # the standalone moment, so external edits of f0 are honoured)
-        self.fuse_moment = all(t.fused_moment_ok(f) for t, f in zip(self.tables, self.flags))
+        self.tiled = [t.fused_moment_ok(f) for t, f in zip(self.tables, self.flags)]
+        self.fuse_moment = all(self.tiled)
         self.partials = ([torch.empty(t.partials_shape(), dtype=torch.float64, device=self.device)
                           for t in self.tables] if self.fuse_moment else None)
         self._last_E = None
@@ -134,14 +135,14 @@ class Simulation:
             E = self.fields.solve(src, stream=stream)
         self._last_E = E
         for s, tab in enumerate(self.tables):
-            tab.update(E, stream)
+            tab.update(E, stream, packed=self.tiled[s])
             nf = None if slot is None else self.nonfinite[slot, s:s + 1]
             timed = self._timing and slot is not None
             if timed:
                 self._events[slot][s][0].record()
             tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
                        dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
-                       partials=self.partials[s] if emit_partials else None)
+                       partials=self.partials[s] if emit_partials else None, packed=self.tiled[s])
             if timed:
                 self._events[slot][s][1].record()
 

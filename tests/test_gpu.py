@@ -367,14 +367,15 @@ def test_tiled_stage_wrap_reads_interior_and_fused_moment(N):
     tab = K.StageTables(pg, sp, torch.device("cuda"))
     Ed = {k: dev(v) for k, v in E.items()}
     stream = K.stream_handle()
-    tab.update(Ed, stream)
+    tab.update(Ed, stream, packed=True)
     flags = K.wrap_flags(pg)
     assert tab.fused_moment_ok(flags)
     d_src = dev(bad)
     d_dest = torch.zeros_like(d_src)
     part = torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda")
     nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
-    tab.launch(d_dest, d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, nonfinite=nf, partials=part)
+    tab.launch(d_dest, d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, nonfinite=nf, partials=part,
+               packed=True)
     got = d_dest.cpu().numpy()
     inner = g.inner()
     assert int(nf.item()) == -1
