@@ -29,6 +29,7 @@
 // periodic-or-halo x/y, stored (frozen) velocity ghosts.
 #include <cuda.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <mutex>
@@ -104,6 +105,7 @@ struct Stage22 {
     int wrap_x, wrap_y;
     int i0, i1;        // x range of cells this launch updates (interior indices)
     int nseg, seglen;  // x segments per column block
+    int sj, sk;        // super-tile of column blocks (block order)
     double *partials;  // moment partials [Nx][Ny][Nvx][Nvy/BL] or nullptr
 };
 
@@ -200,10 +202,18 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     const int ncols = nlt * nkt * njt;
     int b = blockIdx.x % ncols;
     const int seg = blockIdx.x / ncols;
+    // L2-friendly order: all vy tiles of a (y, vx) column block are adjacent,
+    // and column blocks are visited in (sj x sk) super-tiles, so a wave of
+    // resident CTAs covers a compact (y, vx) region whose halos it shares
     const int lt = b % nlt;
     b /= nlt;
-    const int kt = b % nkt;
-    const int jt = b / nkt;
+    const int sj = min(P.sj, njt), sk = min(P.sk, nkt);
+    const int nsk = (nkt + sk - 1) / sk;
+    const int st = b / (sj * sk), wi = b % (sj * sk);
+    const int st_j = st / nsk, st_k = st % nsk;
+    const int rows_j = min(sj, njt - st_j * sj), cols_k = min(sk, nkt - st_k * sk);
+    const int jt = st_j * sj + (wi / cols_k) % rows_j;
+    const int kt = st_k * sk + wi % cols_k;
     const int j0 = jt * BJ, k0 = kt * BK, l0 = lt * BL;
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
@@ -577,6 +587,15 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     P.i1 = P.Nx;
     P.nseg = nseg < 1 ? 1 : nseg;
     P.seglen = (P.Nx + P.nseg - 1) / P.nseg;
+    static int sjk[2] = {-1, -1};
+    if (sjk[0] < 0) {
+        const char *e = getenv("VPFV_SUPER");
+        sjk[0] = 8;
+        sjk[1] = 4;
+        if (e) sscanf(e, "%d,%d", &sjk[0], &sjk[1]);
+    }
+    P.sj = sjk[0] > 0 ? sjk[0] : 1;
+    P.sk = sjk[1] > 0 ? sjk[1] : 1;
     switch (tile_cfg()) {
         case 1: return launch_cfg<4, 3, 4>(maps, P, s);
         case 2: return launch_cfg<4, 2, 2>(maps, P, s);
