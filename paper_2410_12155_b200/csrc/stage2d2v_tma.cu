@@ -308,11 +308,21 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             const double avx = evx + cBvy;
             const double avx_s = avx * mhvx;
             const bool vxpos = avx > 0.0;
+            // register reuse along vx: the (j, l) column k = kb-3 .. kb+CK+2 and
+            // the j+-1 columns k = kb-1 .. kb+CK (y stencil + (y,vx) diagonal)
+            double col[CK + 6], cyp[CK + 2], cym[CK + 2];
+#pragma unroll
+            for (int m = 0; m < CK + 6; ++m) col[m] = c0[(m - 3) * L];
+#pragma unroll
+            for (int m = 0; m < CK + 2; ++m) {
+                cyp[m] = c0[KL + (m - 1) * L];
+                cym[m] = c0[-KL + (m - 1) * L];
+            }
 #pragma unroll
             for (int i = 0; i < CK; ++i) {
                 const double *c = c0 + i * L;
                 // x-stencil contribution of s(p) to cells p - o: slot (r - o) mod 7
-                const double t = ax_s[i] * c[0];
+                const double t = ax_s[i] * col[i + 3];
                 if (xpos[i]) {
                     acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
                     acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
@@ -329,16 +339,32 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                     acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
                 }
                 // x-coupled corrections: D(p) = s[k-1]-s[k+1], G(p) = s[l-1]-s[l+1]
-                const double D = c[-L] - c[L];
+                const double D = col[i + 2] - col[i + 4];
                 const double G = c[-1] - c[1];
                 acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
                 acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
                 if (in_T) {
                     const double avy = evy + bvx[i];
-                    const double Ty = ay_s * wsum<KL>(c, ypos);
-                    const double Tvx = avx_s * wsum<L>(c, vxpos);
+                    double wy, wvx;
+                    if (ypos) {
+                        wy = (fma(15.0, c[-2 * KL], -2.0 * c[-3 * KL]) + fma(20.0, col[i + 3], -60.0 * cym[i + 1])) +
+                             fma(-3.0, c[2 * KL], 30.0 * cyp[i + 1]);
+                    } else {
+                        wy = (fma(-30.0, cym[i + 1], 3.0 * c[-2 * KL]) + fma(60.0, cyp[i + 1], -20.0 * col[i + 3])) +
+                             fma(2.0, c[3 * KL], -15.0 * c[2 * KL]);
+                    }
+                    if (vxpos) {
+                        wvx = (fma(15.0, col[i + 1], -2.0 * col[i]) + fma(20.0, col[i + 3], -60.0 * col[i + 2])) +
+                              fma(-3.0, col[i + 5], 30.0 * col[i + 4]);
+                    } else {
+                        wvx = (fma(-30.0, col[i + 2], 3.0 * col[i + 1]) + fma(60.0, col[i + 4], -20.0 * col[i + 3])) +
+                              fma(2.0, col[i + 6], -15.0 * col[i + 5]);
+                    }
+                    const double Ty = ay_s * wy;
+                    const double Tvx = avx_s * wvx;
                     const double Tvy = (avy * mhvy) * wsum<1>(c, avy > 0.0);
-                    const double Tc = fma(c4, dsum<KL, 1>(c), fma(mc2, dsum<L, 1>(c), -c3 * dsum<KL, L>(c)));
+                    const double dyvx = (cyp[i] + cym[i + 2]) - (cyp[i + 2] + cym[i]);
+                    const double Tc = fma(c4, dsum<KL, 1>(c), fma(mc2, dsum<L, 1>(c), -c3 * dyvx));
                     acc[i][r] += (Ty + Tvx) + (Tvy + Tc);
                 }
             }
