@@ -64,6 +64,21 @@ def make_setup(name):
     raise ValueError(name)
 
 
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_tiled_v4_summary.json")
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the stage kernel from the committed ncu --set full
+    captures (mean over the four RK stages), with the capture it came from."""
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            caps = json.load(f)["captures"]
+        vals = [c["traffic_bytes"] for c in caps if c.get("traffic_bytes")]
+        return (sum(vals) / len(vals) if vals else None), os.path.relpath(PROFILE_SUMMARY, ROOT)
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -212,6 +227,7 @@ def run_b200(args, rank, world, device):
     stage_bytes = sum(b * cells_local for b in STAGE_BYTES) * args.steps
     stage_s = sum(stage_ms) / 1e3
     peak, peak_kind = load_peaks()
+    traffic, traffic_src = load_traffic()
     achieved = stage_bytes / stage_s / 1e9 if stage_s > 0 else None
     share = stage_s / (ms_local / 1e3)
 
@@ -238,7 +254,9 @@ def run_b200(args, rank, world, device):
                    "cells": cells_global, "dt": dt, "l2": "inputs larger than L2 (2.58 GB/buffer)",
                    "parallelism": f"x-slab x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": sum(b * cells_local for b in STAGE_BYTES) / 4,
                      "kernel": "vpfv stage_2d2v (fused RHS + RK4 update)",
                      "algorithmic_bytes_per_cell_per_step": sum(STAGE_BYTES),
                      "stage_ms_per_step": [m / args.steps for m in stage_ms],

@@ -330,10 +330,21 @@ def stage_tables(g, s, E):
                 c1=c["c1"], c2=float(c["c2"]), c3=c["c3"], c4=c["c4"], c5=c["c5"])
 
 
-def fused_rhs(src, g, s, E):
+def slice_tables(T, x0, nloc):
+    """Per-slab view of global line tables (runner.py:398-429: coefficients
+    come from the global E and are sliced per box)."""
+    out = dict(T)
+    for k in ("avx", "evx", "evy", "c1", "c3", "c4", "c5"):
+        if k in out and isinstance(out[k], np.ndarray):
+            out[k] = out[k][x0:x0 + nloc]
+    return out
+
+
+def fused_rhs(src, g, s, E, T=None):
     """RHS exactly as the fused kernels accumulate it (_kernels.py:97-113,
-    167-194, 264-313)."""
-    T = stage_tables(g, s, E)
+    167-194, 264-313).  ``T`` optionally supplies precomputed tables."""
+    if T is None:
+        T = stage_tables(g, s, E)
     h = g.h
     if (g.d, g.v) == (1, 1):
         a_x = T["ax"][None, :]
@@ -386,14 +397,14 @@ def first_nonfinite(dest, g):
     return tuple(int(i) for i in np.unravel_index(np.argmax(bad), g.N))
 
 
-def fused_stage(dest, A, B, src, ca, cb, cd, cL, g, s, E, check=True):
+def fused_stage(dest, A, B, src, ca, cb, cd, cL, g, s, E, check=True, tables=None):
     """``fused_stage`` (_kernels.py:320-373): in-place interior update."""
     if dest is src:
         raise ValueError("dest must not alias src")
     if (g.d, g.v) not in ((1, 1), (1, 2), (2, 2)):
         raise ValueError(f"unsupported dimensionality ({g.d},{g.v})")
     inner = g.inner()
-    rhs = fused_rhs(src, g, s, E)
+    rhs = fused_rhs(src, g, s, E, tables)
     dest[inner] = ((ca * A[inner] + cb * B[inner]) + cd * dest[inner]) + cL * rhs
     if check:
         mi = first_nonfinite(dest, g)

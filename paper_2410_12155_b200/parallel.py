@@ -1,0 +1,344 @@
+"""Multi-GPU driver: x-slab decomposition, one process per GPU.
+
+The B200-native replacement for the reference's in-process
+``SimulatedCluster`` (/root/reference/pkg/src/vpfv/runner.py:259-496,
+partition.py:264-814) for the north-star configuration "2D-2V decomposed over
+the 8 B200 of one box": every rank owns a contiguous x-slab of every species'
+phase space (all of y and velocity space), so
+
+* the halo exchange is two 3-plane slabs per species per stage -- contiguous
+  runs of the padded array (x is the slowest dim), sent with NCCL send/recv
+  over NVLink/NVSwitch, no packing.  Sending the full padded
+  planes is exact: their velocity-ghost entries are the frozen t=0 values the
+  receiver already holds, and the (x-ghost, y-ghost) corners are never read;
+* the charge density needs no reduction: a rank holds the complete velocity
+  space of its cells, so the per-slab densities are all-gathered and every
+  rank solves the (tiny) Poisson problem itself -- the reference's "one
+  global field solve sliced per box" (runner.py:10-18, 386-392), so the run
+  is bitwise equal to the single-GPU one;
+* coefficient tables are computed from the global E and sliced per slab
+  (runner.py:398-429) -- here by pointer offset into the global tables.
+
+``SlabExchange`` holds the communication logic and is backend agnostic
+(NCCL on CUDA tensors, gloo on CPU tensors), so tests/test_parallel.py runs
+it with world size 2 on the CPU against the single-rank oracle.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .fields import FieldSolver
+from .grid import NGHOST, make_grid
+from .kernels import StageTables, stream_handle
+from .runner import RunDiverged, _host_filled, require_cuda, stable_dt
+from .timestepping import DEFAULT_SIGMA, RK4_STAGES, StepContext
+
+
+def slab_bounds(Nx, world, rank):
+    """(x0, nloc) of rank's x-slab; the reference's span rule (>= 8 cells,
+    partition.py:305-313) and divisibility."""
+    if Nx % world:
+        raise ValueError(f"partition count {world} does not divide N[0]={Nx}")
+    nloc = Nx // world
+    if nloc < 8:
+        raise ValueError(f"partition span {nloc} in dim 0 is below the stencil + correction footprint minimum of 8")
+    return rank * nloc, nloc
+
+
+def local_grid(g, x0, nloc):
+    """Slab grid: non-periodic in x (filled by exchange), global widths kept
+    verbatim (partition.py:177-196)."""
+    lo = list(g.lo)
+    hi = list(g.hi)
+    lo[0] = g.lo[0] + x0 * g.h[0]
+    hi[0] = g.lo[0] + (x0 + nloc) * g.h[0]
+    periodic = list(g.periodic)
+    periodic[0] = False
+    N = list(g.N)
+    N[0] = nloc
+    return make_grid(g.d, g.v, N, lo, hi, periodic=periodic, spacing=g.h)
+
+
+class SlabExchange:
+    """x-halo exchange and density all-gather among the ranks of a group."""
+
+    def __init__(self, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self.left = (rank - 1) % world
+        self.right = (rank + 1) % world
+        # gloo moves host memory only: CUDA tensors are staged through the host
+        # (used by the single-box multi-process tests; NCCL sends device memory)
+        self.host_staged = world > 1 and dist.get_backend(group) == "gloo"
+
+    def _gr(self, r):
+        return r if self.group is None else dist.get_global_rank(self.group, r)
+
+    def exchange_x(self, fields):
+        """Fill the 3 low/high x-ghost planes of every padded array in
+        ``fields`` from the periodic x neighbours.  Order per peer pair:
+        (my last planes -> right's low ghosts, recv my low ghosts from left),
+        then (my first planes -> left's high ghosts, recv my high ghosts from
+        right) -- consistent even when left == right (world size 2)."""
+        if self.world == 1:
+            for f in fields:
+                n = f.shape[0] - 2 * NGHOST
+                f[:NGHOST].copy_(f[n:n + NGHOST])
+                f[n + NGHOST:].copy_(f[NGHOST:2 * NGHOST])
+            return
+        staged = self.host_staged and fields[0].is_cuda
+        work = [f.cpu() if staged else f for f in fields]
+        ops = []
+        for f in work:
+            n = f.shape[0] - 2 * NGHOST
+            ops.append(dist.P2POp(dist.isend, f[n:n + NGHOST], self._gr(self.right), self.group))
+            ops.append(dist.P2POp(dist.irecv, f[:NGHOST], self._gr(self.left), self.group))
+            ops.append(dist.P2POp(dist.isend, f[NGHOST:2 * NGHOST], self._gr(self.left), self.group))
+            ops.append(dist.P2POp(dist.irecv, f[n + NGHOST:], self._gr(self.right), self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        if staged:
+            for f, w in zip(fields, work):
+                n = f.shape[0] - 2 * NGHOST
+                f[:NGHOST].copy_(w[:NGHOST])
+                f[n + NGHOST:].copy_(w[n + NGHOST:])
+
+    def gather_x(self, local, out):
+        """All-gather slabs along dim 0: ``local`` (nloc, ...) -> ``out`` (world*nloc, ...)."""
+        if self.world == 1:
+            out.copy_(local)
+            return out
+        if local.is_cuda and not self.host_staged:
+            dist.all_gather_into_tensor(out, local.contiguous(), group=self.group)
+        elif local.is_cuda:
+            host = torch.empty(out.shape, dtype=out.dtype)
+            self.gather_x(local.cpu(), host)
+            out.copy_(host)
+        else:
+            parts = list(out.chunk(self.world, dim=0))
+            tmp = [torch.empty_like(p) for p in parts]
+            dist.all_gather(tmp, local.contiguous(), group=self.group)
+            for p, t in zip(parts, tmp):
+                p.copy_(t)
+        return out
+
+    def any_flag(self, bad: bool, device):
+        if self.world == 1:
+            return bad
+        t = torch.tensor([1 if bad else 0], dtype=torch.int32,
+                         device="cpu" if self.host_staged else device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
+
+class _LocalTables:
+    """A StageTables view launching on the local slab with table pointers
+    offset to the slab's first x row of the global tables."""
+
+    def __init__(self, tables: StageTables, lgrid, x0):
+        self.t = tables
+        self.lgrid = lgrid
+        self.x0 = x0
+
+    def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
+               nonfinite=None, partials=None, packed=False):
+        t, g = self.t, self.lgrid
+        h, N = g.h, g.N
+        Ny = t.grid.N[1] if t.grid.d == 2 else 1
+        off = self.x0 * Ny * 8  # bytes per x row of a [Nx][Ny] fp64 table
+        ptr = lambda a: a.data_ptr() + off  # noqa: E731
+        tail = (flags, None if dt_dev is None else dt_dev.data_ptr(), float(cL_div),
+                None if nonfinite is None else nonfinite.data_ptr())
+        head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
+                float(ca), float(cb), float(cd), float(cL))
+        if (g.d, g.v) == (1, 1):
+            _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr(), ptr(t.e), ptr(t.c1), h[0], h[1],
+                      N[0], N[1], *tail, stream)
+        elif (g.d, g.v) == (1, 2):
+            _lib.call("vpfv_stage_1d2v", *head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.e),
+                      t.avy.data_ptr(), ptr(t.c1), t.c2, h[0], h[1], h[2], N[0], N[1], N[2], *tail, stream)
+        else:
+            args = (*head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.evx), ptr(t.evy), t.cB, ptr(t.c1),
+                    t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3])
+            if packed or partials is not None:
+                # packed rows of the global table: local row r <-> global row x0 + r
+                pk = t.packed.data_ptr() + self.x0 * Ny * 8 * 8 if packed else None
+                _lib.call("vpfv_stage_2d2v_fused", *args, *tail, pk,
+                          None if partials is None else partials.data_ptr(), 0, stream)
+            else:
+                _lib.call("vpfv_stage_2d2v", *args, *tail, stream)
+
+
+class DistributedSimulation:
+    """``Simulation`` over the ranks of the default process group (one GPU
+    each): x-slab decomposition, NCCL halo exchange, replicated Poisson."""
+
+    def __init__(self, setup, cfl_fraction=0.9, dt=None, corrections=True, sigma=DEFAULT_SIGMA, *,
+                 device=None, exact=False, group=None):
+        self.device = require_cuda(device)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.comm = SlabExchange(self.rank, self.world, group)
+        self.species = tuple(setup.species)
+        self.grids = tuple(f.grid for f in setup.dists)  # global grids
+        self.cfl_fraction, self.fixed_dt, self.sigma = cfl_fraction, dt, sigma
+        self.corrections, self.exact = corrections, exact
+        self._names = [f.species for f in setup.dists]
+        g0 = self.grids[0]
+        self.x0, self.nloc = slab_bounds(g0.N[0], self.world, self.rank)
+        self.lgrids = tuple(local_grid(g, self.x0, self.nloc) for g in self.grids)
+        f0 = []
+        for f in setup.dists:
+            data, _ = _host_filled(f)  # global padded, ghosts filled (scatter_field semantics)
+            f0.append(torch.from_numpy(np.ascontiguousarray(data[self.x0:self.x0 + self.nloc + 2 * NGHOST]))
+                      .to(self.device))
+        self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
+        # tables and the field solve on the GLOBAL grid (replicated), launches on the slab
+        self.gtables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
+        base = _lib.VPFV_EXACT if exact else 0
+        # x is exchanged (read from ghost storage); other periodic dims wrap in-kernel
+        self.flags = [base | sum(_lib.VPFV_WRAP(k) for k in range(1, lg.ndim) if lg.periodic[k])
+                      for lg in self.lgrids]
+        self.tiled = [bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*lg.N, fl)) if lg.ndim == 4 else False
+                      for lg, fl in zip(self.lgrids, self.flags)]
+        self.tables = [_LocalTables(t, lg, self.x0) for t, lg in zip(self.gtables, self.lgrids)]
+        self.fields = FieldSolver(self.grids, self.species, self.device)
+        S = len(self.species)
+        phys_loc = (self.nloc,) + tuple(g0.N[1:g0.d])
+        self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)
+        self._n_gather = torch.empty((self.world, S) + phys_loc, dtype=torch.float64, device=self.device)
+        self.fuse_moment = all(self.tiled)
+        self.partials = ([torch.empty((self.nloc,) + tuple(lg.N[1:3]) + (lg.N[3] // 32,),
+                                      dtype=torch.float64, device=self.device) for lg in self.lgrids]
+                         if self.fuse_moment else None)
+        self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
+        self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._timing = False
+        self._events = None
+        self._stage_ms = [0.0] * 4
+        self._launches = 0
+        self._N_arrays = [_lib.int_array(lg.N) for lg in self.lgrids]
+
+    # ------------------------------------------------------------------
+    def local_cells(self):
+        return sum(int(np.prod(lg.N)) for lg in self.lgrids)
+
+    @property
+    def t(self):
+        return self.ctx.t
+
+    @property
+    def step_count(self):
+        return self.ctx.step
+
+    def _densities(self, srcs, from_partials, stream):
+        """Local slab densities -> all-gathered global n in self.fields.n."""
+        for s, (lg, f) in enumerate(zip(self.lgrids, srcs)):
+            if from_partials:
+                _lib.call("vpfv_moment_partials", self.partials[s].data_ptr(), self.n_local[s].data_ptr(),
+                          int(np.prod(lg.N[:lg.d])), lg.N[2], self.partials[s].shape[-1],
+                          self.fields.vols[s], stream)
+            else:
+                _lib.call("vpfv_moment", f.data_ptr(), self.n_local[s].data_ptr(), lg.d, lg.v,
+                          self._N_arrays[s], self.fields.vols[s], stream)
+        self.comm.gather_x(self.n_local.unsqueeze(0).reshape((1,) + tuple(self.n_local.shape)),
+                           self._n_gather)
+        # (world, S, nloc, ...) -> (S, Nx, ...)
+        S = len(self.species)
+        self.fields.n.copy_(self._n_gather.transpose(0, 1).reshape((S,) + tuple(self.fields.n.shape[1:])))
+
+    def _solve(self, srcs, from_partials=False):
+        stream = stream_handle(self.device)
+        self._densities(srcs, from_partials, stream)
+        self.fields.charge(stream)
+        return self.fields.poisson(self.fields.rho, False, stream)
+
+    def _stage(self, dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=None, cL_div=1.0):
+        stream = stream_handle(self.device)
+        self.comm.exchange_x(src)
+        use_partials = self.fuse_moment and slot is not None and slot > 0
+        emit = self.fuse_moment and slot is not None and slot < 3
+        E = self._solve(src, from_partials=use_partials)
+        for s, (gt, lt) in enumerate(zip(self.gtables, self.tables)):
+            gt.update(E, stream, packed=self.tiled[s])
+            nf = None if slot is None else self.nonfinite[slot, s:s + 1]
+            if self._timing and slot is not None:
+                self._events[slot][s][0].record()
+            lt.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream, dt_dev=dt_dev,
+                      cL_div=cL_div, nonfinite=nf, partials=self.partials[s] if emit else None,
+                      packed=self.tiled[s])
+            if self._timing and slot is not None:
+                self._events[slot][s][1].record()
+
+    def launch_step(self, dt):
+        self.dt_dev.fill_(float(dt))
+        start = _lib.launch_counter[0]
+        bufs = {"f0": self.ctx.f0, "f1": self.ctx.f1, "fout": self.ctx.fout}
+        self.nonfinite.fill_(-1)
+        for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
+            self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, slot,
+                        dt_dev=self.dt_dev, cL_div=div)
+        self._launches = _lib.launch_counter[0] - start
+
+    def launches_per_step(self):
+        return self._launches
+
+    def enable_stage_timing(self, on=True):
+        self._timing = bool(on)
+        self._stage_ms = [0.0] * 4
+        if on and self._events is None:
+            S = len(self.species)
+            self._events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                             for _ in range(S)] for _ in range(4)]
+
+    def stage_kernel_ms(self):
+        return list(self._stage_ms)
+
+    # ------------------------------------------------------------------
+    def max_dt(self):
+        E = self._solve(self.ctx.f0)
+        return stable_dt(self.grids, self.species, {k: v.cpu().numpy() for k, v in E.items()}, self.sigma)
+
+    def current_dt(self):
+        if self.fixed_dt is not None:
+            return self.fixed_dt
+        bound = self.max_dt()
+        if not math.isfinite(bound):
+            raise RunDiverged("stability bound is not finite (empty flow?)")
+        return bound * self.cfl_fraction
+
+    def advance(self, dt):
+        self.launch_step(dt)
+        torch.cuda.current_stream(self.device).synchronize()
+        if self._timing:
+            for slot in range(4):
+                for a, b in self._events[slot]:
+                    self._stage_ms[slot] += a.elapsed_time(b)
+        self.ctx.t = self.ctx.t + dt
+        self.ctx.rotate()
+        flags = self.nonfinite[3].cpu().numpy().astype(np.uint64)
+        bad_local = [s for s in range(len(self.species)) if flags[s] != np.uint64(_lib.VPFV_FINITE)]
+        if self.comm.any_flag(bool(bad_local), self.device):
+            self.ctx.f0, self.ctx.fout = self.ctx.fout, self.ctx.f0
+            self.ctx.t -= dt
+            self.ctx.step -= 1
+            name = self._names[bad_local[0]] if bad_local else "?"
+            raise RunDiverged(f"species {name} non-finite on rank {self.rank}" if bad_local
+                              else "non-finite state on another rank")
+
+    def interiors(self):
+        """This rank's slab interiors."""
+        return [a[lg.interior_slices()].cpu().numpy().copy() for a, lg in zip(self.ctx.f0, self.lgrids)]
+
+    def gather(self, s):
+        """Global interior array of species ``s`` (every rank gets it)."""
+        lg, g = self.lgrids[s], self.grids[s]
+        local = self.ctx.f0[s][lg.interior_slices()].contiguous()
+        out = torch.empty(tuple(g.N), dtype=torch.float64, device=self.device)
+        self.comm.gather_x(local, out)
+        return out.cpu().numpy()

@@ -1,0 +1,134 @@
+"""Multi-rank (world size 2, gloo, CPU) coverage of the x-slab layer.
+
+The communication logic of paper_2410_12155_b200.parallel (SlabExchange,
+slab_bounds, local_grid, global-table slicing) drives the oracle's stage on
+each rank; the gathered state must equal the single-rank oracle run bitwise
+-- the reference's SimulatedCluster == Simulation property
+(/root/reference/pkg/tests/test_runner.py:107-155).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import golden_io as G
+from oracle import vpfv_oracle as O
+from paper_2410_12155_b200 import parallel as PL
+from paper_2410_12155_b200.grid import NGHOST
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _cases():
+    """(name, grids, species, init padded arrays, dt) with Nx divisible into
+    two slabs of >= 8 cells."""
+    out = []
+    for name in ("twostream", "landau1d"):
+        c = G.step_case(name)
+        out.append((name, c["grids"], c["species"], c["init"], c["dt"]))
+    # 2D-2V two-species (different velocity boxes), built from oracle pieces
+    sp = [O.Species("i", 1.0, 1.0, 1.0, 0.1, 1.0, (0.0, 0.01)), O.Species("e", -1.0, 0.04, 1.0, 0.1, 1.0, (0.0, 0.01))]
+    grids, init = [], []
+    rng = np.random.default_rng(11)
+    for vmax in (3.0, 6.0):
+        g = O.Grid(2, 2, (16, 8, 8, 8), (0.0, 0.0, -vmax, -vmax), (4 * np.pi, 4 * np.pi, vmax, vmax))
+        a = 1.0 + 0.2 * rng.random(g.padded_shape)
+        grids.append(g)
+        init.append(O.fill_ghosts(a, g, O.capture_frozen(a, g)))
+    out.append(("2d2v-2sp", grids, sp, init, 0.01))
+    return out
+
+
+def _run_slabs(rank, world, grids, species, init, dt, steps):
+    comm = PL.SlabExchange(rank, world)
+    x0, nloc = PL.slab_bounds(grids[0].N[0], world, rank)
+    lgrids = [O.grid_from(PL.local_grid(g, x0, nloc)) for g in grids]
+    filled = [O.fill_ghosts(np.array(d), g, O.capture_frozen(d, g)) for d, g in zip(init, grids)]
+    f0 = [torch.from_numpy(np.ascontiguousarray(a[x0:x0 + nloc + 2 * NGHOST])) for a in filled]
+    local_frozen = [O.capture_frozen(f.numpy(), lg) for f, lg in zip(f0, lgrids)]
+    ctx = O.StepContext(f0=f0, f1=[t.clone() for t in f0], fout=[t.clone() for t in f0])
+    S = len(species)
+
+    def stage(dest, A, B, src, ca, cb, cd, cL, t):
+        for s in range(S):  # local fill (frozen velocity slabs, unsplit periodic dims)
+            O.fill_ghosts(src[s].numpy(), lgrids[s], local_frozen[s])
+        comm.exchange_x(src)
+        n_loc = torch.from_numpy(np.stack([O.zeroth_moment(src[s].numpy(), lgrids[s]) for s in range(S)]))
+        gathered = torch.empty((world,) + tuple(n_loc.shape), dtype=torch.float64)
+        comm.gather_x(n_loc.unsqueeze(0), gathered)
+        dens = list(gathered.transpose(0, 1).reshape((S, grids[0].N[0]) + tuple(n_loc.shape[2:])).numpy())
+        _, E = O.poisson_solve(O.charge_density(dens, species), grids[0])
+        for s in range(S):
+            T = O.slice_tables(O.stage_tables(grids[s], species[s], E), x0, nloc)
+            O.fused_stage(dest[s].numpy(), A[s].numpy(), B[s].numpy(), src[s].numpy(), ca, cb, cd, cL,
+                          lgrids[s], species[s], E, check=False, tables=T)
+
+    for _ in range(steps):
+        O.rk4_38_low_storage_step(ctx, dt, stage)
+        ctx.rotate()
+    out = []
+    for s in range(S):
+        local = torch.from_numpy(np.ascontiguousarray(ctx.f0[s].numpy()[lgrids[s].inner()]))
+        full = torch.empty(tuple(grids[s].N), dtype=torch.float64)
+        comm.gather_x(local, full)
+        out.append(full.numpy())
+    return out
+
+
+def _worker(rank, world, port, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for name, grids, species, init, dt in _cases():
+            res[name] = _run_slabs(rank, world, grids, species, init, dt, steps)
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_slabs_equal_single_rank_bitwise():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 2, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for name, grids, species, init, dt in _cases():
+        ref = O.OracleSimulation(grids, species, init, dt=dt, rhs="fused")
+        for _ in range(2):
+            ref.advance(dt)
+        for a, b in zip(got[name], ref.interiors()):
+            assert np.array_equal(a, b), name
+
+
+def test_slab_bounds_rules():
+    assert PL.slab_bounds(128, 8, 3) == (48, 16)
+    with pytest.raises(ValueError):
+        PL.slab_bounds(128, 3, 0)
+    with pytest.raises(ValueError):
+        PL.slab_bounds(16, 4, 0)
+
+
+def test_local_grid_keeps_global_widths():
+    from paper_2410_12155_b200.grid import make_grid
+
+    g = make_grid(2, 2, (16, 8, 8, 8), (0, 0, -1, -1), (1.3, 1, 1, 1))
+    lg = PL.local_grid(g, 8, 8)
+    assert lg.h == g.h and lg.periodic == (False, True, False, False)
+    assert lg.centers(2).tolist() == g.centers(2).tolist()
