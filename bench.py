@@ -359,10 +359,16 @@ def main():
     import torch
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("VPFV_SAME_DEVICE"):  # validation only: all ranks on GPU 0 (gloo transport)
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("VPFV_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=device)
+        else:
+            torch.distributed.init_process_group(backend)
     line = run_b200(args, rank, world, device)
     if rank == 0:
         print(json.dumps(line), flush=True)
