@@ -228,6 +228,8 @@ def run_b200(args, rank, world, device):
     stage_s = sum(stage_ms) / 1e3
     peak, peak_kind = load_peaks()
     traffic, traffic_src = load_traffic()
+    if args.workload != "landau2d-128" or world != 1:  # the capture is of that configuration
+        traffic, traffic_src = None, None
     achieved = stage_bytes / stage_s / 1e9 if stage_s > 0 else None
     share = stage_s / (ms_local / 1e3)
 
