@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libvpfv.so")
+LIB_PATH = os.environ.get("VPFV_LIB") or os.path.join(HERE, "lib", "libvpfv.so")
 
 VPFV_OK = 0
 VPFV_EALIAS = 1

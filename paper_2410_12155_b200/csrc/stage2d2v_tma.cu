@@ -343,7 +343,11 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                 const double G = c[-1] - c[1];
                 acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
                 acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
+#ifndef VPFV_EXP_SKIP_T
                 if (in_T) {
+#else
+                if (in_T && P.Nx < 0) {
+#endif
                     const double avy = evy + bvx[i];
                     double wy, wvx;
                     if (ypos) {
