@@ -119,14 +119,15 @@ struct Tile {
     static constexpr int TELEMS = 3 * BJ * 8;              // packed E tables, planes p-1..p+1
     static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS + TELEMS;
     static constexpr int TAB_BYTES = TELEMS * 8;
-    static constexpr int HALO_BYTES = ELEMS * 8, OP_BYTES = OELEMS * 8;
+    static constexpr int HROWS = BK + 2;                  // vx rows a y-halo row needs (k-1 .. k+BK)
+    static constexpr int HALO_BYTES = (BJ * K + 6 * HROWS) * L * 8, OP_BYTES = OELEMS * 8;
     static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
     static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ, BK_ = BK, BL_ = BL;
     static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
 };
 
 struct Maps {
-    CUtensorMap core, halo, op[3], tab;
+    CUtensorMap core, hrow, op[3], tab;
 };
 
 // upwinded 6-point weighted sum (face difference * 60) along an in-tile
@@ -176,9 +177,18 @@ __device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, cons
     const int cx = px + NG;
     // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
     tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
-    tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
     tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx);
-    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
+    // y-halo rows: only vx rows k0-1 .. k0+BK (tile rows 2 .. BK+3) are read
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        int ylo = cy_lo - NG + r, yhi = cy_hi - NG + r;
+        if (P.wrap_y) {
+            if (ylo >= P.Ny) ylo -= P.Ny;
+            if (yhi >= P.Ny) yhi -= P.Ny;
+        }
+        tma::load4d(dst + (r * TL::K + 2) * TL::L, &M->hrow, &bars[s], l0, k0 + 2, ylo + NG, cx);
+        tma::load4d(dst + ((TL::BJ_ + 3 + r) * TL::K + 2) * TL::L, &M->hrow, &bars[s], l0, k0 + 2, yhi + NG, cx);
+    }
     if (ops) {
         for (int o = 0; o < P.nops; ++o)
             tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
@@ -323,7 +333,11 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                 const double *c = c0 + i * L;
                 // x-stencil contribution of s(p) to cells p - o: slot (r - o) mod 7
                 const double t = ax_s[i] * col[i + 3];
+#ifdef VPFV_EXP_SKIP_X
+                if (P.Nx < 0) {
+#else
                 if (xpos[i]) {
+#endif
                     acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
                     acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
                     acc[i][(r + 8) % 7] = fma(-60.0, t, acc[i][(r + 8) % 7]);
@@ -339,10 +353,12 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                     acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
                 }
                 // x-coupled corrections: D(p) = s[k-1]-s[k+1], G(p) = s[l-1]-s[l+1]
+#ifndef VPFV_EXP_SKIP_DG
                 const double D = col[i + 2] - col[i + 4];
                 const double G = c[-1] - c[1];
                 acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
                 acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
+#endif
 #ifndef VPFV_EXP_SKIP_T
                 if (in_T) {
 #else
@@ -392,12 +408,24 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                             atomicMin(P.nonfinite,
                                       (((unsigned long long)q * P.Ny + jj) * P.Nvx + kfirst + i) * P.Nvy + ll);
                 }
+#ifdef VPFV_EXP_SKIP_PARTIALS
+                if (P.partials && P.Nx < 0) {
+#else
                 if (P.partials) {
+#endif
+                    // fold-tree subtrees of two rows at once: lanes pair up
+                    // (even lane keeps row i, odd lane row i+1), then the usual
+                    // ascending shuffle levels on one register
                     const long long pb = ((long long)q * P.Ny + jj) * P.Nvx + kfirst;
+                    const bool odd = lane & 1;
 #pragma unroll
-                    for (int i = 0; i < CK; ++i) {
-                        const double sub = warp_tree_sum(out[i]);
-                        if (lane == 0) P.partials[(pb + i) * nlt + lt] = sub;
+                    for (int i = 0; i < CK; i += 2) {
+                        const double keep = odd ? out[i + 1] : out[i];
+                        const double send = odd ? out[i] : out[i + 1];
+                        double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+#pragma unroll
+                        for (int off = 2; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+                        if (lane < 2) P.partials[(pb + i + lane) * nlt + lt] = v;
                     }
                 }
             }
@@ -602,10 +630,10 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
     const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
-    const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
+    const int box_hrow[4] = {TBL + 8, TBK + 2, 1, 1};
     const int box_op[4] = {TBL + 2, TBK, c.bj, 1};
     Maps maps;
-    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_halo, &maps.halo))
+    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_hrow, &maps.hrow))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
     for (int o = 0; o < P.nops; ++o)
         if (!get_map(ops[o], Npad, box_op, &maps.op[o])) return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
