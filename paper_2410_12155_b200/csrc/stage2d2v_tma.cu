@@ -119,15 +119,14 @@ struct Tile {
     static constexpr int TELEMS = 3 * BJ * 8;              // packed E tables, planes p-1..p+1
     static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS + TELEMS;
     static constexpr int TAB_BYTES = TELEMS * 8;
-    static constexpr int HROWS = BK + 2;                  // vx rows a y-halo row needs (k-1 .. k+BK)
-    static constexpr int HALO_BYTES = (BJ * K + 6 * HROWS) * L * 8, OP_BYTES = OELEMS * 8;
+    static constexpr int HALO_BYTES = ELEMS * 8, OP_BYTES = OELEMS * 8;
     static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
     static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ, BK_ = BK, BL_ = BL;
     static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
 };
 
 struct Maps {
-    CUtensorMap core, hrow, op[3], tab;
+    CUtensorMap core, halo, op[3], tab;
 };
 
 // upwinded 6-point weighted sum (face difference * 60) along an in-tile
@@ -177,18 +176,9 @@ __device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, cons
     const int cx = px + NG;
     // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
     tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
+    tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
     tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx);
-    // y-halo rows: only vx rows k0-1 .. k0+BK (tile rows 2 .. BK+3) are read
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        int ylo = cy_lo - NG + r, yhi = cy_hi - NG + r;
-        if (P.wrap_y) {
-            if (ylo >= P.Ny) ylo -= P.Ny;
-            if (yhi >= P.Ny) yhi -= P.Ny;
-        }
-        tma::load4d(dst + (r * TL::K + 2) * TL::L, &M->hrow, &bars[s], l0, k0 + 2, ylo + NG, cx);
-        tma::load4d(dst + ((TL::BJ_ + 3 + r) * TL::K + 2) * TL::L, &M->hrow, &bars[s], l0, k0 + 2, yhi + NG, cx);
-    }
+    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
     if (ops) {
         for (int o = 0; o < P.nops; ++o)
             tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
@@ -630,10 +620,10 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
     const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
-    const int box_hrow[4] = {TBL + 8, TBK + 2, 1, 1};
+    const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
     const int box_op[4] = {TBL + 2, TBK, c.bj, 1};
     Maps maps;
-    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_hrow, &maps.hrow))
+    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_halo, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
     for (int o = 0; o < P.nops; ++o)
         if (!get_map(ops[o], Npad, box_op, &maps.op[o])) return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
