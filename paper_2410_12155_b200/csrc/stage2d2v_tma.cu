@@ -254,28 +254,19 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     // Persistent CTAs: work units blockIdx.x, +gridDim.x, ...; thread 0 is
     // the TMA producer, running NSTAGE-1 planes ahead across unit boundaries.
     const Maps *M = &maps;
-    // producer state lives in shared memory (only thread 0 touches it) so it
-    // costs the consumers no registers
-    __shared__ Work prod_w;
-    __shared__ int prod_state[2];  // block id, plane index
+    int prod_blk = blockIdx.x, prod_n = 0;
+    Work prod_w = work_of<BJ, BK, BL>(prod_blk, P);
     auto produce = [&](int slot) {
-        int pb = prod_state[0], pn = prod_state[1];
-        while (pb < nblocks && pn >= prod_w.nplanes) {
-            pb += gridDim.x;
-            pn = 0;
-            if (pb < nblocks) prod_w = work_of<BJ, BK, BL>(pb, P);
+        while (prod_blk < nblocks && prod_n >= prod_w.nplanes) {
+            prod_blk += gridDim.x;
+            prod_n = 0;
+            if (prod_blk < nblocks) prod_w = work_of<BJ, BK, BL>(prod_blk, P);
         }
-        prod_state[0] = pb;
-        if (pb >= nblocks) return;
+        if (prod_blk >= nblocks) return;
         tma::fence_proxy_async();
-        issue_plane<TL>(stages, bars, M, slot, pn, prod_w, P);
-        prod_state[1] = pn + 1;
+        issue_plane<TL>(stages, bars, M, slot, prod_n, prod_w, P);
+        ++prod_n;
     };
-    if (tid == 0) {
-        prod_state[0] = blockIdx.x;
-        prod_state[1] = 0;
-        prod_w = work_of<BJ, BK, BL>(blockIdx.x, P);
-    }
     if (tid == 0)
         for (int t = 0; t < NSTAGE - 1; ++t) produce(t);
 
