@@ -156,58 +156,15 @@ __device__ __forceinline__ double warp_tree_sum(double x) {
     return x;
 }
 
-// One unit of work: a (y, vx, vy) column block and an x range of cells.
-struct Work {
-    int j0, k0, l0, i0, i1, cy_lo, cy_core, cy_hi, nplanes;
-};
-
-// Block b -> column block and x segment.  x segment outermost; within it all
-// vy tiles of a (y, vx) column block are adjacent and column blocks run in
-// (sj x sk) super-tiles, so CTAs working at the same time cover a compact
-// (y, vx) region whose halos they share in L2.
-template <int BJ, int BK, int BL>
-__device__ __forceinline__ Work work_of(int blk, const Stage22 &P) {
-    const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
-    const int ncols = nlt * nkt * njt;
-    int b = blk % ncols;
-    const int seg = blk / ncols;
-    const int lt = b % nlt;
-    b /= nlt;
-    const int sj = min(P.sj, njt), sk = min(P.sk, nkt);
-    const int nsk = (nkt + sk - 1) / sk;
-    const int st = b / (sj * sk), wi = b % (sj * sk);
-    const int st_j = st / nsk, st_k = st % nsk;
-    const int rows_j = min(sj, njt - st_j * sj), cols_k = min(sk, nkt - st_k * sk);
-    const int jt = st_j * sj + (wi / cols_k) % rows_j;
-    const int kt = st_k * sk + wi % cols_k;
-    Work w;
-    w.j0 = jt * BJ;
-    w.k0 = kt * BK;
-    w.l0 = lt * BL;
-    w.i0 = P.i0 + seg * P.seglen;
-    w.i1 = min(P.i1, w.i0 + P.seglen);
-    int yl = w.j0 - 3, yh = w.j0 + BJ;
-    if (P.wrap_y) {
-        if (yl < 0) yl += P.Ny;
-        if (yh >= P.Ny) yh -= P.Ny;
-    }
-    w.cy_lo = yl + NG;
-    w.cy_core = w.j0 + NG;
-    w.cy_hi = yh + NG;
-    w.nplanes = w.i1 > w.i0 ? (w.i1 - w.i0) + 6 : 0;
-    return w;
-}
-
-// Plane n of work w into stage slot s: the src halo tile of plane
-// p = i0 - 3 + n, and the RK operand core tiles of cell-plane q = p - 3 when
-// q is updated by this work unit.
+// Plane n: the src halo tile of plane p = p_first + n, and the RK operand core
+// tiles of cell-plane q = p - 3 when q is updated by this CTA.
 template <class TL>
-__device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, const Maps *M, int s, int n,
-                                            const Work &w, const Stage22 &P) {
-    const int i0 = w.i0, i1 = w.i1, l0 = w.l0, k0 = w.k0, j0 = w.j0;
-    const int cy_lo = w.cy_lo, cy_core = w.cy_core, cy_hi = w.cy_hi;
+__device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, const Maps *M, int n,
+                                            int p_first, int i0, int i1, const Stage22 &P, int l0,
+                                            int k0, int j0, int cy_lo, int cy_core, int cy_hi) {
+    const int s = n % TL::NSTAGE_;
     double *dst = stages + s * TL::STAGE_ELEMS;
-    const int p = i0 - 3 + n;
+    const int p = p_first + n;
     int px = p;
     if (P.wrap_x) {
         px %= P.Nx;
@@ -239,11 +196,42 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::STAGE_ELEMS * 8);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nblocks = (P.Ny / BJ) * (P.Nvx / BK) * (P.Nvy / BL) * P.nseg;
+    // column block; x segment outermost so the CTAs resident at once cover
+    // neighbouring column blocks of the same x range (halo reuse in L2)
+    const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
+    const int ncols = nlt * nkt * njt;
+    int b = blockIdx.x % ncols;
+    const int seg = blockIdx.x / ncols;
+    // L2-friendly order: all vy tiles of a (y, vx) column block are adjacent,
+    // and column blocks are visited in (sj x sk) super-tiles, so a wave of
+    // resident CTAs covers a compact (y, vx) region whose halos it shares
+    const int lt = b % nlt;
+    b /= nlt;
+    const int sj = min(P.sj, njt), sk = min(P.sk, nkt);
+    const int nsk = (nkt + sk - 1) / sk;
+    const int st = b / (sj * sk), wi = b % (sj * sk);
+    const int st_j = st / nsk, st_k = st % nsk;
+    const int rows_j = min(sj, njt - st_j * sj), cols_k = min(sk, nkt - st_k * sk);
+    const int jt = st_j * sj + (wi / cols_k) % rows_j;
+    const int kt = st_k * sk + wi % cols_k;
+    const int j0 = jt * BJ, k0 = kt * BK, l0 = lt * BL;
+    const int i0 = P.i0 + seg * P.seglen;
+    const int i1 = min(P.i1, i0 + P.seglen);
+    if (i0 >= i1) return;
 
     // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at the lane's vy
     const int a = warp / (BK / CK);
     const int kb = (warp % (BK / CK)) * CK;
+    const int jj = j0 + a;
+    const int kfirst = k0 + kb;
+    const int ll = l0 + lane;
+
+    int yl = j0 - 3, yh = j0 + BJ;
+    if (P.wrap_y) {
+        if (yl < 0) yl += P.Ny;
+        if (yh >= P.Ny) yh -= P.Ny;
+    }
+    const int cy_lo = yl + NG, cy_core = j0 + NG, cy_hi = yh + NG;
 
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) tma::mbar_init(&bars[s], 1);
@@ -251,46 +239,13 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     }
     __syncthreads();
 
-    // Persistent CTAs: work units blockIdx.x, +gridDim.x, ...; thread 0 is
-    // the TMA producer, running NSTAGE-1 planes ahead across unit boundaries.
+    const int p_first = i0 - 3, p_last = i1 + 2;
+    const int nplanes = p_last - p_first + 1;
     const Maps *M = &maps;
-    int prod_blk = blockIdx.x, prod_n = 0;
-    Work prod_w = work_of<BJ, BK, BL>(prod_blk, P);
-    auto produce = [&](int slot) {
-        while (prod_blk < nblocks && prod_n >= prod_w.nplanes) {
-            prod_blk += gridDim.x;
-            prod_n = 0;
-            if (prod_blk < nblocks) prod_w = work_of<BJ, BK, BL>(prod_blk, P);
-        }
-        if (prod_blk >= nblocks) return;
-        tma::fence_proxy_async();
-        issue_plane<TL>(stages, bars, M, slot, prod_n, prod_w, P);
-        ++prod_n;
-    };
-    if (tid == 0)
-        for (int t = 0; t < NSTAGE - 1; ++t) produce(t);
-
-    const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
-    const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
-    const int nops = P.nops;
-    const double oc0 = P.opc[0], oc1 = P.opc[1], oc2 = P.opc[2];
-    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);   // first cell in the halo tile
-    const int ooff = TL::ELEMS + (a * BK + kb) * TL::OL + lane + 1;  // first cell in operand tile 0
-    const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
-                    P1 = (long long)(P.Ny + 2 * NG) * P2;
-    int gn = 0;  // planes consumed by this CTA (stage slot and mbarrier phase)
-
-    for (int wb = blockIdx.x; wb < nblocks; wb += gridDim.x) {
-    const Work w = work_of<BJ, BK, BL>(wb, P);
-    if (w.nplanes == 0) continue;
-    const int i0 = w.i0, i1 = w.i1, j0 = w.j0, k0 = w.k0, l0 = w.l0;
-    const int jj = j0 + a;
-    const int kfirst = k0 + kb;
-    const int ll = l0 + lane;
-    const int p_first = i0 - 3;
-    const int nplanes = w.nplanes;
-    const int nlt = P.Nvy / BL, lt = l0 / BL;
-    (void)j0;
+    if (tid == 0) {
+        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
+            issue_plane<TL>(stages, bars, M, n, p_first, i0, i1, P, l0, k0, j0, cy_lo, cy_core, cy_hi);
+    }
 
     double ax_s[CK], bvx[CK];
     bool xpos[CK];
@@ -305,6 +260,16 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     const double ay_s = vy * P.mhy;
     const bool ypos = vy > 0.0;
     const double cBvy = P.cB * vy;
+    const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
+    const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
+    const int nops = P.nops;
+    const double oc0 = P.opc[0], oc1 = P.opc[1], oc2 = P.opc[2];
+
+    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);   // first cell in the halo tile
+    const int ooff = TL::ELEMS + (a * BK + kb) * TL::OL + lane + 1;  // first cell in operand tile 0
+
+    const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
+                    P1 = (long long)(P.Ny + 2 * NG) * P2;
     long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(jj + NG) * P2 +
                    (long long)(kfirst + NG) * P3 + (ll + NG);  // cell q = p - 3
 
@@ -322,12 +287,16 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
             const int n = blk + r;
             if (n >= nplanes) break;
             const int p = p_first + n;
-            if (tid == 0) produce((gn + NSTAGE - 1) % NSTAGE);
+            if (tid == 0 && n + NSTAGE - 1 < nplanes) {
+                tma::fence_proxy_async();
+                issue_plane<TL>(stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
+                                cy_core, cy_hi);
+            }
             const bool in_T = (p >= i0 && p < i1);
             const bool has_m = (p - 1 >= i0 && p - 1 < i1);
             const bool has_p = (p + 1 >= i0 && p + 1 < i1);
-            const int s = gn % NSTAGE;
-            tma::mbar_wait(&bars[s], (gn / NSTAGE) & 1);
+            const int s = n % NSTAGE;
+            tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
             const double *stage = stages + s * TL::STAGE_ELEMS;
             const double *c0 = stage + off;
             const double *tb = stage + TL::ELEMS + 3 * TL::OELEMS + a * 8;  // row p-1, this j
@@ -453,10 +422,8 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
 #pragma unroll
             for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
             gq += P1;
-            ++gn;
             __syncthreads();  // stage s is free for the next refill
         }
-    }
     }
 }
 
@@ -616,15 +583,7 @@ static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
         attr = true;
     }
     const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-    }
-    const int grid = nblocks < nsm ? nblocks : nsm;  // persistent: one CTA per SM
-    kern<<<grid, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(maps, P);
+    kern<<<nblocks, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
 }
 
