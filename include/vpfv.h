@@ -81,8 +81,9 @@ int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double
 
 /* 2D-2V stage with the fused velocity-moment epilogue: as vpfv_stage_2d2v,
  * and when moment_partials is non-NULL the kernel also writes, for every new
- * dest cell row (x, y, vx) and every aligned 32-wide vy chunk c, the
- * fold-tree subtree sum  moment_partials[((x*Ny + y)*Nvx + vx)*(Nvy/32) + c]
+ * dest cell row (x, y, vx) and every aligned vy chunk c (width
+ * vpfv_stage_2d2v_partials_chunk(), 16 or 32), the fold-tree subtree sum
+ * moment_partials[((x*Ny + y)*Nvx + vx)*(Nvy/chunk) + c]
  * (finish with vpfv_moment_partials).  Runs the TMA-tiled x-marching kernel
  * (requires the fast path, stored velocity ghosts, Ny%4 == Nvx%8 == Nvy%32
  * == 0); otherwise falls back to the generic kernel (and rejects a non-NULL
@@ -104,6 +105,10 @@ int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const 
 /* 1 when vpfv_stage_2d2v_fused would take the tiled path (and so accepts
  * moment_partials) for these extents and flags, else 0. */
 int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
+
+/* Width of the vy chunks the fused-moment partials are summed over (the
+ * tiled kernel's vy tile, 16 or 32): partials hold Nvy/chunk values per row. */
+int vpfv_stage_2d2v_partials_chunk(void);
 
 /* The untiled one-thread-per-cell 2D-2V kernel (exact or fast), always. */
 int vpfv_stage_2d2v_generic(double *dest, const double *A, const double *B, const double *src,

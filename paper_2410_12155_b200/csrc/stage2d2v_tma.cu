@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     double *stages = reinterpret_cast<double *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::STAGE_ELEMS * 8);
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     // column block; x segment outermost so the CTAs resident at once cover
     // neighbouring column blocks of the same x range (halo reuse in L2)
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
@@ -219,9 +219,11 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at the lane's vy
-    const int a = warp / (BK / CK);
-    const int kb = (warp % (BK / CK)) * CK;
+    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at vy lane `lane`
+    // of its BL-wide row group (BL = 32: one warp per row, 16: two rows)
+    const int lane = tid % BL, colid = tid / BL;
+    const int a = colid / (BK / CK);
+    const int kb = (colid % (BK / CK)) * CK;
     const int jj = j0 + a;
     const int kfirst = k0 + kb;
     const int ll = l0 + lane;
@@ -412,9 +414,10 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                     for (int i = 0; i < CK; i += 2) {
                         const double keep = odd ? out[i + 1] : out[i];
                         const double send = odd ? out[i] : out[i + 1];
-                        double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                        double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1, BL));
 #pragma unroll
-                        for (int off = 2; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+                        for (int off = 2; off < BL; off <<= 1)
+                            v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off, BL));
                         if (lane < 2) P.partials[(pb + i + lane) * nlt + lt] = v;
                     }
                 }
@@ -455,7 +458,7 @@ __global__ void moment_partials_kernel(const double *__restrict__ part, double *
     double *bufA = sm + (size_t)warp * 2 * nvx, *bufB = bufA + nvx;
     const double *src = part + (size_t)p * nvx * nlt;
     for (int k = lane; k < nvx; k += 32) {
-        double tmp[8];
+        double tmp[16];
         for (int t = 0; t < nlt; ++t) tmp[t] = src[(size_t)k * nlt + t];
         bufA[k] = fold_small(tmp, nlt);
     }
@@ -544,13 +547,13 @@ static bool get_map(const double *src, const int Npad[4] /* x,y,vx,vy */, const 
     return true;
 }
 
-// Tile configurations: (BJ, NSTAGE, CK) with BK = 8, BL = 32.  Chosen at run
-// time (VPFV_TCFG overrides; default 0).
-constexpr int TBK = 8, TBL = 32;
+// Tile configurations: (BJ, BL, NSTAGE, CK) with BK = 8.  Chosen at run time
+// (VPFV_TCFG overrides; default 0).
+constexpr int TBK = 8;
 struct TCfg {
-    int bj, ns, ck;
+    int bj, bl, ns, ck;
 };
-static const TCfg kCfgs[] = {{4, 3, 2}, {4, 3, 4}, {4, 2, 2}};
+static const TCfg kCfgs[] = {{4, 32, 3, 2}, {8, 16, 3, 2}, {4, 32, 2, 2}};
 
 static int tile_cfg() {
     static int c = -1;
@@ -562,28 +565,33 @@ static int tile_cfg() {
     return c;
 }
 
+int tma_2d2v_chunk() { return kCfgs[tile_cfg()].bl; }
+
 bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
     const TCfg &c = kCfgs[tile_cfg()];
     if (flags & VPFV_EXACT) return false;
     if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
-    if (Ny % c.bj || Nvx % TBK || Nvy % TBL || (Nvy & 1)) return false;
+    if (Ny % c.bj || Nvx % TBK || Nvy % c.bl || (Nvy & 1)) return false;
     if (Nx < 1 || Ny < 3 + c.bj) return false;
     return encode_fn() != nullptr;
 }
 
-int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / kCfgs[tile_cfg()].bj) * (Nvx / TBK) * (Nvy / TBL); }
+int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
+    const TCfg &c = kCfgs[tile_cfg()];
+    return (Ny / c.bj) * (Nvx / TBK) * (Nvy / c.bl);
+}
 
-template <int BJ, int NS, int CK>
+template <int BJ, int BL, int NS, int CK>
 static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
-    using TL = Tile<BJ, TBK, TBL, NS>;
-    auto kern = stage2d2v_tma_kernel<BJ, TBK, TBL, NS, CK>;
+    using TL = Tile<BJ, TBK, BL, NS>;
+    auto kern = stage2d2v_tma_kernel<BJ, TBK, BL, NS, CK>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM);
         attr = true;
     }
-    const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / TBL) * P.nseg;
-    kern<<<nblocks, BJ * (TBK / CK) * TBL, TL::SMEM, s>>>(maps, P);
+    const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / BL) * P.nseg;
+    kern<<<nblocks, BJ * (TBK / CK) * BL, TL::SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
 }
 
@@ -619,9 +627,9 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
                     unsigned flags, int nseg, cudaStream_t s) {
     const TCfg &c = kCfgs[tile_cfg()];
     const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
-    const int box_core[4] = {TBL + 8, TBK + 6, c.bj, 1};
-    const int box_halo[4] = {TBL + 8, TBK + 6, 3, 1};
-    const int box_op[4] = {TBL + 2, TBK, c.bj, 1};
+    const int box_core[4] = {c.bl + 8, TBK + 6, c.bj, 1};
+    const int box_halo[4] = {c.bl + 8, TBK + 6, 3, 1};
+    const int box_op[4] = {c.bl + 2, TBK, c.bj, 1};
     Maps maps;
     if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_halo, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
@@ -645,15 +653,15 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     P.sj = sjk[0] > 0 ? sjk[0] : 1;
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
     switch (tile_cfg()) {
-        case 1: return launch_cfg<4, 3, 4>(maps, P, s);
-        case 2: return launch_cfg<4, 2, 2>(maps, P, s);
-        default: return launch_cfg<4, 3, 2>(maps, P, s);
+        case 1: return launch_cfg<8, 16, 3, 2>(maps, P, s);
+        case 2: return launch_cfg<4, 32, 2, 2>(maps, P, s);
+        default: return launch_cfg<4, 32, 3, 2>(maps, P, s);
     }
 }
 
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
                                 cudaStream_t s) {
-    if (nlt > 8) return set_error(VPFV_EARG, "moment partials: at most 8 vy chunks");
+    if (nlt > 16) return set_error(VPFV_EARG, "moment partials: at most 16 vy chunks");
     const int wpb = 4;
     size_t smem = sizeof(double) * (size_t)wpb * 2 * nvx;
     static bool attr = false;
@@ -759,5 +767,7 @@ extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys
 }
 
 extern "C" int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
-    return tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) && Nvy / 32 <= 8 ? 1 : 0;
+    return tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) && Nvy / tma_2d2v_chunk() <= 16 ? 1 : 0;
 }
+
+extern "C" int vpfv_stage_2d2v_partials_chunk(void) { return tma_2d2v_chunk(); }

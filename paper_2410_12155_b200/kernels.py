@@ -94,7 +94,7 @@ class StageTables:
 
     def partials_shape(self):
         g = self.grid
-        return (g.N[0], g.N[1], g.N[2], g.N[3] // 32)
+        return (g.N[0], g.N[1], g.N[2], g.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk())
 
     # -- per-stage tables from E (device arrays on the physical grid) ---------
     def update(self, E, stream, packed=False):

@@ -213,7 +213,7 @@ class DistributedSimulation:
         self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)
         self._n_gather = torch.empty((self.world, S) + phys_loc, dtype=torch.float64, device=self.device)
         self.fuse_moment = all(self.tiled)
-        self.partials = ([torch.empty((self.nloc,) + tuple(lg.N[1:3]) + (lg.N[3] // 32,),
+        self.partials = ([torch.empty((self.nloc,) + tuple(lg.N[1:3]) + (lg.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk(),),
                                       dtype=torch.float64, device=self.device) for lg in self.lgrids]
                          if self.fuse_moment else None)
         self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
