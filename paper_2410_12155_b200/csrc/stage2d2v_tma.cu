@@ -186,8 +186,8 @@ __device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, cons
     }
 }
 
-template <int BJ, int BK, int BL, int NSTAGE, int CK>
-__global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
+template <int BJ, int BK, int BL, int NSTAGE, int CK, int MINB>
+__global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
     stage2d2v_tma_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using TL = Tile<BJ, BK, BL, NSTAGE>;
     constexpr int L = TL::L, KL = TL::KL;
@@ -281,6 +281,8 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
 #pragma unroll
         for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
 
+    int stage_s = 0;
+    unsigned stage_par = 0;
     // Accumulator ring: cell c = p_first + m lives in slot m % 7; the plane
     // loop is unrolled by 7 so every slot index is a compile-time constant.
     for (int blk = 0; blk < nplanes; blk += 7) {
@@ -294,18 +296,21 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                 issue_plane<TL>(stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
                                 cy_core, cy_hi);
             }
-            const bool in_T = (p >= i0 && p < i1);
-            const bool has_m = (p - 1 >= i0 && p - 1 < i1);
-            const bool has_p = (p + 1 >= i0 && p + 1 < i1);
-            const int s = n % NSTAGE;
-            tma::mbar_wait(&bars[s], (n / NSTAGE) & 1);
+            // no range tests: contributions of halo planes land in accumulator
+            // slots of cells outside [i0, i1), which are never finalised
+            const int s = stage_s;
+            tma::mbar_wait(&bars[s], stage_par);
+            if (++stage_s == NSTAGE) {
+                stage_s = 0;
+                stage_par ^= 1u;
+            }
             const double *stage = stages + s * TL::STAGE_ELEMS;
             const double *c0 = stage + off;
             const double *tb = stage + TL::ELEMS + 3 * TL::OELEMS + a * 8;  // row p-1, this j
             const double evx = tb[BJ * 8 + 0], evy = tb[BJ * 8 + 1];
-            const double c3 = in_T ? tb[BJ * 8 + 3] : 0.0, c4 = in_T ? tb[BJ * 8 + 4] : 0.0;
-            const double c1m = has_m ? tb[2] : 0.0, c5m = has_m ? tb[5] : 0.0;
-            const double c1p = has_p ? tb[2 * BJ * 8 + 2] : 0.0, c5p = has_p ? tb[2 * BJ * 8 + 5] : 0.0;
+            const double c3 = tb[BJ * 8 + 3], c4 = tb[BJ * 8 + 4];
+            const double c1m = tb[2], c5m = tb[5];
+            const double c1p = tb[2 * BJ * 8 + 2], c5p = tb[2 * BJ * 8 + 5];
 
             const double avx = evx + cBvy;
             const double avx_s = avx * mhvx;
@@ -351,11 +356,10 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, 1)
                 acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
                 acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
 #endif
-#ifndef VPFV_EXP_SKIP_T
-                if (in_T) {
-#else
-                if (in_T && P.Nx < 0) {
+#ifdef VPFV_EXP_SKIP_T
+                if (P.Nx < 0)
 #endif
+                {
                     const double avy = evy + bvx[i];
                     double wy, wvx;
                     if (ypos) {
@@ -553,14 +557,14 @@ constexpr int TBK = 8;
 struct TCfg {
     int bj, bl, ns, ck;
 };
-static const TCfg kCfgs[] = {{4, 32, 3, 2}, {8, 16, 3, 2}, {4, 32, 2, 2}};
+static const TCfg kCfgs[] = {{4, 32, 3, 2}, {8, 16, 3, 2}, {4, 32, 2, 2}, {4, 16, 2, 2}, {2, 32, 2, 2}};
 
 static int tile_cfg() {
     static int c = -1;
     if (c < 0) {
         const char *e = getenv("VPFV_TCFG");
         c = e ? atoi(e) : 0;
-        if (c < 0 || c > 2) c = 0;
+        if (c < 0 || c > 4) c = 0;
     }
     return c;
 }
@@ -581,10 +585,10 @@ int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
     return (Ny / c.bj) * (Nvx / TBK) * (Nvy / c.bl);
 }
 
-template <int BJ, int BL, int NS, int CK>
+template <int BJ, int BL, int NS, int CK, int MINB = 1>
 static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
     using TL = Tile<BJ, TBK, BL, NS>;
-    auto kern = stage2d2v_tma_kernel<BJ, TBK, BL, NS, CK>;
+    auto kern = stage2d2v_tma_kernel<BJ, TBK, BL, NS, CK, MINB>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM);
@@ -655,6 +659,8 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     switch (tile_cfg()) {
         case 1: return launch_cfg<8, 16, 3, 2>(maps, P, s);
         case 2: return launch_cfg<4, 32, 2, 2>(maps, P, s);
+        case 3: return launch_cfg<4, 16, 2, 2, 2>(maps, P, s);
+        case 4: return launch_cfg<2, 32, 2, 2, 2>(maps, P, s);
         default: return launch_cfg<4, 32, 3, 2>(maps, P, s);
     }
 }
