@@ -102,6 +102,21 @@ int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const 
                           unsigned long long *nonfinite, const double *packed_tables,
                           double *moment_partials, int xsegments, void *stream);
 
+/* 1D-2V with the tiled x-marching kernel and optional fused moment partials
+ * [Nx][Nvx][Nvy/32] (finish with vpfv_moment_partials(nphys = Nx)); tiled
+ * when packed_tables (vpfv_tables_1d_packed) is given, the fast path is
+ * requested, velocity ghosts are stored and Nvx % 32 == Nvy % 32 == 0;
+ * otherwise the generic kernel (and moment_partials must be NULL). */
+int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const double *src,
+                          double ca, double cb, double cd, double cL,
+                          const double *vxc, const double *vyc, const double *evx,
+                          const double *avy, const double *c1, double c2,
+                          double hx, double hvx, double hvy, int Nx, int Nvx, int Nvy,
+                          unsigned flags, const double *dt_dev, double cL_div,
+                          unsigned long long *nonfinite, const double *packed_tables,
+                          double *moment_partials, int xsegments, void *stream);
+int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags);
+
 /* 1 when vpfv_stage_2d2v_fused would take the tiled path (and so accepts
  * moment_partials) for these extents and flags, else 0. */
 int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
@@ -164,6 +179,11 @@ int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, double *evy,
                    double *c1, double *c3, double *c4, double *c5, int Nx, int Ny,
                    double qmk2, double nqmk2, double gx, double gy,
                    double t1, double t4, double denx, double deny, void *stream);
+
+/* 1D tables packed for the tiled 1D-2V kernel: packed[(Nx+2)][8] =
+ * (evx, c1, 0, ...) with periodic ghost rows 0 (= x Nx-1) and Nx+1 (= x 0). */
+int vpfv_tables_1d_packed(const double *Ex, double *packed, int Nx, double qmk2, double g,
+                          double t1, double den1, void *stream);
 
 /* The same 2D tables packed for the tiled kernel: packed[(Nx+2)][Ny][8] =
  * (evx, evy, c1, c3, c4, c5, 0, 0) with x rows shifted by one and periodic

@@ -47,6 +47,10 @@ SIGNATURES = {
                                 + [_d] * 4 + [_i] * 4 + [_u, _p, _d, _p, _p]),
     "vpfv_moment_partials": (_i, [_p, _p, _i, _i, _i, _d, _p]),
     "vpfv_stage_2d2v_tiled_ok": (_i, [_i, _i, _i, _i, _u]),
+    "vpfv_stage_1d2v_fused": (_i, [_p] * 4 + [_d] * 4 + [_p] * 5 + [_d] * 4 + [_i] * 3
+                              + [_u, _p, _d, _p, _p, _p, _i, _p]),
+    "vpfv_stage_1d2v_tiled_ok": (_i, [_i, _i, _i, _u]),
+    "vpfv_tables_1d_packed": (_i, [_p, _p, _i, _d, _d, _d, _d, _p]),
     "vpfv_stage_2d2v_partials_chunk": (_i, []),
     "vpfv_moment": (_i, [_p, _p, _i, _i, _p, _d, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
@@ -100,7 +104,7 @@ def check_device(dev: int):
 # kernels launched per entry-point call (for launch accounting); default 1
 KERNELS_PER_CALL = {"vpfv_poisson_2d": 3, "vpfv_version": 0, "vpfv_check_device": 0,
                     "vpfv_last_error": 0, "vpfv_stage_2d2v_tiled_ok": 0,
-                    "vpfv_stage_2d2v_partials_chunk": 0}
+                    "vpfv_stage_2d2v_partials_chunk": 0, "vpfv_stage_1d2v_tiled_ok": 0}
 launch_counter = [0]
 
 

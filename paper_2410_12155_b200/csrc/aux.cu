@@ -60,6 +60,20 @@ __global__ void tables2d_kernel(const double *__restrict__ Ex, const double *__r
     c5[p] = __ddiv_rn(__dmul_rn(nqmk2, dEy_x), deny);
 }
 
+// packed layout for the tiled 1D-2V kernel: tab[(Nx+2)][8] = (evx, c1, 0...),
+// rows shifted by one with periodic ghost rows 0 and Nx+1.
+__global__ void tables1d_packed_kernel(const double *__restrict__ E, double *__restrict__ tab, int n,
+                                       double qmk2, double g, double t1, double den1) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n + 2) return;
+    const int i = r == 0 ? n - 1 : (r == n + 1 ? 0 : r - 1);
+    const double dE = __dsub_rn(E[i + 1 < n ? i + 1 : 0], E[i > 0 ? i - 1 : n - 1]);
+    double *o = tab + (size_t)r * 8;
+    o[0] = __dadd_rn(__dmul_rn(qmk2, E[i]), g);
+    o[1] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, dE), den1));
+    for (int k = 2; k < 8; ++k) o[k] = 0.0;
+}
+
 // packed layout for the tiled 2D-2V kernel: tab[(Nx+2)][Ny][8] =
 // (evx, evy, c1, c3, c4, c5, 0, 0), x rows shifted by one with periodic ghost
 // rows 0 and Nx+1, so one TMA box brings planes p-1, p, p+1.
@@ -154,6 +168,13 @@ extern "C" int vpfv_tables_1d(const double *Ex, double *e, double *c1, int Nx, d
     tables1d_kernel<<<(Nx + 255) / 256, 256, 0, (cudaStream_t)stream>>>(Ex, e, c1, Nx, qmk2, g, t1,
                                                                        den1);
     return check_launch("tables_1d");
+}
+
+extern "C" int vpfv_tables_1d_packed(const double *Ex, double *packed, int Nx, double qmk2, double g,
+                                     double t1, double den1, void *stream) {
+    tables1d_packed_kernel<<<(Nx + 2 + 255) / 256, 256, 0, (cudaStream_t)stream>>>(Ex, packed, Nx, qmk2, g,
+                                                                                  t1, den1);
+    return check_launch("tables_1d_packed");
 }
 
 extern "C" int vpfv_tables_2d(const double *Ex, const double *Ey, double *evx, double *evy,

@@ -36,60 +36,11 @@
 #include <unordered_map>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace vpfv {
 
-namespace tma {
 
-__device__ __forceinline__ unsigned smem_addr(const void *p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void load4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
-                                       int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-}
-
-__device__ __forceinline__ void load3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
-                                       int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-}  // namespace tma
 
 struct Stage22 {
     double *dest;
@@ -485,72 +436,6 @@ __global__ void moment_partials_kernel(const double *__restrict__ part, double *
 // ---------------------------------------------------------------------------
 // host side: tensor maps and launch
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    });
-    return fn;
-}
-
-struct MapKey {
-    const void *ptr;
-    int n[4];
-    int box[4];
-    bool operator==(const MapKey &o) const {
-        if (ptr != o.ptr) return false;
-        for (int i = 0; i < 4; ++i)
-            if (n[i] != o.n[i] || box[i] != o.box[i]) return false;
-        return true;
-    }
-};
-struct MapKeyHash {
-    size_t operator()(const MapKey &k) const {
-        size_t h = reinterpret_cast<size_t>(k.ptr);
-        for (int i = 0; i < 4; ++i) h = h * 1000003u ^ (size_t)(k.n[i] * 131 + k.box[i]);
-        return h;
-    }
-};
-
-static bool get_map(const double *src, const int Npad[4] /* x,y,vx,vy */, const int box[4] /* l,k,j,i */,
-                    CUtensorMap *out) {
-    static std::mutex mu;
-    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-    MapKey key{src, {Npad[0], Npad[1], Npad[2], Npad[3]}, {box[0], box[1], box[2], box[3]}};
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-        *out = it->second;
-        return true;
-    }
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[4] = {(cuuint64_t)Npad[3], (cuuint64_t)Npad[2], (cuuint64_t)Npad[1], (cuuint64_t)Npad[0]};
-    cuuint64_t strides[3] = {(cuuint64_t)Npad[3] * 8, (cuuint64_t)Npad[3] * Npad[2] * 8,
-                             (cuuint64_t)Npad[3] * Npad[2] * Npad[1] * 8};
-    cuuint32_t bdim[4] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2], (cuuint32_t)box[3]};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUtensorMap m;
-    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(src), dims, strides, bdim,
-                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return false;
-    if (cache.size() > 256) cache.clear();
-    cache.emplace(key, m);
-    *out = m;
-    return true;
-}
-
 // Tile configurations: (BJ, BL, NSTAGE, CK) with BK = 8.  Chosen at run time
 // (VPFV_TCFG overrides; default 0).
 constexpr int TBK = 8;
@@ -577,7 +462,7 @@ bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
     if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
     if (Ny % c.bj || Nvx % TBK || Nvy % c.bl || (Nvy & 1)) return false;
     if (Nx < 1 || Ny < 3 + c.bj) return false;
-    return encode_fn() != nullptr;
+    return tma_available();
 }
 
 int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
@@ -600,33 +485,6 @@ static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
 }
 
 // ops: up to three (coefficient, array) RK operands, already de-duplicated
-static bool get_tab_map(const double *tab, int Nx, int Ny, int bj, CUtensorMap *out) {
-    static std::mutex mu;
-    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-    MapKey key{tab, {Nx, Ny, 8, -1}, {8, bj, 3, -1}};
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-        *out = it->second;
-        return true;
-    }
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[3] = {8, (cuuint64_t)Ny, (cuuint64_t)Nx + 2};
-    cuuint64_t strides[2] = {64, (cuuint64_t)Ny * 64};
-    cuuint32_t bdim[3] = {8, (cuuint32_t)bj, 3};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUtensorMap m;
-    if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(tab), dims, strides, bdim, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    if (cache.size() > 256) cache.clear();
-    cache.emplace(key, m);
-    *out = m;
-    return true;
-}
-
 int launch_tma_2d2v(const double *src, const double *const ops[3], const double *tab, Stage22 P,
                     unsigned flags, int nseg, cudaStream_t s) {
     const TCfg &c = kCfgs[tile_cfg()];
@@ -635,12 +493,28 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     const int box_halo[4] = {c.bl + 8, TBK + 6, 3, 1};
     const int box_op[4] = {c.bl + 2, TBK, c.bj, 1};
     Maps maps;
-    if (!get_map(src, Npad, box_core, &maps.core) || !get_map(src, Npad, box_halo, &maps.halo))
+    // 4D fp64 padded arrays, innermost (vy) first
+    const unsigned long long dims[4] = {(unsigned long long)Npad[3], (unsigned long long)Npad[2],
+                                        (unsigned long long)Npad[1], (unsigned long long)Npad[0]};
+    const unsigned long long strides[3] = {dims[0] * 8, dims[0] * dims[1] * 8, dims[0] * dims[1] * dims[2] * 8};
+    auto box4 = [](const int *b) {
+        struct B {
+            unsigned v[4];
+        } r{{(unsigned)b[0], (unsigned)b[1], (unsigned)b[2], (unsigned)b[3]}};
+        return r;
+    };
+    const auto bc = box4(box_core), bh = box4(box_halo), bo = box4(box_op);
+    if (!tma_map(src, 4, dims, strides, bc.v, &maps.core) || !tma_map(src, 4, dims, strides, bh.v, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
     for (int o = 0; o < P.nops; ++o)
-        if (!get_map(ops[o], Npad, box_op, &maps.op[o])) return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
+        if (!tma_map(ops[o], 4, dims, strides, bo.v, &maps.op[o]))
+            return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
     for (int o = P.nops; o < 3; ++o) maps.op[o] = maps.core;
-    if (!get_tab_map(tab, P.Nx, P.Ny, c.bj, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
+    // packed tables [(Nx+2)][Ny][8]
+    const unsigned long long tdims[3] = {8, (unsigned long long)P.Ny, (unsigned long long)P.Nx + 2};
+    const unsigned long long tstr[2] = {64, (unsigned long long)P.Ny * 64};
+    const unsigned tbox[3] = {8, (unsigned)c.bj, 3};
+    if (!tma_map(tab, 3, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
     P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
     P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
     P.i0 = 0;

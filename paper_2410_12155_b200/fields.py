@@ -97,7 +97,7 @@ class FieldSolver:
             if part is None:
                 raise ValueError("species without fused moment partials")
             _lib.call("vpfv_moment_partials", part.data_ptr(), self.n[s].data_ptr(), self.nphys,
-                      g.N[2], part.shape[-1], self.vols[s], stream)
+                      g.N[g.d], part.shape[-1], self.vols[s], stream)
         return self.n
 
     def solve_from_partials(self, partials, stream=None):

@@ -69,6 +69,8 @@ class StageTables:
             self.t1, self.den1 = h[1] / (48.0 * h[0]), 96.0 * h[1]
             self.e = torch.empty(phys_shape, dtype=torch.float64, device=device)   # evx
             self.c1 = torch.empty(phys_shape, dtype=torch.float64, device=device)
+            # packed (evx, c1) rows with periodic x ghost rows, for the tiled kernel
+            self.packed = torch.zeros((g.N[0] + 2, 8), dtype=torch.float64, device=device)
         else:
             self.vxc = dev(g.centers(2))
             self.vyc = dev(g.centers(3))
@@ -84,17 +86,22 @@ class StageTables:
         self.nphys = nphys
 
     def fused_moment_ok(self, flags):
-        """True when the TMA-tiled 2D-2V kernel (and its fused moment) applies."""
+        """True when a TMA-tiled kernel (2D-2V or 1D-2V, with its fused
+        moment epilogue) applies to this grid and these flags."""
         g = self.grid
-        if (g.d, g.v) != (2, 2) or flags & _lib.VPFV_EXACT:
+        if flags & _lib.VPFV_EXACT:
             return False
-        if flags & (_lib.VPFV_WRAP(2) | _lib.VPFV_WRAP(3)):
-            return False
-        return bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*g.N, flags))
+        if (g.d, g.v) == (2, 2):
+            return bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*g.N, flags))
+        if (g.d, g.v) == (1, 2):
+            return bool(_lib.load().vpfv_stage_1d2v_tiled_ok(*g.N, flags))
+        return False
 
     def partials_shape(self):
         g = self.grid
-        return (g.N[0], g.N[1], g.N[2], g.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk())
+        if (g.d, g.v) == (2, 2):
+            return (g.N[0], g.N[1], g.N[2], g.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk())
+        return (g.N[0], g.N[1], g.N[2] // 32)
 
     # -- per-stage tables from E (device arrays on the physical grid) ---------
     def update(self, E, stream, packed=False):
@@ -103,10 +110,16 @@ class StageTables:
         g = self.grid
         if g.d == 1:
             Ex = E["Ex"]
-            _lib.call("vpfv_tables_1d", Ex.data_ptr(), self.e.data_ptr(), self.c1.data_ptr(),
-                      g.N[0], self.qmk2, self.gx, self.t1, self.den1, stream)
-            if not self.corrections:
-                self.c1.zero_()
+            if packed:
+                _lib.call("vpfv_tables_1d_packed", Ex.data_ptr(), self.packed.data_ptr(), g.N[0],
+                          self.qmk2, self.gx, self.t1, self.den1, stream)
+                if not self.corrections:
+                    self.packed[:, 1].zero_()
+            else:
+                _lib.call("vpfv_tables_1d", Ex.data_ptr(), self.e.data_ptr(), self.c1.data_ptr(),
+                          g.N[0], self.qmk2, self.gx, self.t1, self.den1, stream)
+                if not self.corrections:
+                    self.c1.zero_()
         else:
             common = (g.N[0], g.N[1], self.qmk2, self.nqmk2, self.gx, self.gy, self.t1, self.t4,
                       self.denx, self.deny, stream)
@@ -134,9 +147,14 @@ class StageTables:
             _lib.call("vpfv_stage_1d1v", *head, self.ax.data_ptr(), self.e.data_ptr(),
                       self.c1.data_ptr(), h[0], h[1], N[0], N[1], *common_tail)
         elif (g.d, g.v) == (1, 2):
-            _lib.call("vpfv_stage_1d2v", *head, self.vxc.data_ptr(), self.vyc.data_ptr(),
-                      self.e.data_ptr(), self.avy.data_ptr(), self.c1.data_ptr(), self.c2,
-                      h[0], h[1], h[2], N[0], N[1], N[2], *common_tail)
+            args = (*head, self.vxc.data_ptr(), self.vyc.data_ptr(), self.e.data_ptr(),
+                    self.avy.data_ptr(), self.c1.data_ptr(), self.c2, h[0], h[1], h[2], N[0], N[1], N[2])
+            if packed or partials is not None:
+                _lib.call("vpfv_stage_1d2v_fused", *args, flags, _ptr(dt_dev), float(cL_div),
+                          _ptr(nonfinite), self.packed.data_ptr() if packed else None,
+                          _ptr(partials), 0, stream)
+            else:
+                _lib.call("vpfv_stage_1d2v", *args, *common_tail)
         else:
             args = (*head, self.vxc.data_ptr(), self.vyc.data_ptr(), self.evx.data_ptr(),
                     self.evy.data_ptr(), self.cB, self.c1.data_ptr(), self.c2, self.c3.data_ptr(),

@@ -136,6 +136,16 @@ class SlabExchange:
         return bool(t.item())
 
 
+class _GridView:
+    """Minimal stand-in carrying a slab grid, for StageTables' shape queries."""
+
+    def __init__(self, tables, lgrid):
+        self.grid = lgrid
+
+    fused_moment_ok = StageTables.fused_moment_ok
+    partials_shape = StageTables.partials_shape
+
+
 class _LocalTables:
     """A StageTables view launching on the local slab with table pointers
     offset to the slab's first x row of the global tables."""
@@ -160,8 +170,14 @@ class _LocalTables:
             _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr(), ptr(t.e), ptr(t.c1), h[0], h[1],
                       N[0], N[1], *tail, stream)
         elif (g.d, g.v) == (1, 2):
-            _lib.call("vpfv_stage_1d2v", *head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.e),
-                      t.avy.data_ptr(), ptr(t.c1), t.c2, h[0], h[1], h[2], N[0], N[1], N[2], *tail, stream)
+            args = (*head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.e), t.avy.data_ptr(), ptr(t.c1), t.c2,
+                    h[0], h[1], h[2], N[0], N[1], N[2])
+            if packed or partials is not None:
+                pk = t.packed.data_ptr() + self.x0 * 8 * 8 if packed else None
+                _lib.call("vpfv_stage_1d2v_fused", *args, *tail, pk,
+                          None if partials is None else partials.data_ptr(), 0, stream)
+            else:
+                _lib.call("vpfv_stage_1d2v", *args, *tail, stream)
         else:
             args = (*head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.evx), ptr(t.evy), t.cB, ptr(t.c1),
                     t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3])
@@ -204,8 +220,7 @@ class DistributedSimulation:
         # x is exchanged (read from ghost storage); other periodic dims wrap in-kernel
         self.flags = [base | sum(_lib.VPFV_WRAP(k) for k in range(1, lg.ndim) if lg.periodic[k])
                       for lg in self.lgrids]
-        self.tiled = [bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*lg.N, fl)) if lg.ndim == 4 else False
-                      for lg, fl in zip(self.lgrids, self.flags)]
+        self.tiled = [_GridView(t, lg).fused_moment_ok(fl) for t, lg, fl in zip(self.gtables, self.lgrids, self.flags)]
         self.tables = [_LocalTables(t, lg, self.x0) for t, lg in zip(self.gtables, self.lgrids)]
         self.fields = FieldSolver(self.grids, self.species, self.device)
         S = len(self.species)
@@ -213,9 +228,8 @@ class DistributedSimulation:
         self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)
         self._n_gather = torch.empty((self.world, S) + phys_loc, dtype=torch.float64, device=self.device)
         self.fuse_moment = all(self.tiled)
-        self.partials = ([torch.empty((self.nloc,) + tuple(lg.N[1:3]) + (lg.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk(),),
-                                      dtype=torch.float64, device=self.device) for lg in self.lgrids]
-                         if self.fuse_moment else None)
+        self.partials = ([torch.empty(_GridView(t, lg).partials_shape(), dtype=torch.float64, device=self.device)
+                          for t, lg in zip(self.gtables, self.lgrids)] if self.fuse_moment else None)
         self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
         self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._timing = False
@@ -241,7 +255,7 @@ class DistributedSimulation:
         for s, (lg, f) in enumerate(zip(self.lgrids, srcs)):
             if from_partials:
                 _lib.call("vpfv_moment_partials", self.partials[s].data_ptr(), self.n_local[s].data_ptr(),
-                          int(np.prod(lg.N[:lg.d])), lg.N[2], self.partials[s].shape[-1],
+                          int(np.prod(lg.N[:lg.d])), lg.N[lg.d], self.partials[s].shape[-1],
                           self.fields.vols[s], stream)
             else:
                 _lib.call("vpfv_moment", f.data_ptr(), self.n_local[s].data_ptr(), lg.d, lg.v,

@@ -416,3 +416,86 @@ def test_landau2d_steps_fused_path_vs_c_oracle(N):
         sim.advance(dt)
         ref.advance(dt)
         assert rel_l2(sim.interiors()[0], ref.interiors()[0]) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# the TMA-tiled 1D-2V kernel
+
+
+def _tiled12_case(N, seed):
+    g = O.Grid(1, 2, N, (0.0, -4.0, -6.0), (2 * np.pi, 4.0, 6.0), (True, False, False))
+    rng = np.random.default_rng(seed)
+    src = 1.0 + 0.3 * rng.random(g.padded_shape)
+    O.fill_ghosts(src, g, O.capture_frozen(src, g))
+    E = {"Ex": 0.4 * np.sin(g.centers(0)) + 0.05}
+    sp = O.Species("e", -1.0, 1.0, 1.1, 0.3, 1.0, (0.02, -0.01))
+    return g, sp, src, E, rng
+
+
+@pytest.mark.parametrize("N", [(8, 32, 32), (12, 64, 32), (9, 32, 96)])
+@pytest.mark.parametrize("coef", [(1.0, 0.0, 0.0, 0.01), (2.0, -1.0, 0.0, 0.03), (-1.0, 0.0, 2.0, 0.03),
+                                  (-0.125, 0.375, 0.75, 0.00375)])
+def test_tiled12_stage_vs_oracle(N, coef):
+    g, sp, src, E, rng = _tiled12_case(N, sum(N))
+    A, dest0 = rng.random(g.padded_shape), rng.random(g.padded_shape)
+    ca, cb, cd, cL = coef
+    want = dest0.copy()
+    O.fused_stage(want, A, src, src, ca, cb, cd, cL, g, sp, E, check=False)
+    got = dest0.copy()
+    pg = pgrid(g)
+    assert K.StageTables(pg, sp, torch.device("cuda")).fused_moment_ok(0)
+    K.fused_stage(got, A, src, src, ca, cb, cd, cL, pg, sp, E, exact=False)
+    inner = g.inner()
+    assert np.max(np.abs(got[inner] - want[inner])) <= 2e-14 * np.max(np.abs(want[inner]))
+    assert np.array_equal(got[~_interior_mask(g)], dest0[~_interior_mask(g)])
+
+
+def test_tiled12_wrap_and_fused_moment():
+    N = (16, 32, 64)
+    g, sp, src, E, rng = _tiled12_case(N, 5)
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    bad = src.copy()
+    bad[:3] = np.nan
+    bad[-3:] = np.nan
+    want = np.zeros(g.padded_shape)
+    O.fused_stage(want, src, src, src, 1.0, 0.0, 0.0, 0.02, g, sp, E, check=False)
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({k: dev(v) for k, v in E.items()}, stream, packed=True)
+    flags = K.wrap_flags(pg)
+    assert tab.fused_moment_ok(flags)
+    d_src = dev(bad)
+    d_dest = torch.zeros_like(d_src)
+    part = torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda")
+    nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    tab.launch(d_dest, d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, nonfinite=nf, partials=part,
+               packed=True)
+    got = d_dest.cpu().numpy()
+    inner = g.inner()
+    assert int(nf.item()) == -1
+    assert np.max(np.abs(got[inner] - want[inner])) <= 2e-14 * np.max(np.abs(want[inner]))
+    n = torch.empty((N[0],), dtype=torch.float64, device="cuda")
+    _lib.call("vpfv_moment_partials", part.data_ptr(), n.data_ptr(), N[0], N[1], part.shape[-1],
+              O.velocity_volume(g), stream)
+    assert np.array_equal(n.cpu().numpy(), O.zeroth_moment(got, g))
+
+
+@pytest.mark.parametrize("maker", ["bimax", "lhdi", "dgh"])
+def test_1d2v_fused_path_steps_vs_c_oracle(maker):
+    from oracle import cbackend as C
+
+    mk = {"bimax": lambda: P.make_bimaxwellian_1d2v(32, 64, 32),
+          "lhdi": lambda: P.make_problem(P.ProblemSpec("lhdi"), 16, 32),
+          "dgh": lambda: P.make_problem(P.ProblemSpec("dgh"), 16, 32)}[maker]
+    setup = mk()
+    sim = R.Simulation(setup)
+    assert sim.fuse_moment
+    dt = 0.9 * sim.max_dt()
+    sim.fixed_dt = dt
+    ref = C.CSimulation([f.grid for f in setup.dists], setup.species, [f.data for f in mk().dists], dt=dt)
+    for _ in range(3):
+        sim.advance(dt)
+        ref.advance(dt)
+        for a, b in zip(sim.interiors(), ref.interiors()):
+            assert rel_l2(a, b) <= 1e-12

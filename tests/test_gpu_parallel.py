@@ -28,7 +28,7 @@ def _setup(name):
     if name == "twostream":
         return P.make_problem(P.ProblemSpec("two-stream"), 64, 64)
     if name == "lhdi":
-        return P.make_problem(P.ProblemSpec("lhdi"), 16, 16)
+        return P.make_problem(P.ProblemSpec("lhdi"), 16, 32)
     return P.make_electron_proton_2d2v(16, 32)
 
 
