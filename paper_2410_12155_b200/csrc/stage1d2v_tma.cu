@@ -48,25 +48,29 @@ struct Tile12 {
     static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
 };
 
-template <class TL, int BK>
-__device__ __forceinline__ void issue12(double *stages, uint64_t *bars, const Maps12 *M, int n, int p_first,
-                                        int i0, int i1, const Stage12 &P, int l0, int k0, int nstage) {
+// Copies of plane n split into parts issued by different warps (see
+// issue_part in stage2d2v_tma.cu): 0 = expect_tx + tables, 1 = halo, 2+o =
+// RK operand o.
+template <class TL>
+__device__ __forceinline__ void issue12(int w, double *stages, uint64_t *bars, const Maps12 *M, int n,
+                                        int p_first, int i0, int i1, const Stage12 &P, int l0, int k0,
+                                        int nstage) {
     const int s = n % nstage;
     double *dst = stages + s * TL::STAGE_ELEMS;
-    const int p = p_first + n;
+    const int p = p_first + n;  // in [-3, Nx + 3)
     int px = p;
-    if (P.wrap_x) {
-        px %= P.Nx;
-        if (px < 0) px += P.Nx;
-    }
+    if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
     const int q = p - 3;
     const bool ops = (q >= i0 && q < i1);
-    tma::mbar_expect_tx(&bars[s], (TL::ELEMS + 24 + (ops ? P.nops * TL::OELEMS : 0)) * 8);
-    tma::load3d(dst, &M->halo, &bars[s], l0, k0, px + NG);
-    tma::load2d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, px);
-    if (ops)
-        for (int o = 0; o < P.nops; ++o)
-            tma::load3d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, q + NG);
+    if (w == 0) {
+        tma::mbar_expect_tx(&bars[s], (TL::ELEMS + 24 + (ops ? P.nops * TL::OELEMS : 0)) * 8);
+        tma::load2d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, px);
+    } else if (w == 1) {
+        tma::load3d(dst, &M->halo, &bars[s], l0, k0, px + NG);
+    } else if (ops && w - 2 < P.nops) {
+        const int o = w - 2;
+        tma::load3d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, q + NG);
+    }
 }
 
 template <int BK, int BL, int NSTAGE, int CK>
@@ -102,7 +106,9 @@ __global__ void __launch_bounds__((BK / CK) * BL, 1)
     const Maps12 *M = &maps;
     if (tid == 0)
         for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
-            issue12<TL, BK>(stages, bars, M, n, p_first, i0, i1, P, l0, k0, NSTAGE);
+            for (int w = 0; w < 5; ++w) issue12<TL>(w, stages, bars, M, n, p_first, i0, i1, P, l0, k0, NSTAGE);
+    const int warp = tid >> 5;
+    const bool issuer = (tid & 31) == 0 && warp < 2 + P.nops;
 
     double ax_s[CK], avy_s[CK];
     bool xpos[CK], vypos[CK];
@@ -139,10 +145,8 @@ __global__ void __launch_bounds__((BK / CK) * BL, 1)
             const int n = blk + r;
             if (n >= nplanes) break;
             const int p = p_first + n;
-            if (tid == 0 && n + NSTAGE - 1 < nplanes) {
-                tma::fence_proxy_async();
-                issue12<TL, BK>(stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, NSTAGE);
-            }
+            if (issuer && n + NSTAGE - 1 < nplanes)
+                issue12<TL>(warp, stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, NSTAGE);
             const int s = stage_s;
             tma::mbar_wait(&bars[s], stage_par);
             if (++stage_s == NSTAGE) {

@@ -108,32 +108,40 @@ __device__ __forceinline__ double warp_tree_sum(double x) {
 }
 
 // Plane n: the src halo tile of plane p = p_first + n, and the RK operand core
-// tiles of cell-plane q = p - 3 when q is updated by this CTA.
+// tiles of cell-plane q = p - 3 when q is updated by this CTA.  The copies of
+// one plane are split into parts (0: expect_tx + tables, 1-3: halo/core/halo,
+// 4+o: operand o) so that a different warp issues each part and no warp
+// carries the whole producer cost (the per-plane barrier waits for the
+// slowest warp).  complete_tx may land before the expect_tx: the mbarrier
+// transaction count is allowed to go transiently negative, and the phase
+// cannot complete before part 0 arrives.
 template <class TL>
-__device__ __forceinline__ void issue_plane(double *stages, uint64_t *bars, const Maps *M, int n,
-                                            int p_first, int i0, int i1, const Stage22 &P, int l0,
-                                            int k0, int j0, int cy_lo, int cy_core, int cy_hi) {
+__device__ __forceinline__ void issue_part(int w, double *stages, uint64_t *bars, const Maps *M, int n,
+                                           int p_first, int i0, int i1, const Stage22 &P, int l0, int k0,
+                                           int j0, int cy_lo, int cy_core, int cy_hi) {
     const int s = n % TL::NSTAGE_;
     double *dst = stages + s * TL::STAGE_ELEMS;
-    const int p = p_first + n;
+    const int p = p_first + n;  // in [-3, Nx + 3)
     int px = p;
-    if (P.wrap_x) {
-        px %= P.Nx;
-        if (px < 0) px += P.Nx;
-    }
+    if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
     const int q = p - 3;
     const bool ops = (q >= i0 && q < i1);
-    tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + TL::TAB_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
     const int cx = px + NG;
-    // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
-    tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
-    tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
-    tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx);
-    tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
-    if (ops) {
-        for (int o = 0; o < P.nops; ++o)
-            tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
-                        q + NG);
+    switch (w) {
+        case 0:
+            tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + TL::TAB_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
+            // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
+            tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
+            break;
+        case 1: tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx); break;
+        case 2: tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx); break;
+        case 3: tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx); break;
+        default: {
+            const int o = w - 4;
+            if (ops && o < P.nops)
+                tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
+                            q + NG);
+        }
     }
 }
 
@@ -197,8 +205,11 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
     const Maps *M = &maps;
     if (tid == 0) {
         for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
-            issue_plane<TL>(stages, bars, M, n, p_first, i0, i1, P, l0, k0, j0, cy_lo, cy_core, cy_hi);
+            for (int w = 0; w < 7; ++w)
+                issue_part<TL>(w, stages, bars, M, n, p_first, i0, i1, P, l0, k0, j0, cy_lo, cy_core, cy_hi);
     }
+    const int warp = tid >> 5;
+    const bool issuer = (tid & 31) == 0 && warp < 4 + P.nops;
 
     double ax_s[CK], bvx[CK];
     bool xpos[CK];
@@ -242,11 +253,9 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
             const int n = blk + r;
             if (n >= nplanes) break;
             const int p = p_first + n;
-            if (tid == 0 && n + NSTAGE - 1 < nplanes) {
-                tma::fence_proxy_async();
-                issue_plane<TL>(stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
-                                cy_core, cy_hi);
-            }
+            if (issuer && n + NSTAGE - 1 < nplanes)
+                issue_part<TL>(warp, stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
+                               cy_core, cy_hi);
             // no range tests: contributions of halo planes land in accumulator
             // slots of cells outside [i0, i1), which are never finalised
             const int s = stage_s;
