@@ -82,11 +82,11 @@ int vpfv_stage_2d2v(double *dest, const double *A, const double *B, const double
 /* 2D-2V stage with the fused velocity-moment epilogue: as vpfv_stage_2d2v,
  * and when moment_partials is non-NULL the kernel also writes, for every new
  * dest cell row (x, y, vx) and every aligned vy chunk c (width
- * vpfv_stage_2d2v_partials_chunk(), 16 or 32), the fold-tree subtree sum
+ * vpfv_stage_2d2v_partials_chunk(), 16), the fold-tree subtree sum
  * moment_partials[((x*Ny + y)*Nvx + vx)*(Nvy/chunk) + c]
  * (finish with vpfv_moment_partials).  Runs the TMA-tiled x-marching kernel
- * (requires the fast path, stored velocity ghosts, Ny%4 == Nvx%8 == Nvy%32
- * == 0); otherwise falls back to the generic kernel (and rejects a non-NULL
+ * (requires the fast path, stored velocity ghosts, Ny%8 == Nvx%16 == Nvy%16
+ * == 0 and at most two RK operands besides src); otherwise falls back to the generic kernel (and rejects a non-NULL
  * moment_partials with VPFV_EARG).  The tiled path reads the E tables from
  * packed_tables (vpfv_tables_2d_packed); with packed_tables NULL the generic
  * kernel runs.  xsegments <= 0 picks a split of the x march automatically.
@@ -122,7 +122,7 @@ int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags);
 int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
 
 /* Width of the vy chunks the fused-moment partials are summed over (the
- * tiled kernel's vy tile, 16 or 32): partials hold Nvy/chunk values per row. */
+ * tiled kernel's vy tile, 16): partials hold Nvy/chunk values per row. */
 int vpfv_stage_2d2v_partials_chunk(void);
 
 /* The untiled one-thread-per-cell 2D-2V kernel (exact or fast), always. */

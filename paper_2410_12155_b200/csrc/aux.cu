@@ -75,8 +75,9 @@ __global__ void tables1d_packed_kernel(const double *__restrict__ E, double *__r
 }
 
 // packed layout for the tiled 2D-2V kernel: tab[(Nx+2)][Ny][8] =
-// (evx, evy, c1, c3, c4, c5, 0, 0), x rows shifted by one with periodic ghost
-// rows 0 and Nx+1, so one TMA box brings planes p-1, p, p+1.
+// (evx, evy, c3, c4, c1, c5, 0, 0) -- the kernel reads (evx, evy, c3, c4) of
+// plane p and (c1, c5) of planes p+-1 -- x rows shifted by one with periodic
+// ghost rows 0 and Nx+1, so one TMA box brings planes p-1, p, p+1.
 __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const double *__restrict__ Ey,
                                        double *__restrict__ tab, int nx, int ny, double qmk2,
                                        double nqmk2, double gx, double gy, double t1, double t4,
@@ -91,10 +92,10 @@ __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const doub
     double *o = tab + (size_t)t * 8;
     o[0] = __dadd_rn(__dmul_rn(qmk2, Ex[p]), gx);
     o[1] = __dadd_rn(__dmul_rn(qmk2, Ey[p]), gy);
-    o[2] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ex[ip], Ex[im])), denx));
-    o[3] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ex[jp], Ex[jm])), denx);
-    o[4] = __dadd_rn(t4, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ey[jp], Ey[jm])), deny));
-    o[5] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ey[ip], Ey[im])), deny);
+    o[4] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ex[ip], Ex[im])), denx));  // c1
+    o[2] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ex[jp], Ex[jm])), denx);                 // c3
+    o[3] = __dadd_rn(t4, __ddiv_rn(__dmul_rn(qmk2, __dsub_rn(Ey[jp], Ey[jm])), deny));  // c4
+    o[5] = __ddiv_rn(__dmul_rn(nqmk2, __dsub_rn(Ey[ip], Ey[im])), deny);                 // c5
     o[6] = 0.0;
     o[7] = 0.0;
 }

@@ -1,174 +1,202 @@
-// 2D-2V fused stage, x-marching with TMA-staged halo tiles (sm_100a, fast path).
+// 2D-2V fused stage: x-marching, TMA-staged halo tiles, 2x4 register blocks
+// (sm_100a, fast arithmetic path).
 //
-// Same operator as stage_2d2v (/root/reference/pkg/src/vpfv/_kernels.py:254-317)
-// with the fast arithmetic policy.  Organisation:
+// Same operator as stage_2d2v (/root/reference/pkg/src/vpfv/_kernels.py:254-317):
+//   rhs = -a_x D_x f - a_y D_y f - a_vx D_vx f - a_vy D_vy f
+//         + c1 diag(x,vx) + c4 diag(y,vy) - c2 diag(vx,vy) - c3 diag(y,vx) - c5 diag(x,vy)
+//   dest = ca A + cb B + cd dest + cL rhs            (interior cells only)
 //
-//  * A CTA owns a (y, vx, vy) = (BJ, BK, BL) block of columns and marches
-//    along x (the slowest dim) over planes p = i0-3 .. i1+2.
-//  * Every plane's (BJ+6, BK+6, BL+8) halo tile (the vy box starts at the
-//    16 B-aligned padded column l0 -- TMA requires an aligned inner start) is copied global -> shared by
-//    the Tensor Memory Accelerator (cp.async.bulk.tensor.4d, one core box plus
-//    two 3-row y-halo boxes so periodic y wraps cost nothing), NSTAGE deep,
-//    completion tracked by mbarrier transaction counts.
-//  * Each thread keeps, per column, 7 register accumulators for the cells
-//    p-3..p+3 currently "in flight" along x.  When plane p lands, it adds
-//      - its x-stencil contribution (a_x/(60 h_x) * w_o * s(p)) to cells p-o,
-//      - the in-plane part T(p): y/vx/vy fluxes + (y,vy),(vx,vy),(y,vx)
-//        corrections, all read from shared memory with immediate offsets,
-//      - the x-coupled corrections through D(p) = s[k-1]-s[k+1] and
-//        G(p) = s[l-1]-s[l+1]:  c1(q)(D(q+1)-D(q-1)) - c5(q)(G(q+1)-G(q-1)),
-//    then finalises cell p-3 with the RK4 stage combination and streams it
-//    to HBM (coalesced 256 B warp rows).
-//  * Optionally the epilogue also emits the velocity-moment partials of the
-//    new dest: a warp-shuffle fold-tree subtree over each aligned 32-wide vy
-//    chunk (bitwise the reference fold tree's first five levels), finished by
-//    vpfv_moment_from_partials.  This saves the separate moment pass over f.
+// Why this shape.  The stencil has radius 3 along four axes plus the
+// (+-1, +-1) diagonals of five axis pairs; it is fp64 and HBM-bound in
+// principle, but every cell's ~31-point footprint has to reach the FP64
+// pipes through the SM's 128 B/clk shared-memory/L1 datapath.  The design
+// therefore minimises datapath bytes per cell:
+//
+//  * A CTA (256 threads, one per SM) owns a (y, vx, vy) = (8, 16, 16)
+//    column block and marches along x (the slowest dim) over planes
+//    p = i0-3 .. i1+2.  The x direction costs no shared-memory traffic: each
+//    thread keeps, per cell, a sliding window of 6 register accumulators for
+//    the cells p-3..p+2 in flight along x and scatters s(p) into them.
+//  * Each plane's (14, 22, 24) halo tile is copied global -> shared by TMA
+//    (cp.async.bulk.tensor.4d: a core box plus two 3-row y-halo boxes, so
+//    periodic y wraps are free), 3 stages deep, completion tracked by
+//    mbarrier transaction counts.  On x-halo planes only the core box moves.
+//  * Each thread owns a 2 (y) x 4 (vx) block of cells at one vy lane; the
+//    block's footprint is 120 shared loads per plane, 15 per cell (one cell
+//    per thread would need 31).  The diagonal corrections are rebuilt from
+//    per-row differences D = s[vx-1]-s[vx+1] and G = s[vy-1]-s[vy+1] that the
+//    x-coupled corrections need anyway:  diag(vx,vy) = G(vx+1)-G(vx-1),
+//    diag(y,vy) = G(y+1)-G(y-1), diag(y,vx) = D(y+1)-D(y-1).
+//  * RK operands that alias src are folded into the accumulator when their
+//    plane is resident (cfold/cL * s(q)), so stage 1 reads only src; other
+//    operands are TMA-staged one plane ahead of their use.
+//  * The epilogue writes dest (coalesced 128 B half-warp rows) and, when
+//    asked, the velocity-moment partials of the new dest: the exact first
+//    four levels of the reference fold tree over each aligned 16-wide vy
+//    chunk (transpose-reduce over the 16 vy lanes), finished by
+//    vpfv_moment_partials.  This replaces a separate moment pass over f.
 //
 // Requirements (checked by the launcher, else the generic kernel runs):
-// Ny % BJ == 0, Nvx % BK == 0, Nvy % BL == 0, even Nvy (16 B TMA strides),
-// periodic-or-halo x/y, stored (frozen) velocity ghosts.
+// Ny % 8 == 0, Nvx % 16 == 0, Nvy % 16 == 0, periodic-or-halo x/y, stored
+// (frozen) velocity ghosts, at most two RK operands besides src.
 #include <cuda.h>
 
 #include <stdio.h>
 #include <stdlib.h>
-
-#include <mutex>
-#include <unordered_map>
 
 #include "common.cuh"
 #include "tma.cuh"
 
 namespace vpfv {
 
-
-
 struct Stage22 {
     double *dest;
+    const double *src;
     double cL;
     const double *dt_dev;
     double cL_div;
-    int nops;          // RK operands staged by TMA (A, B, dest as needed)
-    double opc[3];     // their coefficients
+    int nops;          // RK operands staged by TMA (those that do not alias src)
+    double opc[2];     // their coefficients
+    int fold;          // src is an RK operand too: its coefficient is folded
+    double cfold;
     unsigned long long *nonfinite;
-    const double *vxc, *vyc, *evx, *evy, *c1, *c3, *c4, *c5;
+    const double *vxc, *vyc;
     double cB, c2, mhx, mhy, mhvx, mhvy;
     int Nx, Ny, Nvx, Nvy;
     int wrap_x, wrap_y;
     int i0, i1;        // x range of cells this launch updates (interior indices)
     int nseg, seglen;  // x segments per column block
     int sj, sk;        // super-tile of column blocks (block order)
-    double *partials;  // moment partials [Nx][Ny][Nvx][Nvy/BL] or nullptr
+    double *partials;  // moment partials [Nx][Ny][Nvx][Nvy/16] or nullptr
 };
 
-template <int BJ, int BK, int BL, int NSTAGE>
-struct Tile {
-    static constexpr int J = BJ + 6, K = BK + 6, L = BL + 8;
-    static constexpr int KL = K * L;
-    static constexpr int ELEMS = J * K * L;              // src halo tile
-    static constexpr int OL = BL + 2;                     // operand row (16 B aligned start)
-    static constexpr int OELEMS = BJ * BK * OL;           // one RK operand core tile
-    static constexpr int TELEMS = 3 * BJ * 8;              // packed E tables, planes p-1..p+1
-    static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS + TELEMS;
-    static constexpr int TAB_BYTES = TELEMS * 8;
-    static constexpr int HALO_BYTES = ELEMS * 8, OP_BYTES = OELEMS * 8;
-    static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
-    static constexpr int NSTAGE_ = NSTAGE, BJ_ = BJ, BK_ = BK, BL_ = BL;
-    static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
-};
+namespace rb {
+constexpr int BJ = 8, BK = 16, BL = 16, NS = 3, THREADS = 256;
+constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile extents (vy box starts 16 B aligned)
+constexpr int KL = TK * TW;
+constexpr int HALO = TJ * KL;
+constexpr int TAB = 3 * BJ * 8;  // packed tables of planes p-1, p, p+1
+constexpr int STAGE = HALO + TAB;
+constexpr int OPW = BL + 2;      // RK operand row (16 B aligned start)
+constexpr int OPE = BJ * BK * OPW;
+constexpr int OPS_MAX = 2;
+constexpr int HALO_BYTES = HALO * 8, CORE_BYTES = BJ * KL * 8, TAB_BYTES = TAB * 8, OP_BYTES = OPE * 8;
+constexpr int SMEM = NS * STAGE * 8 + OPS_MAX * OPE * 8 + 64;
+static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
+              "TMA destinations must stay 128 B aligned");
+static_assert(SMEM <= 227 * 1024, "shared memory budget");
+// packed table entry (vpfv_tables_2d_packed): evx, evy, c3, c4, c1, c5, 0, 0
+enum { T_EVX = 0, T_EVY = 1, T_C3 = 2, T_C4 = 3, T_C1 = 4, T_C5 = 5 };
+}  // namespace rb
 
 struct Maps {
-    CUtensorMap core, halo, op[3], tab;
+    CUtensorMap core, halo, op[rb::OPS_MAX], tab;
 };
 
-// upwinded 6-point weighted sum (face difference * 60) along an in-tile
-// direction of stride ST, evaluated as three independent pairs (ILP); the
-// sign test is warp-uniform in practice.
-template <int ST>
-__device__ __forceinline__ double wsum(const double *c, bool pos) {
-    if (pos) {
-        const double t1 = fma(15.0, c[-2 * ST], -2.0 * c[-3 * ST]);
-        const double t2 = fma(20.0, c[0], -60.0 * c[-ST]);
-        const double t3 = fma(-3.0, c[2 * ST], 30.0 * c[ST]);
-        return (t1 + t2) + t3;
+// upwinded 6-point face-difference sums (x 60); offsets -3..2 for a > 0 and
+// -2..3 for a <= 0 (_kernels.py:28-30, ties to the negative branch)
+__device__ __forceinline__ double wpos(double m3, double m2, double m1, double z, double p1, double p2) {
+    return fma(-3.0, p2, fma(30.0, p1, fma(20.0, z, fma(-60.0, m1, fma(15.0, m2, -2.0 * m3)))));
+}
+__device__ __forceinline__ double wneg(double m2, double m1, double z, double p1, double p2, double p3) {
+    return fma(2.0, p3, fma(-15.0, p2, fma(60.0, p1, fma(-20.0, z, fma(-30.0, m1, 3.0 * m2)))));
+}
+
+// Scatter of plane p into the accumulator window and extraction of the
+// finished cell p-3.  Before plane p, acc[i][j] holds cell p-3+j (j < 6);
+// afterwards the window slides by one (cell p+3 enters).  A cell's slot is
+// initialised by its first contribution -- x-stencil offset -3 (a_x > 0) or
+// -2 (a_x <= 0) -- so no slot is zeroed.
+__device__ __forceinline__ void window_apply(double (&acc)[8][6], const double (&s0)[8], const double (&ax_s)[4],
+                                             const bool (&xpos)[4], const double (&Xm)[8], const double (&Xp)[8],
+                                             const double (&T)[8], double (&fin)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double ti = ax_s[i & 3] * s0[i];
+        double nw;
+        if (xpos[i & 3]) {
+            acc[i][5] = fma(15.0, ti, acc[i][5]);
+            acc[i][4] = fma(-60.0, ti, acc[i][4]);
+            acc[i][3] = fma(20.0, ti, acc[i][3]);
+            acc[i][2] = fma(30.0, ti, acc[i][2]);
+            acc[i][1] = fma(-3.0, ti, acc[i][1]);
+            fin[i] = acc[i][0];
+            nw = -2.0 * ti;          // cell p+3
+        } else {
+            acc[i][5] = 3.0 * ti;    // cell p+2 enters
+            acc[i][4] = fma(-30.0, ti, acc[i][4]);
+            acc[i][3] = fma(-20.0, ti, acc[i][3]);
+            acc[i][2] = fma(60.0, ti, acc[i][2]);
+            acc[i][1] = fma(-15.0, ti, acc[i][1]);
+            fin[i] = fma(2.0, ti, acc[i][0]);
+            nw = 0.0;
+        }
+        // x-coupled corrections of cells p-1 and p+1, in-plane terms of cell p
+        acc[i][0] = acc[i][1];
+        acc[i][1] = acc[i][2] + Xm[i];
+        acc[i][2] = acc[i][3] + T[i];
+        acc[i][3] = acc[i][4] + Xp[i];
+        acc[i][4] = acc[i][5];
+        acc[i][5] = nw;
     }
-    const double t1 = fma(-30.0, c[-ST], 3.0 * c[-2 * ST]);
-    const double t2 = fma(60.0, c[ST], -20.0 * c[0]);
-    const double t3 = fma(2.0, c[3 * ST], -15.0 * c[2 * ST]);
-    return (t1 + t2) + t3;
 }
 
-template <int SA, int SB>
-__device__ __forceinline__ double dsum(const double *c) {  // s[+a,-b]+s[-a,+b]-s[+a,+b]-s[-a,-b]
-    return (c[SA - SB] + c[-SA + SB]) - (c[SA + SB] + c[-SA - SB]);
-}
-
-__device__ __forceinline__ double warp_tree_sum(double x) {
-    for (int off = 1; off < 32; off <<= 1) x = __dadd_rn(x, __shfl_down_sync(0xffffffffu, x, off));
-    return x;
-}
-
-// Plane n: the src halo tile of plane p = p_first + n, and the RK operand core
-// tiles of cell-plane q = p - 3 when q is updated by this CTA.  The copies of
-// one plane are split into parts (0: expect_tx + tables, 1-3: halo/core/halo,
-// 4+o: operand o) so that a different warp issues each part and no warp
-// carries the whole producer cost (the per-plane barrier waits for the
-// slowest warp).  complete_tx may land before the expect_tx: the mbarrier
-// transaction count is allowed to go transiently negative, and the phase
-// cannot complete before part 0 arrives.
-template <class TL>
-__device__ __forceinline__ void issue_part(int w, double *stages, uint64_t *bars, const Maps *M, int n,
-                                           int p_first, int i0, int i1, const Stage22 &P, int l0, int k0,
-                                           int j0, int cy_lo, int cy_core, int cy_hi) {
-    const int s = n % TL::NSTAGE_;
-    double *dst = stages + s * TL::STAGE_ELEMS;
-    const int p = p_first + n;  // in [-3, Nx + 3)
+// One plane's copies are split into parts issued by different warps so that
+// no warp carries the whole producer cost: 0 = expect_tx + tables, 1-3 =
+// y-low halo / core / y-high halo.  complete_tx may land before expect_tx
+// (the transaction count may go transiently negative; the phase cannot
+// complete before part 0 arrives).  On x-halo planes only the core moves.
+__device__ __forceinline__ void issue_plane_part(int w, double *stages, uint64_t *bars, const Maps *M, int n,
+                                                 int p_first, const Stage22 &P, int i0, int i1, int l0, int k0,
+                                                 int j0, int cy_lo, int cy_core, int cy_hi) {
+    using namespace rb;
+    const int s = n % NS;
+    double *dst = stages + s * STAGE;
+    const int p = p_first + n;  // in [i0-3, i1+3)
     int px = p;
     if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
-    const int q = p - 3;
-    const bool ops = (q >= i0 && q < i1);
+    const bool inner = p >= i0 && p < i1;
     const int cx = px + NG;
     switch (w) {
         case 0:
-            tma::mbar_expect_tx(&bars[s], TL::HALO_BYTES + TL::TAB_BYTES + (ops ? P.nops * TL::OP_BYTES : 0));
-            // packed tables rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
-            tma::load3d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, j0, px);
+            tma::mbar_expect_tx(&bars[s], (inner ? HALO_BYTES : CORE_BYTES) + TAB_BYTES);
+            // packed table rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
+            tma::load3d(dst + HALO, &M->tab, &bars[s], 0, j0, px);
             break;
-        case 1: tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx); break;
-        case 2: tma::load4d(dst + 3 * TL::KL, &M->core, &bars[s], l0, k0, cy_core, cx); break;
-        case 3: tma::load4d(dst + (3 + TL::BJ_) * TL::KL, &M->halo, &bars[s], l0, k0, cy_hi, cx); break;
-        default: {
-            const int o = w - 4;
-            if (ops && o < P.nops)
-                tma::load4d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, j0 + NG,
-                            q + NG);
-        }
+        case 1:
+            if (inner) tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
+            break;
+        case 2: tma::load4d(dst + 3 * KL, &M->core, &bars[s], l0, k0, cy_core, cx); break;
+        case 3:
+            if (inner) tma::load4d(dst + (3 + BJ) * KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
+            break;
+        default: break;
     }
 }
 
-template <int BJ, int BK, int BL, int NSTAGE, int CK, int MINB>
-__global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
-    stage2d2v_tma_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
-    using TL = Tile<BJ, BK, BL, NSTAGE>;
-    constexpr int L = TL::L, KL = TL::KL;
+__global__ void __launch_bounds__(rb::THREADS, 1)
+    stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
+    using namespace rb;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::STAGE_ELEMS * 8);
+    double *opbuf = stages + NS * STAGE;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(opbuf + OPS_MAX * OPE);  // NS stage barriers + 1 operand barrier
+    uint64_t *opbar = bars + NS;
 
     const int tid = threadIdx.x;
     // column block; x segment outermost so the CTAs resident at once cover
     // neighbouring column blocks of the same x range (halo reuse in L2)
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK, njt = P.Ny / BJ;
     const int ncols = nlt * nkt * njt;
-    int b = blockIdx.x % ncols;
+    int blk = blockIdx.x % ncols;
     const int seg = blockIdx.x / ncols;
-    // L2-friendly order: all vy tiles of a (y, vx) column block are adjacent,
-    // and column blocks are visited in (sj x sk) super-tiles, so a wave of
-    // resident CTAs covers a compact (y, vx) region whose halos it shares
-    const int lt = b % nlt;
-    b /= nlt;
+    // all vy tiles of a (y, vx) column block are adjacent, and column blocks
+    // are visited in (sj x sk) super-tiles
+    const int lt = blk % nlt;
+    blk /= nlt;
     const int sj = min(P.sj, njt), sk = min(P.sk, nkt);
     const int nsk = (nkt + sk - 1) / sk;
-    const int st = b / (sj * sk), wi = b % (sj * sk);
+    const int st = blk / (sj * sk), wi = blk % (sj * sk);
     const int st_j = st / nsk, st_k = st % nsk;
     const int rows_j = min(sj, njt - st_j * sj), cols_k = min(sk, nkt - st_k * sk);
     const int jt = st_j * sj + (wi / cols_k) % rows_j;
@@ -178,14 +206,12 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    // thread -> CK consecutive vx cells (a, kb .. kb+CK-1) at vy lane `lane`
-    // of its BL-wide row group (BL = 32: one warp per row, 16: two rows)
-    const int lane = tid % BL, colid = tid / BL;
-    const int a = colid / (BK / CK);
-    const int kb = (colid % (BK / CK)) * CK;
-    const int jj = j0 + a;
-    const int kfirst = k0 + kb;
-    const int ll = l0 + lane;
+    // thread -> cells (y0 + a, vx0 + b, vy), a < 2, b < 4
+    const int lane = tid & 31, warp = tid >> 5;
+    const int tl = lane & 15;
+    const int rg = (warp << 1) | (lane >> 4);
+    const int tj = rg >> 2, tk = rg & 3;
+    const int y0 = j0 + 2 * tj, vx0 = k0 + 4 * tk, vy = l0 + tl;
 
     int yl = j0 - 3, yh = j0 + BJ;
     if (P.wrap_y) {
@@ -195,7 +221,7 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
     const int cy_lo = yl + NG, cy_core = j0 + NG, cy_hi = yh + NG;
 
     if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) tma::mbar_init(&bars[s], 1);
+        for (int s = 0; s <= NS; ++s) tma::mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -204,199 +230,254 @@ __global__ void __launch_bounds__(BJ * (BK / CK) * BL, MINB)
     const int nplanes = p_last - p_first + 1;
     const Maps *M = &maps;
     if (tid == 0) {
-        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
-            for (int w = 0; w < 7; ++w)
-                issue_part<TL>(w, stages, bars, M, n, p_first, i0, i1, P, l0, k0, j0, cy_lo, cy_core, cy_hi);
+        for (int n = 0; n < NS - 1 && n < nplanes; ++n)
+            for (int w = 0; w < 4; ++w)
+                issue_plane_part(w, stages, bars, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
     }
-    const int warp = tid >> 5;
-    const bool issuer = (tid & 31) == 0 && warp < 4 + P.nops;
 
-    double ax_s[CK], bvx[CK];
-    bool xpos[CK];
+    // per-thread constants
+    double ax_s[4], bvx[4];
+    bool xpos[4];
 #pragma unroll
-    for (int i = 0; i < CK; ++i) {
-        const double v = __ldg(P.vxc + kfirst + i);
-        ax_s[i] = v * P.mhx;
-        xpos[i] = v > 0.0;
-        bvx[i] = -P.cB * v;
+    for (int b = 0; b < 4; ++b) {
+        const double v = __ldg(P.vxc + vx0 + b);
+        ax_s[b] = v * P.mhx;
+        xpos[b] = v > 0.0;
+        bvx[b] = -P.cB * v;
     }
-    const double vy = __ldg(P.vyc + ll);
-    const double ay_s = vy * P.mhy;
-    const bool ypos = vy > 0.0;
-    const double cBvy = P.cB * vy;
+    const double vyv = __ldg(P.vyc + vy);
+    const double ay_s = vyv * P.mhy;
+    const bool ypos = vyv > 0.0;
+    const double cBvy = P.cB * vyv;
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
+    const bool fold = P.fold && cL != 0.0;        // else the src operand is read at finalisation
+    const double kfold = fold ? P.cfold / cL : 0.0;
     const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
     const int nops = P.nops;
-    const double oc0 = P.opc[0], oc1 = P.opc[1], oc2 = P.opc[2];
+    const double oc0 = P.opc[0], oc1 = P.opc[1];
 
-    const int off = ((a + 3) * TL::K + (kb + 3)) * L + (lane + 3);   // first cell in the halo tile
-    const int ooff = TL::ELEMS + (a * BK + kb) * TL::OL + lane + 1;  // first cell in operand tile 0
+    const int off = ((2 * tj + 3) * TK + (4 * tk + 3)) * TW + (tl + 3);  // cell (a=0, b=0) in the halo tile
+    const int ooff = ((2 * tj) * BK + 4 * tk) * OPW + tl + 1;           // cell (0, 0) in an operand tile
+    const int toff = (2 * tj) * 8;                                      // table entry of row y0, plane p-1
 
     const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
                     P1 = (long long)(P.Ny + 2 * NG) * P2;
-    long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(jj + NG) * P2 +
-                   (long long)(kfirst + NG) * P3 + (ll + NG);  // cell q = p - 3
+    // padded index of cell (q = p - 3, y0, vx0, vy) for the first plane
+    long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(y0 + NG) * P2 +
+                   (long long)(vx0 + NG) * P3 + (vy + NG);
 
-    double acc[CK][7];
+    double acc[8][6];
 #pragma unroll
-    for (int i = 0; i < CK; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
+        for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
     int stage_s = 0;
-    unsigned stage_par = 0;
-    // Accumulator ring: cell c = p_first + m lives in slot m % 7; the plane
-    // loop is unrolled by 7 so every slot index is a compile-time constant.
-    for (int blk = 0; blk < nplanes; blk += 7) {
-#pragma unroll
-        for (int r = 0; r < 7; ++r) {
-            const int n = blk + r;
-            if (n >= nplanes) break;
-            const int p = p_first + n;
-            if (issuer && n + NSTAGE - 1 < nplanes)
-                issue_part<TL>(warp, stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, j0, cy_lo,
-                               cy_core, cy_hi);
-            // no range tests: contributions of halo planes land in accumulator
-            // slots of cells outside [i0, i1), which are never finalised
-            const int s = stage_s;
-            tma::mbar_wait(&bars[s], stage_par);
-            if (++stage_s == NSTAGE) {
-                stage_s = 0;
-                stage_par ^= 1u;
+    unsigned stage_par = 0, op_par = 0;
+    for (int n = 0; n < nplanes; ++n) {
+        const int p = p_first + n, q = p - 3;
+        const bool inner = p >= i0 && p < i1;
+        const bool fin_q = q >= i0 && q < i1;
+        // producers: plane n+NS-1 into the stage freed at the end of plane n-1,
+        // and this plane's RK operand tiles (cell plane q) into the operand buffer
+        if ((tid & 31) == 0) {
+            if (warp < 4 && n + NS - 1 < nplanes)
+                issue_plane_part(warp, stages, bars, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo,
+                                 cy_core, cy_hi);
+            if (warp >= 4 && warp < 4 + nops && fin_q) {
+                const int o = warp - 4;
+                if (o == 0) tma::mbar_expect_tx(opbar, nops * OP_BYTES);
+                tma::load4d(opbuf + o * OPE, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
             }
-            const double *stage = stages + s * TL::STAGE_ELEMS;
-            const double *c0 = stage + off;
-            const double *tb = stage + TL::ELEMS + 3 * TL::OELEMS + a * 8;  // row p-1, this j
-            const double evx = tb[BJ * 8 + 0], evy = tb[BJ * 8 + 1];
-            const double c3 = tb[BJ * 8 + 3], c4 = tb[BJ * 8 + 4];
-            const double c1m = tb[2], c5m = tb[5];
-            const double c1p = tb[2 * BJ * 8 + 2], c5p = tb[2 * BJ * 8 + 5];
-
-            const double avx = evx + cBvy;
-            const double avx_s = avx * mhvx;
-            const bool vxpos = avx > 0.0;
-            // register reuse along vx: the (j, l) column k = kb-3 .. kb+CK+2 and
-            // the j+-1 columns k = kb-1 .. kb+CK (y stencil + (y,vx) diagonal)
-            double col[CK + 6], cyp[CK + 2], cym[CK + 2];
-#pragma unroll
-            for (int m = 0; m < CK + 6; ++m) col[m] = c0[(m - 3) * L];
-#pragma unroll
-            for (int m = 0; m < CK + 2; ++m) {
-                cyp[m] = c0[KL + (m - 1) * L];
-                cym[m] = c0[-KL + (m - 1) * L];
-            }
-#pragma unroll
-            for (int i = 0; i < CK; ++i) {
-                const double *c = c0 + i * L;
-                // x-stencil contribution of s(p) to cells p - o: slot (r - o) mod 7
-                const double t = ax_s[i] * col[i + 3];
-#ifdef VPFV_EXP_SKIP_X
-                if (P.Nx < 0) {
-#else
-                if (xpos[i]) {
-#endif
-                    acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
-                    acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
-                    acc[i][(r + 8) % 7] = fma(-60.0, t, acc[i][(r + 8) % 7]);
-                    acc[i][r] = fma(20.0, t, acc[i][r]);
-                    acc[i][(r + 6) % 7] = fma(30.0, t, acc[i][(r + 6) % 7]);
-                    acc[i][(r + 5) % 7] = fma(-3.0, t, acc[i][(r + 5) % 7]);
-                } else {
-                    acc[i][(r + 9) % 7] = fma(3.0, t, acc[i][(r + 9) % 7]);
-                    acc[i][(r + 8) % 7] = fma(-30.0, t, acc[i][(r + 8) % 7]);
-                    acc[i][r] = fma(-20.0, t, acc[i][r]);
-                    acc[i][(r + 6) % 7] = fma(60.0, t, acc[i][(r + 6) % 7]);
-                    acc[i][(r + 5) % 7] = fma(-15.0, t, acc[i][(r + 5) % 7]);
-                    acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
-                }
-                // x-coupled corrections: D(p) = s[k-1]-s[k+1], G(p) = s[l-1]-s[l+1]
-#ifndef VPFV_EXP_SKIP_DG
-                const double D = col[i + 2] - col[i + 4];
-                const double G = c[-1] - c[1];
-                acc[i][(r + 6) % 7] = fma(c1m, D, fma(-c5m, G, acc[i][(r + 6) % 7]));
-                acc[i][(r + 1) % 7] = fma(-c1p, D, fma(c5p, G, acc[i][(r + 1) % 7]));
-#endif
-#ifdef VPFV_EXP_SKIP_T
-                if (P.Nx < 0)
-#endif
-                {
-                    const double avy = evy + bvx[i];
-                    double wy, wvx;
-                    if (ypos) {
-                        wy = (fma(15.0, c[-2 * KL], -2.0 * c[-3 * KL]) + fma(20.0, col[i + 3], -60.0 * cym[i + 1])) +
-                             fma(-3.0, c[2 * KL], 30.0 * cyp[i + 1]);
-                    } else {
-                        wy = (fma(-30.0, cym[i + 1], 3.0 * c[-2 * KL]) + fma(60.0, cyp[i + 1], -20.0 * col[i + 3])) +
-                             fma(2.0, c[3 * KL], -15.0 * c[2 * KL]);
-                    }
-                    if (vxpos) {
-                        wvx = (fma(15.0, col[i + 1], -2.0 * col[i]) + fma(20.0, col[i + 3], -60.0 * col[i + 2])) +
-                              fma(-3.0, col[i + 5], 30.0 * col[i + 4]);
-                    } else {
-                        wvx = (fma(-30.0, col[i + 2], 3.0 * col[i + 1]) + fma(60.0, col[i + 4], -20.0 * col[i + 3])) +
-                              fma(2.0, col[i + 6], -15.0 * col[i + 5]);
-                    }
-                    const double Ty = ay_s * wy;
-                    const double Tvx = avx_s * wvx;
-                    const double Tvy = (avy * mhvy) * wsum<1>(c, avy > 0.0);
-                    const double dyvx = (cyp[i] + cym[i + 2]) - (cyp[i + 2] + cym[i]);
-                    const double Tc = fma(c4, dsum<KL, 1>(c), fma(mc2, dsum<L, 1>(c), -c3 * dyvx));
-                    acc[i][r] += (Ty + Tvx) + (Tvy + Tc);
-                }
-            }
-            // finalise cells q = p - 3 (slot (r + 4) % 7) from the staged RK operands
-            const int q = p - 3;
-            if (q >= i0 && q < i1) {
-                const double *op = stage + ooff;
-                double out[CK];
-#pragma unroll
-                for (int i = 0; i < CK; ++i) {
-                    double rk = oc0 * op[i * TL::OL];
-                    if (nops > 1) rk = fma(oc1, op[TL::OELEMS + i * TL::OL], rk);
-                    if (nops > 2) rk = fma(oc2, op[2 * TL::OELEMS + i * TL::OL], rk);
-                    out[i] = fma(cL, acc[i][(r + 4) % 7], rk);
-                    P.dest[gq + i * P3] = out[i];
-                }
-                if (P.nonfinite) {
-#pragma unroll
-                    for (int i = 0; i < CK; ++i)
-                        if (!isfinite(out[i]))
-                            atomicMin(P.nonfinite,
-                                      (((unsigned long long)q * P.Ny + jj) * P.Nvx + kfirst + i) * P.Nvy + ll);
-                }
-#ifdef VPFV_EXP_SKIP_PARTIALS
-                if (P.partials && P.Nx < 0) {
-#else
-                if (P.partials) {
-#endif
-                    // fold-tree subtrees of two rows at once: lanes pair up
-                    // (even lane keeps row i, odd lane row i+1), then the usual
-                    // ascending shuffle levels on one register
-                    const long long pb = ((long long)q * P.Ny + jj) * P.Nvx + kfirst;
-                    const bool odd = lane & 1;
-#pragma unroll
-                    for (int i = 0; i < CK; i += 2) {
-                        const double keep = odd ? out[i + 1] : out[i];
-                        const double send = odd ? out[i] : out[i + 1];
-                        double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1, BL));
-#pragma unroll
-                        for (int off = 2; off < BL; off <<= 1)
-                            v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off, BL));
-                        if (lane < 2) P.partials[(pb + i + lane) * nlt + lt] = v;
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
-            gq += P1;
-            __syncthreads();  // stage s is free for the next refill
         }
+        tma::mbar_wait(&bars[stage_s], stage_par);
+        const double *stage = stages + stage_s * STAGE;
+        if (++stage_s == NS) {
+            stage_s = 0;
+            stage_par ^= 1u;
+        }
+        const double *c = stage + off;
+        const double *tb = stage + HALO + toff;
+        double evx[2], evy[2], c3[2], c4[2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const double *e1 = tb + (BJ + a) * 8;
+            evx[a] = e1[T_EVX];
+            evy[a] = e1[T_EVY];
+            c3[a] = e1[T_C3];
+            c4[a] = e1[T_C4];
+        }
+
+        // ---- own rows (a = 0, 1): vy lines, vx lines, D and G -------------
+        double s0[8], Dk[8], Gc[8], T[8];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            asm volatile("" ::: "memory");  // one row at a time (register pressure)
+            const double *ca = c + a * KL;
+            double v[4][7];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int d = 0; d < 7; ++d) v[b][d] = ca[b * TW + d - 3];
+            double r0[10];  // vy-offset-0 values at vx offsets -3 .. 6
+            r0[0] = ca[-3 * TW];
+            r0[1] = ca[-2 * TW];
+            r0[2] = ca[-TW];
+            r0[7] = ca[4 * TW];
+            r0[8] = ca[5 * TW];
+            r0[9] = ca[6 * TW];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                r0[b + 3] = v[b][3];
+                s0[a * 4 + b] = v[b][3];
+                Gc[a * 4 + b] = v[b][2] - v[b][4];
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) Dk[a * 4 + b] = r0[b + 2] - r0[b + 4];
+            if (inner) {
+                const double gm = ca[-TW - 1] - ca[-TW + 1];         // G at vx offset -1
+                const double gp = ca[4 * TW - 1] - ca[4 * TW + 1];   // G at vx offset 4
+                const double avx = evx[a] + cBvy;
+                const double avx_s = avx * mhvx;
+                if (avx > 0.0) {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        T[a * 4 + b] = avx_s * wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        T[a * 4 + b] = avx_s * wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]);
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const double avy = evy[a] + bvx[b];
+                    const double avy_s = avy * mhvy;
+                    double w;
+                    if (avy > 0.0)
+                        w = wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]);
+                    else
+                        w = wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
+                    T[a * 4 + b] = fma(avy_s, w, T[a * 4 + b]);
+                }
+                // diag(vx,vy) = G(vx+1) - G(vx-1)
+                double gr[6] = {gm, Gc[a * 4], Gc[a * 4 + 1], Gc[a * 4 + 2], Gc[a * 4 + 3], gp};
+#pragma unroll
+                for (int b = 0; b < 4; ++b) T[a * 4 + b] = fma(mc2, gr[b + 2] - gr[b], T[a * 4 + b]);
+            }
+        }
+
+        // ---- y arms: y stencil, diag(y,vy), diag(y,vx), folded src operand --
+        if (inner) {
+            const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                asm volatile("" ::: "memory");  // keep the per-b loads from being hoisted (register pressure)
+                const double qm = rm[b * TW], qp = rp[b * TW];
+                const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
+                const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
+                const double Dkm = rm[(b - 1) * TW] - rm[(b + 1) * TW];
+                const double Dkp = rp[(b - 1) * TW] - rp[(b + 1) * TW];
+                const double z0 = s0[b], z1 = s0[4 + b];
+                double w0, w1;
+                if (ypos) {
+                    const double ym3 = c[-3 * KL + b * TW], ym2 = c[-2 * KL + b * TW], y3 = c[3 * KL + b * TW];
+                    w0 = wpos(ym3, ym2, qm, z0, z1, qp);
+                    w1 = wpos(ym2, qm, z0, z1, qp, y3);
+                } else {
+                    const double ym2 = c[-2 * KL + b * TW], y3 = c[3 * KL + b * TW], y4 = c[4 * KL + b * TW];
+                    w0 = wneg(ym2, qm, z0, z1, qp, y3);
+                    w1 = wneg(qm, z0, z1, qp, y3, y4);
+                }
+                double t0 = fma(ay_s, w0, T[b]), t1 = fma(ay_s, w1, T[4 + b]);
+                t0 = fma(c4[0], Gc[4 + b] - Gm, t0);      // diag(y,vy) = G(y+1) - G(y-1)
+                t1 = fma(c4[1], Gp - Gc[b], t1);
+                t0 = fma(-c3[0], Dk[4 + b] - Dkm, t0);    // diag(y,vx) = D(y+1) - D(y-1)
+                t1 = fma(-c3[1], Dkp - Dk[b], t1);
+                T[b] = fma(kfold, z0, t0);
+                T[4 + b] = fma(kfold, z1, t1);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) T[i] = 0.0;
+        }
+
+        // ---- scatter into the accumulator ring, extract cell q --------------
+        // x-coupled corrections: cell p-1 gets c1(p-1) D(p) - c5(p-1) G(p), cell p+1 the negative with c(p+1)
+        double Xm[8], Xp[8], fin[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int a = i >> 2;
+            const double *e0 = tb + a * 8, *e2 = e0 + 2 * BJ * 8;
+            Xm[i] = fma(e0[T_C1], Dk[i], -e0[T_C5] * Gc[i]);
+            Xp[i] = fma(e2[T_C5], Gc[i], -e2[T_C1] * Dk[i]);
+        }
+        window_apply(acc, s0, ax_s, xpos, Xm, Xp, T, fin);
+
+
+        // ---- finalise cells q: RK combination, store, non-finite, moment ----
+        if (fin_q) {
+            if (nops) {
+                tma::mbar_wait(opbar, op_par);
+                op_par ^= 1u;
+            }
+            const double *op = opbuf + ooff;
+            double out[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int a = i >> 2, b = i & 3;
+                const int oi = a * BK * OPW + b * OPW;
+                double rk = 0.0;
+                if (nops > 0) rk = oc0 * op[oi];
+                if (nops > 1) rk = fma(oc1, op[OPE + oi], rk);
+                const long long g = gq + a * P2 + b * P3;
+                if (P.fold && !fold) rk = fma(P.cfold, P.src[g], rk);
+                out[i] = fma(cL, fin[i], rk);
+                __stcs(P.dest + g, out[i]);
+            }
+            if (P.nonfinite) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (!isfinite(out[i]))
+                        atomicMin(P.nonfinite,
+                                  (((unsigned long long)q * P.Ny + y0 + (i >> 2)) * P.Nvx + vx0 + (i & 3)) * P.Nvy +
+                                      vy);
+            }
+            if (P.partials) {
+                // reference fold tree over each aligned 16-wide vy chunk
+                // (fields.py:28-47): transpose-reduce the 8 rows over the 16
+                // vy lanes; after level k lane bit k-1 selects the row half
+                const bool o1 = tl & 1, o2 = tl & 2, o4 = tl & 4;
+                double w4[4], w2[2];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const double keep = o1 ? out[2 * m + 1] : out[2 * m];
+                    const double send = o1 ? out[2 * m] : out[2 * m + 1];
+                    w4[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                }
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const double keep = o2 ? w4[2 * m + 1] : w4[2 * m];
+                    const double send = o2 ? w4[2 * m] : w4[2 * m + 1];
+                    w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                }
+                const double keep = o4 ? w2[1] : w2[0];
+                const double send = o4 ? w2[0] : w2[1];
+                double w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
+                if (tl < 8) {  // lane tl holds row tl = 4a + b
+                    const long long pr = (((long long)q * P.Ny + y0 + (tl >> 2)) * P.Nvx + vx0 + (tl & 3));
+                    P.partials[pr * nlt + lt] = w1;
+                }
+            }
+        }
+        gq += P1;
+        __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
 }
 
 // ---------------------------------------------------------------------------
 // moment from partials: per physical cell, fold over the vy chunks of every
-// vx row (chunk sums are exact 32-wide subtrees), then over vx, times vol.
+// vx row (chunk sums are exact subtrees), then over vx, times vol.
 
 __device__ double fold_small(double *x, int n) {  // single thread, in place
     while (n > 1) {
@@ -445,84 +526,38 @@ __global__ void moment_partials_kernel(const double *__restrict__ part, double *
 // ---------------------------------------------------------------------------
 // host side: tensor maps and launch
 
-// Tile configurations: (BJ, BL, NSTAGE, CK) with BK = 8.  Chosen at run time
-// (VPFV_TCFG overrides; default 0).
-constexpr int TBK = 8;
-struct TCfg {
-    int bj, bl, ns, ck;
-};
-static const TCfg kCfgs[] = {{4, 32, 3, 2}, {8, 16, 3, 2}, {4, 32, 2, 2}, {4, 16, 2, 2}, {2, 32, 2, 2}};
-
-static int tile_cfg() {
-    static int c = -1;
-    if (c < 0) {
-        const char *e = getenv("VPFV_TCFG");
-        c = e ? atoi(e) : 0;
-        if (c < 0 || c > 4) c = 0;
-    }
-    return c;
-}
-
-int tma_2d2v_chunk() { return kCfgs[tile_cfg()].bl; }
-
 bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
-    const TCfg &c = kCfgs[tile_cfg()];
     if (flags & VPFV_EXACT) return false;
     if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
-    if (Ny % c.bj || Nvx % TBK || Nvy % c.bl || (Nvy & 1)) return false;
-    if (Nx < 1 || Ny < 3 + c.bj) return false;
+    if (Ny % rb::BJ || Nvx % rb::BK || Nvy % rb::BL) return false;
+    if (Nx < 1 || Ny < rb::BJ) return false;
     return tma_available();
 }
 
-int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
-    const TCfg &c = kCfgs[tile_cfg()];
-    return (Ny / c.bj) * (Nvx / TBK) * (Nvy / c.bl);
-}
+int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / rb::BJ) * (Nvx / rb::BK) * (Nvy / rb::BL); }
 
-template <int BJ, int BL, int NS, int CK, int MINB = 1>
-static int launch_cfg(const Maps &maps, const Stage22 &P, cudaStream_t s) {
-    using TL = Tile<BJ, TBK, BL, NS>;
-    auto kern = stage2d2v_tma_kernel<BJ, TBK, BL, NS, CK, MINB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM);
-        attr = true;
-    }
-    const int nblocks = (P.Ny / BJ) * (P.Nvx / TBK) * (P.Nvy / BL) * P.nseg;
-    kern<<<nblocks, BJ * (TBK / CK) * BL, TL::SMEM, s>>>(maps, P);
-    return check_launch("stage_2d2v_tma");
-}
-
-// ops: up to three (coefficient, array) RK operands, already de-duplicated
-int launch_tma_2d2v(const double *src, const double *const ops[3], const double *tab, Stage22 P,
-                    unsigned flags, int nseg, cudaStream_t s) {
-    const TCfg &c = kCfgs[tile_cfg()];
-    const int Npad[4] = {P.Nx + 6, P.Ny + 6, P.Nvx + 6, P.Nvy + 6};
-    const int box_core[4] = {c.bl + 8, TBK + 6, c.bj, 1};
-    const int box_halo[4] = {c.bl + 8, TBK + 6, 3, 1};
-    const int box_op[4] = {c.bl + 2, TBK, c.bj, 1};
-    Maps maps;
-    // 4D fp64 padded arrays, innermost (vy) first
-    const unsigned long long dims[4] = {(unsigned long long)Npad[3], (unsigned long long)Npad[2],
-                                        (unsigned long long)Npad[1], (unsigned long long)Npad[0]};
+static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
+                     unsigned flags, int nseg, cudaStream_t s) {
+    using namespace rb;
+    const unsigned long long dims[4] = {(unsigned long long)P.Nvy + 6, (unsigned long long)P.Nvx + 6,
+                                        (unsigned long long)P.Ny + 6, (unsigned long long)P.Nx + 6};
     const unsigned long long strides[3] = {dims[0] * 8, dims[0] * dims[1] * 8, dims[0] * dims[1] * dims[2] * 8};
-    auto box4 = [](const int *b) {
-        struct B {
-            unsigned v[4];
-        } r{{(unsigned)b[0], (unsigned)b[1], (unsigned)b[2], (unsigned)b[3]}};
-        return r;
-    };
-    const auto bc = box4(box_core), bh = box4(box_halo), bo = box4(box_op);
-    if (!tma_map(src, 4, dims, strides, bc.v, &maps.core) || !tma_map(src, 4, dims, strides, bh.v, &maps.halo))
+    const unsigned box_core[4] = {TW, TK, BJ, 1}, box_halo[4] = {TW, TK, 3, 1}, box_op[4] = {OPW, BK, BJ, 1};
+    Maps maps;
+    if (!tma_map(src, 4, dims, strides, box_core, &maps.core) || !tma_map(src, 4, dims, strides, box_halo, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
-    for (int o = 0; o < P.nops; ++o)
-        if (!tma_map(ops[o], 4, dims, strides, bo.v, &maps.op[o]))
-            return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
-    for (int o = P.nops; o < 3; ++o) maps.op[o] = maps.core;
+    for (int o = 0; o < OPS_MAX; ++o) {
+        if (o < P.nops) {
+            if (!tma_map(ops[o], 4, dims, strides, box_op, &maps.op[o]))
+                return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
+        } else {
+            maps.op[o] = maps.core;
+        }
+    }
     // packed tables [(Nx+2)][Ny][8]
     const unsigned long long tdims[3] = {8, (unsigned long long)P.Ny, (unsigned long long)P.Nx + 2};
     const unsigned long long tstr[2] = {64, (unsigned long long)P.Ny * 64};
-    const unsigned tbox[3] = {8, (unsigned)c.bj, 3};
+    const unsigned tbox[3] = {8, (unsigned)BJ, 3};
     if (!tma_map(tab, 3, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
     P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
     P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
@@ -533,19 +568,20 @@ int launch_tma_2d2v(const double *src, const double *const ops[3], const double 
     static int sjk[2] = {-1, -1};
     if (sjk[0] < 0) {
         const char *e = getenv("VPFV_SUPER");
-        sjk[0] = 8;
-        sjk[1] = 4;
+        sjk[0] = 4;
+        sjk[1] = 8;
         if (e) sscanf(e, "%d,%d", &sjk[0], &sjk[1]);
     }
     P.sj = sjk[0] > 0 ? sjk[0] : 1;
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
-    switch (tile_cfg()) {
-        case 1: return launch_cfg<8, 16, 3, 2>(maps, P, s);
-        case 2: return launch_cfg<4, 32, 2, 2>(maps, P, s);
-        case 3: return launch_cfg<4, 16, 2, 2, 2>(maps, P, s);
-        case 4: return launch_cfg<2, 32, 2, 2, 2>(maps, P, s);
-        default: return launch_cfg<4, 32, 3, 2>(maps, P, s);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(stage2d2v_rb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        attr = true;
     }
+    const int nblocks = tma_2d2v_columns(P.Ny, P.Nvx, P.Nvy) * P.nseg;
+    stage2d2v_rb_kernel<<<nblocks, THREADS, SMEM, s>>>(maps, P);
+    return check_launch("stage_2d2v_tma");
 }
 
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
@@ -573,6 +609,33 @@ extern "C" int vpfv_stage_2d2v_generic(double *, const double *, const double *,
                                        double, double, int, int, int, int, unsigned, const double *,
                                        double, unsigned long long *, void *);
 
+namespace {
+// RK operands ca A + cb B + cd dest grouped by array: the src-aliased part
+// is folded into the accumulator, the others are staged by TMA.
+struct Operands {
+    const double *ptr[3];
+    double coef[3];
+    int n = 0;
+    double cfold = 0.0;
+    int fold = 0;
+    void add(const double *p, double c, const double *src) {
+        if (c == 0.0) return;
+        if (p == src) {
+            cfold += c;
+            fold = 1;
+            return;
+        }
+        for (int i = 0; i < n; ++i)
+            if (ptr[i] == p) {
+                coef[i] += c;
+                return;
+            }
+        ptr[n] = p;
+        coef[n++] = c;
+    }
+};
+}  // namespace
+
 extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B,
                                      const double *src, double ca, double cb, double cd, double cL,
                                      const double *vxc, const double *vyc, const double *evx,
@@ -583,7 +646,11 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
                                      unsigned long long *nonfinite, const double *packed_tables,
                                      double *moment_partials, int xsegments, void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
-    if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags)) {
+    Operands ops;
+    ops.add(A, ca, src);
+    ops.add(B, cb, src);
+    ops.add(dest, cd, src);
+    if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) || ops.n > rb::OPS_MAX) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 2D-2V path");
         return vpfv_stage_2d2v_generic(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2,
                                        c3, c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev,
@@ -591,38 +658,17 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
     }
     Stage22 P{};
     P.dest = dest;
+    P.src = src;
     P.cL = cL;
     P.dt_dev = dt_dev;
     P.cL_div = cL_div;
-    // RK operands: ca*A + cb*B + cd*dest, merging B into A when they alias
-    const double *ops[3] = {nullptr, nullptr, nullptr};
-    int nops = 0;
-    if (ca != 0.0 || (cb != 0.0 && B == A)) {
-        ops[nops] = A;
-        P.opc[nops++] = (B == A) ? ca + cb : ca;
-    }
-    if (cb != 0.0 && B != A) {
-        ops[nops] = B;
-        P.opc[nops++] = cb;
-    }
-    if (cd != 0.0) {
-        ops[nops] = dest;
-        P.opc[nops++] = cd;
-    }
-    if (nops == 0) {  // pure RHS: one zero-weighted operand keeps the code path uniform
-        ops[nops] = src;
-        P.opc[nops++] = 0.0;
-    }
-    P.nops = nops;
+    P.nops = ops.n;
+    for (int o = 0; o < ops.n; ++o) P.opc[o] = ops.coef[o];
+    P.fold = ops.fold;
+    P.cfold = ops.cfold;
     P.nonfinite = nonfinite;
     P.vxc = vxc;
     P.vyc = vyc;
-    P.evx = evx;
-    P.evy = evy;
-    P.c1 = c1;
-    P.c3 = c3;
-    P.c4 = c4;
-    P.c5 = c5;
     P.cB = cB;
     P.c2 = c2;
     P.mhx = -1.0 / (60.0 * hx);
@@ -641,13 +687,14 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
         env_seg = e ? atoi(e) : 0;
     }
     if (nseg <= 0 && env_seg > 0) nseg = env_seg;
-    if (nseg <= 0) {  // at least ~4 waves of one CTA per SM, segments >= 8 planes
+    if (nseg <= 0) {  // at least ~3 waves of one CTA per SM, segments >= 8 planes
         const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
-        nseg = (4 * 148 + cols - 1) / cols;
+        nseg = (3 * 148 + cols - 1) / cols;
         if (nseg > Nx / 8) nseg = Nx / 8;
         if (nseg < 1) nseg = 1;
     }
-    return launch_tma_2d2v(src, ops, packed_tables, P, flags, nseg, (cudaStream_t)stream);
+    const double *opp[rb::OPS_MAX] = {ops.n > 0 ? ops.ptr[0] : nullptr, ops.n > 1 ? ops.ptr[1] : nullptr};
+    return launch_rb(src, opp, packed_tables, P, flags, nseg, (cudaStream_t)stream);
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,
@@ -656,7 +703,7 @@ extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys
 }
 
 extern "C" int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
-    return tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) && Nvy / tma_2d2v_chunk() <= 16 ? 1 : 0;
+    return tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) && Nvy / rb::BL <= 16 ? 1 : 0;
 }
 
-extern "C" int vpfv_stage_2d2v_partials_chunk(void) { return tma_2d2v_chunk(); }
+extern "C" int vpfv_stage_2d2v_partials_chunk(void) { return rb::BL; }
