@@ -81,7 +81,8 @@ constexpr int OPW = BL + 2;      // RK operand row (16 B aligned start)
 constexpr int OPE = BJ * BK * OPW;
 constexpr int OPS_MAX = 2;
 constexpr int HALO_BYTES = HALO * 8, CORE_BYTES = BJ * KL * 8, TAB_BYTES = TAB * 8, OP_BYTES = OPE * 8;
-constexpr int SMEM = NS * STAGE * 8 + OPS_MAX * OPE * 8 + 64;
+constexpr int BAR_OFF = NS * STAGE * 8 + OPS_MAX * OPE * 8;  // NS stage barriers, then the operand barrier
+constexpr int SMEM = BAR_OFF + 64;
 static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
               "TMA destinations must stay 128 B aligned");
 static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -102,42 +103,60 @@ __device__ __forceinline__ double wneg(double m2, double m1, double z, double p1
     return fma(2.0, p3, fma(-15.0, p2, fma(60.0, p1, fma(-20.0, z, fma(-30.0, m1, 3.0 * m2)))));
 }
 
-// Scatter of plane p into the accumulator window and extraction of the
-// finished cell p-3.  Before plane p, acc[i][j] holds cell p-3+j (j < 6);
-// afterwards the window slides by one (cell p+3 enters).  A cell's slot is
-// initialised by its first contribution -- x-stencil offset -3 (a_x > 0) or
-// -2 (a_x <= 0) -- so no slot is zeroed.
-__device__ __forceinline__ void window_apply(double (&acc)[8][6], const double (&s0)[8], const double (&ax_s)[4],
-                                             const bool (&xpos)[4], const double (&Xm)[8], const double (&Xp)[8],
-                                             const double (&T)[8], double (&fin)[8]) {
+#ifdef VPFV_NO_SCHED_FENCE
+#define SCHED_FENCE()
+#else
+#define SCHED_FENCE() asm volatile("" ::: "memory")  // limit load hoisting (register pressure)
+#endif
+
+// x stencil scatter of s(p) into one cell's accumulator window, extraction
+// of the finished cell p-3 and the window slide.  Before plane p, w[j] holds
+// cell p-3+j; a cell's slot is initialised by its first contribution --
+// x-stencil offset -3 (a_x > 0) or -2 (a_x <= 0) -- so no slot is zeroed.
+template <int SIGN>  // +1: a_x > 0, -1: a_x <= 0
+__device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &fin) {
+    if (SIGN > 0) {
+        w[5] = fma(15.0, ti, w[5]);
+        w[4] = fma(-60.0, ti, w[4]);
+        w[3] = fma(20.0, ti, w[3]);
+        w[2] = fma(30.0, ti, w[2]);
+        w[1] = fma(-3.0, ti, w[1]);
+        fin = w[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double ti = ax_s[i & 3] * s0[i];
-        double nw;
-        if (xpos[i & 3]) {
-            acc[i][5] = fma(15.0, ti, acc[i][5]);
-            acc[i][4] = fma(-60.0, ti, acc[i][4]);
-            acc[i][3] = fma(20.0, ti, acc[i][3]);
-            acc[i][2] = fma(30.0, ti, acc[i][2]);
-            acc[i][1] = fma(-3.0, ti, acc[i][1]);
-            fin[i] = acc[i][0];
-            nw = -2.0 * ti;          // cell p+3
-        } else {
-            acc[i][5] = 3.0 * ti;    // cell p+2 enters
-            acc[i][4] = fma(-30.0, ti, acc[i][4]);
-            acc[i][3] = fma(-20.0, ti, acc[i][3]);
-            acc[i][2] = fma(60.0, ti, acc[i][2]);
-            acc[i][1] = fma(-15.0, ti, acc[i][1]);
-            fin[i] = fma(2.0, ti, acc[i][0]);
-            nw = 0.0;
+        for (int j = 0; j < 5; ++j) w[j] = w[j + 1];
+        w[5] = -2.0 * ti;  // cell p+3 enters
+    } else {
+        const double c2 = 3.0 * ti;  // cell p+2 enters (its slot was freed last plane)
+        w[4] = fma(-30.0, ti, w[4]);
+        w[3] = fma(-20.0, ti, w[3]);
+        w[2] = fma(60.0, ti, w[2]);
+        w[1] = fma(-15.0, ti, w[1]);
+        fin = fma(2.0, ti, w[0]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = w[j + 1];
+        w[4] = c2;
+        w[5] = 0.0;
+    }
+}
+
+// The sign of a_x is per vx; a thread's 4 vx cells share it unless the zero
+// crossing falls inside the quad (one uniform branch, no predication).
+__device__ __forceinline__ void window_apply(double (&acc)[8][6], const double (&s0)[8], const double (&ax_s)[4],
+                                             const bool (&xpos)[4], double (&fin)[8]) {
+    if (xpos[0] && xpos[3]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) scatter_cell<1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+    } else if (!xpos[0] && !xpos[3]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) scatter_cell<-1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (xpos[i & 3])
+                scatter_cell<1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+            else
+                scatter_cell<-1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
         }
-        // x-coupled corrections of cells p-1 and p+1, in-plane terms of cell p
-        acc[i][0] = acc[i][1];
-        acc[i][1] = acc[i][2] + Xm[i];
-        acc[i][2] = acc[i][3] + T[i];
-        acc[i][3] = acc[i][4] + Xp[i];
-        acc[i][4] = acc[i][5];
-        acc[i][5] = nw;
     }
 }
 
@@ -146,12 +165,12 @@ __device__ __forceinline__ void window_apply(double (&acc)[8][6], const double (
 // y-low halo / core / y-high halo.  complete_tx may land before expect_tx
 // (the transaction count may go transiently negative; the phase cannot
 // complete before part 0 arrives).  On x-halo planes only the core moves.
-__device__ __forceinline__ void issue_plane_part(int w, double *stages, uint64_t *bars, const Maps *M, int n,
-                                                 int p_first, const Stage22 &P, int i0, int i1, int l0, int k0,
-                                                 int j0, int cy_lo, int cy_core, int cy_hi) {
+__device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Maps *M, int n, int p_first,
+                                                 const Stage22 &P, int i0, int i1, int l0, int k0, int j0, int cy_lo,
+                                                 int cy_core, int cy_hi) {
     using namespace rb;
     const int s = n % NS;
-    double *dst = stages + s * STAGE;
+    const unsigned dst = sbase + s * STAGE * 8, bar = sbase + BAR_OFF + s * 8;
     const int p = p_first + n;  // in [i0-3, i1+3)
     int px = p;
     if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
@@ -159,16 +178,16 @@ __device__ __forceinline__ void issue_plane_part(int w, double *stages, uint64_t
     const int cx = px + NG;
     switch (w) {
         case 0:
-            tma::mbar_expect_tx(&bars[s], (inner ? HALO_BYTES : CORE_BYTES) + TAB_BYTES);
+            tma::mbar_expect_tx_s(bar, (inner ? HALO_BYTES : CORE_BYTES) + TAB_BYTES);
             // packed table rows px..px+2 = planes p-1, p, p+1 (row = x + 1)
-            tma::load3d(dst + HALO, &M->tab, &bars[s], 0, j0, px);
+            tma::load3d_s(dst + HALO * 8, &M->tab, bar, 0, j0, px);
             break;
         case 1:
-            if (inner) tma::load4d(dst, &M->halo, &bars[s], l0, k0, cy_lo, cx);
+            if (inner) tma::load4d_s(dst, &M->halo, bar, l0, k0, cy_lo, cx);
             break;
-        case 2: tma::load4d(dst + 3 * KL, &M->core, &bars[s], l0, k0, cy_core, cx); break;
+        case 2: tma::load4d_s(dst + 3 * KL * 8, &M->core, bar, l0, k0, cy_core, cx); break;
         case 3:
-            if (inner) tma::load4d(dst + (3 + BJ) * KL, &M->halo, &bars[s], l0, k0, cy_hi, cx);
+            if (inner) tma::load4d_s(dst + (3 + BJ) * KL * 8, &M->halo, bar, l0, k0, cy_hi, cx);
             break;
         default: break;
     }
@@ -179,9 +198,10 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     using namespace rb;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
-    double *opbuf = stages + NS * STAGE;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(opbuf + OPS_MAX * OPE);  // NS stage barriers + 1 operand barrier
-    uint64_t *opbar = bars + NS;
+    const double *opbuf = stages + NS * STAGE;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + BAR_OFF);  // NS stage barriers + 1 operand barrier
+    const unsigned sbase = tma::smem_addr(smem_raw);
+    const unsigned opbar = sbase + BAR_OFF + NS * 8, opdst = sbase + NS * STAGE * 8;
 
     const int tid = threadIdx.x;
     // column block; x segment outermost so the CTAs resident at once cover
@@ -232,7 +252,7 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     if (tid == 0) {
         for (int n = 0; n < NS - 1 && n < nplanes; ++n)
             for (int w = 0; w < 4; ++w)
-                issue_plane_part(w, stages, bars, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
+                issue_plane_part(w, sbase, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
     }
 
     // per-thread constants
@@ -249,9 +269,12 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     const double ay_s = vyv * P.mhy;
     const bool ypos = vyv > 0.0;
     const double cBvy = P.cB * vyv;
+    const double bvx_min = fmin(fmin(bvx[0], bvx[1]), fmin(bvx[2], bvx[3]));
+    const double bvx_max = fmax(fmax(bvx[0], bvx[1]), fmax(bvx[2], bvx[3]));
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
     const bool fold = P.fold && cL != 0.0;        // else the src operand is read at finalisation
     const double kfold = fold ? P.cfold / cL : 0.0;
+    const bool fold_fb = P.fold && !fold;
     const double mc2 = -P.c2, mhvx = P.mhvx, mhvy = P.mhvy;
     const int nops = P.nops;
     const double oc0 = P.opc[0], oc1 = P.opc[1];
@@ -272,8 +295,6 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
 #pragma unroll
         for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
-    int stage_s = 0;
-    unsigned stage_par = 0, op_par = 0;
     for (int n = 0; n < nplanes; ++n) {
         const int p = p_first + n, q = p - 3;
         const bool inner = p >= i0 && p < i1;
@@ -282,20 +303,17 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
         // and this plane's RK operand tiles (cell plane q) into the operand buffer
         if ((tid & 31) == 0) {
             if (warp < 4 && n + NS - 1 < nplanes)
-                issue_plane_part(warp, stages, bars, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo,
-                                 cy_core, cy_hi);
+                issue_plane_part(warp, sbase, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
             if (warp >= 4 && warp < 4 + nops && fin_q) {
                 const int o = warp - 4;
-                if (o == 0) tma::mbar_expect_tx(opbar, nops * OP_BYTES);
-                tma::load4d(opbuf + o * OPE, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
+                if (o == 0) tma::mbar_expect_tx_s(opbar, nops * OP_BYTES);
+                tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
             }
         }
-        tma::mbar_wait(&bars[stage_s], stage_par);
+        // stage and parity from the plane number (loop-carried counters get spilled)
+        const int nq3 = n / NS, stage_s = n - nq3 * NS;
+        tma::mbar_wait_s(sbase + BAR_OFF + stage_s * 8, nq3 & 1);
         const double *stage = stages + stage_s * STAGE;
-        if (++stage_s == NS) {
-            stage_s = 0;
-            stage_par ^= 1u;
-        }
         const double *c = stage + off;
         const double *tb = stage + HALO + toff;
         double evx[2], evy[2], c3[2], c4[2];
@@ -308,11 +326,18 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
             c4[a] = e1[T_C4];
         }
 
+        // acc[i][2], acc[i][3], acc[i][4] hold cells p-1, p, p+1: every
+        // contribution goes straight into its slot.  The y-corner terms are
+        // linear in the per-row differences G = s[vy-1]-s[vy+1] and
+        // D = s[vx-1]-s[vx+1]:  c4 diag(y,vy) = c4 (G(y+1) - G(y-1)),
+        // -c3 diag(y,vx) = -c3 (D(y+1) - D(y-1)); each row's G and D are
+        // consumed as soon as they exist (rows -1 and 2 are the y arms).
+        double s0[8];
+
         // ---- own rows (a = 0, 1): vy lines, vx lines, D and G -------------
-        double s0[8], Dk[8], Gc[8], T[8];
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
-            asm volatile("" ::: "memory");  // one row at a time (register pressure)
+            SCHED_FENCE();  // one row at a time
             const double *ca = c + a * KL;
             double v[4][7];
 #pragma unroll
@@ -326,52 +351,82 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
             r0[7] = ca[4 * TW];
             r0[8] = ca[5 * TW];
             r0[9] = ca[6 * TW];
+            double G[4], D[4];
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 r0[b + 3] = v[b][3];
                 s0[a * 4 + b] = v[b][3];
-                Gc[a * 4 + b] = v[b][2] - v[b][4];
+                G[b] = v[b][2] - v[b][4];
             }
 #pragma unroll
-            for (int b = 0; b < 4; ++b) Dk[a * 4 + b] = r0[b + 2] - r0[b + 4];
+            for (int b = 0; b < 4; ++b) D[b] = r0[b + 2] - r0[b + 4];
+            // x-coupled corrections: cell p-1 gets c1(p-1) D(p) - c5(p-1) G(p),
+            // cell p+1 gets -c1(p+1) D(p) + c5(p+1) G(p)
+            const double *e0 = tb + a * 8, *e2 = e0 + 2 * BJ * 8;
+            const double c1m = e0[T_C1], c5m = e0[T_C5], c1p = e2[T_C1], c5p = e2[T_C5];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int i = a * 4 + b;
+                acc[i][2] = fma(c1m, D[b], fma(-c5m, G[b], acc[i][2]));
+                acc[i][4] = fma(-c1p, D[b], fma(c5p, G[b], acc[i][4]));
+            }
             if (inner) {
+                // y corners of the other own row: G(0) and D(0) feed cell row 1
+                // with the minus sign, G(1) and D(1) feed row 0 with the plus sign
+                const int o = (1 - a) * 4;
+                const double sg = a ? 1.0 : -1.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    acc[o + b][3] = fma(sg * c4[1 - a], G[b], fma(-sg * c3[1 - a], D[b], acc[o + b][3]));
                 const double gm = ca[-TW - 1] - ca[-TW + 1];         // G at vx offset -1
                 const double gp = ca[4 * TW - 1] - ca[4 * TW + 1];   // G at vx offset 4
-                const double avx = evx[a] + cBvy;
+                const double avx = evx[a] + cBvy;                    // a_vx is independent of vx
                 const double avx_s = avx * mhvx;
                 if (avx > 0.0) {
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
-                        T[a * 4 + b] = avx_s * wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]);
+                        acc[a * 4 + b][3] = fma(avx_s, wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]),
+                                                acc[a * 4 + b][3]);
                 } else {
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
-                        T[a * 4 + b] = avx_s * wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]);
+                        acc[a * 4 + b][3] = fma(avx_s, wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]),
+                                                acc[a * 4 + b][3]);
                 }
+                // a_vy = evy - cB vx: one branch for the row when the four
+                // signs agree (always when cB == 0; fl(e + x) is monotone in x)
+                if (evy[a] + bvx_min > 0.0) {
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const double avy = evy[a] + bvx[b];
-                    const double avy_s = avy * mhvy;
-                    double w;
-                    if (avy > 0.0)
-                        w = wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]);
-                    else
-                        w = wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
-                    T[a * 4 + b] = fma(avy_s, w, T[a * 4 + b]);
+                    for (int b = 0; b < 4; ++b)
+                        acc[a * 4 + b][3] = fma((evy[a] + bvx[b]) * mhvy,
+                                                wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]), acc[a * 4 + b][3]);
+                } else if (evy[a] + bvx_max <= 0.0) {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        acc[a * 4 + b][3] = fma((evy[a] + bvx[b]) * mhvy,
+                                                wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]), acc[a * 4 + b][3]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const double avy = evy[a] + bvx[b];
+                        const double w = avy > 0.0 ? wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
+                                                   : wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
+                        acc[a * 4 + b][3] = fma(avy * mhvy, w, acc[a * 4 + b][3]);
+                    }
                 }
                 // diag(vx,vy) = G(vx+1) - G(vx-1)
-                double gr[6] = {gm, Gc[a * 4], Gc[a * 4 + 1], Gc[a * 4 + 2], Gc[a * 4 + 3], gp};
+                const double gr[6] = {gm, G[0], G[1], G[2], G[3], gp};
 #pragma unroll
-                for (int b = 0; b < 4; ++b) T[a * 4 + b] = fma(mc2, gr[b + 2] - gr[b], T[a * 4 + b]);
+                for (int b = 0; b < 4; ++b) acc[a * 4 + b][3] = fma(mc2, gr[b + 2] - gr[b], acc[a * 4 + b][3]);
             }
         }
 
-        // ---- y arms: y stencil, diag(y,vy), diag(y,vx), folded src operand --
+        // ---- y arms: y stencil, the arm rows' y corners, folded src operand --
         if (inner) {
             const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                asm volatile("" ::: "memory");  // keep the per-b loads from being hoisted (register pressure)
+                SCHED_FENCE();
                 const double qm = rm[b * TW], qp = rp[b * TW];
                 const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
                 const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
@@ -388,59 +443,55 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
                     w0 = wneg(ym2, qm, z0, z1, qp, y3);
                     w1 = wneg(qm, z0, z1, qp, y3, y4);
                 }
-                double t0 = fma(ay_s, w0, T[b]), t1 = fma(ay_s, w1, T[4 + b]);
-                t0 = fma(c4[0], Gc[4 + b] - Gm, t0);      // diag(y,vy) = G(y+1) - G(y-1)
-                t1 = fma(c4[1], Gp - Gc[b], t1);
-                t0 = fma(-c3[0], Dk[4 + b] - Dkm, t0);    // diag(y,vx) = D(y+1) - D(y-1)
-                t1 = fma(-c3[1], Dkp - Dk[b], t1);
-                T[b] = fma(kfold, z0, t0);
-                T[4 + b] = fma(kfold, z1, t1);
+                double t0 = fma(ay_s, w0, acc[b][3]), t1 = fma(ay_s, w1, acc[4 + b][3]);
+                t0 = fma(-c4[0], Gm, fma(c3[0], Dkm, t0));  // row -1 feeds row 0 with the minus sign
+                t1 = fma(c4[1], Gp, fma(-c3[1], Dkp, t1));  // row 2 feeds row 1 with the plus sign
+                acc[b][3] = fma(kfold, z0, t0);
+                acc[4 + b][3] = fma(kfold, z1, t1);
             }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) T[i] = 0.0;
         }
 
-        // ---- scatter into the accumulator ring, extract cell q --------------
-        // x-coupled corrections: cell p-1 gets c1(p-1) D(p) - c5(p-1) G(p), cell p+1 the negative with c(p+1)
-        double Xm[8], Xp[8], fin[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int a = i >> 2;
-            const double *e0 = tb + a * 8, *e2 = e0 + 2 * BJ * 8;
-            Xm[i] = fma(e0[T_C1], Dk[i], -e0[T_C5] * Gc[i]);
-            Xp[i] = fma(e2[T_C5], Gc[i], -e2[T_C1] * Dk[i]);
-        }
-        window_apply(acc, s0, ax_s, xpos, Xm, Xp, T, fin);
-
+        // ---- x stencil scatter, extract cell q, slide the window -------------
+        double fin[8];
+        window_apply(acc, s0, ax_s, xpos, fin);
 
         // ---- finalise cells q: RK combination, store, non-finite, moment ----
         if (fin_q) {
-            if (nops) {
-                tma::mbar_wait(opbar, op_par);
-                op_par ^= 1u;
-            }
+            if (nops) tma::mbar_wait_s(opbar, (q - i0) & 1);  // the (q-i0)-th use of the operand barrier
             const double *op = opbuf + ooff;
             double out[8];
+            if (nops == 0) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int a = i >> 2, b = i & 3;
-                const int oi = a * BK * OPW + b * OPW;
-                double rk = 0.0;
-                if (nops > 0) rk = oc0 * op[oi];
-                if (nops > 1) rk = fma(oc1, op[OPE + oi], rk);
-                const long long g = gq + a * P2 + b * P3;
-                if (P.fold && !fold) rk = fma(P.cfold, P.src[g], rk);
-                out[i] = fma(cL, fin[i], rk);
-                __stcs(P.dest + g, out[i]);
+                for (int i = 0; i < 8; ++i) out[i] = cL * fin[i];
+            } else if (nops == 1) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) out[i] = fma(cL, fin[i], oc0 * op[(i >> 2) * BK * OPW + (i & 3) * OPW]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int oi = (i >> 2) * BK * OPW + (i & 3) * OPW;
+                    out[i] = fma(cL, fin[i], fma(oc1, op[OPE + oi], oc0 * op[oi]));
+                }
             }
-            if (P.nonfinite) {
+            double *dq = P.dest + gq;
+            if (fold_fb) {  // cL == 0: the src operand could not be folded
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    if (!isfinite(out[i]))
-                        atomicMin(P.nonfinite,
-                                  (((unsigned long long)q * P.Ny + y0 + (i >> 2)) * P.Nvx + vx0 + (i & 3)) * P.Nvy +
-                                      vy);
+                    out[i] = fma(P.cfold, P.src[gq + (i >> 2) * P2 + (i & 3) * P3], out[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) __stcs(dq + (i >> 2) * P2 + (i & 3) * P3, out[i]);
+            if (P.nonfinite) {
+                // inf/nan propagate through the sum (a finite overflow only
+                // sends the thread to the exact per-cell scan)
+                const double sum = ((out[0] + out[1]) + (out[2] + out[3])) + ((out[4] + out[5]) + (out[6] + out[7]));
+                if (!isfinite(sum)) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (!isfinite(out[i]))
+                            atomicMin(P.nonfinite,
+                                      (((unsigned long long)q * P.Ny + y0 + (i >> 2)) * P.Nvx + vx0 + (i & 3)) * P.Nvy + vy);
+                }
             }
             if (P.partials) {
                 // reference fold tree over each aligned 16-wide vy chunk
