@@ -99,23 +99,48 @@ REASON_BITS = {
 
 
 class ClockSampler:
-    def __init__(self, gpu_index):
+    """SM clock and clock-event reasons sampled through NVML every few ms while
+    the timed region runs (nvidia-smi as a fallback when pynvml is missing)."""
+
+    def __init__(self, gpu_index, period_s=0.005):
         self.gpu = gpu_index
+        self.period = period_s
         self.samples = []
         self._stop = threading.Event()
+        self._thread = None
         self._proc = None
 
     def __enter__(self):
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                             float(smax),
+                                             int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                    except pynvml.NVMLError:
+                        pass
+                    self._stop.wait(self.period)
+
+            self._thread = threading.Thread(target=poll, daemon=True)
             self._thread.start()
-        except (OSError, ValueError):
-            self._proc = None
+        except Exception:  # noqa: BLE001 -- no NVML: fall back to nvidia-smi
+            try:
+                self._proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self._thread = threading.Thread(target=self._read, daemon=True)
+                self._thread.start()
+            except (OSError, ValueError):
+                self._proc = None
         return self
 
     def _read(self):
@@ -128,12 +153,15 @@ class ClockSampler:
                     pass
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self._proc is not None:
             self._proc.terminate()
             try:
                 self._proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self._proc.kill()
+        if self._thread is not None:
+            self._thread.join(timeout=5)
 
     def summary(self):
         if not self.samples:

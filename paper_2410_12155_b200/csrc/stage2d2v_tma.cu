@@ -71,7 +71,8 @@ struct Stage22 {
 };
 
 namespace rb {
-constexpr int BJ = 8, BK = 16, BL = 16, NS = 3, THREADS = 256;
+constexpr int BJ = 8, BK = 16, BL = 16, NS = 3;
+constexpr int threads(int bb) { return (BJ / 2) * (BK / bb) * BL; }  // one thread per 2 (y) x bb (vx) cells
 constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile extents (vy box starts 16 B aligned)
 constexpr int KL = TK * TW;
 constexpr int HALO = TJ * KL;
@@ -139,23 +140,25 @@ __device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &
     }
 }
 
-// The sign of a_x is per vx; a thread's 4 vx cells share it unless the zero
-// crossing falls inside the quad (one uniform branch, no predication).
-__device__ __forceinline__ void window_apply(double (&acc)[8][6], const double (&s0)[8], const double (&ax_s)[4],
-                                             const bool (&xpos)[4], double (&fin)[8]) {
-    if (xpos[0] && xpos[3]) {
+// The sign of a_x is per vx; a thread's BB vx cells share it unless the zero
+// crossing falls inside them (one uniform branch, no predication).
+template <int BB>
+__device__ __forceinline__ void window_apply(double (&acc)[2 * BB][6], const double (&s0)[2 * BB],
+                                             const double (&ax_s)[BB], const bool (&xpos)[BB],
+                                             double (&fin)[2 * BB]) {
+    if (xpos[0] && xpos[BB - 1]) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) scatter_cell<1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
-    } else if (!xpos[0] && !xpos[3]) {
+        for (int i = 0; i < 2 * BB; ++i) scatter_cell<1>(acc[i], ax_s[i % BB] * s0[i], fin[i]);
+    } else if (!xpos[0] && !xpos[BB - 1]) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) scatter_cell<-1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+        for (int i = 0; i < 2 * BB; ++i) scatter_cell<-1>(acc[i], ax_s[i % BB] * s0[i], fin[i]);
     } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (xpos[i & 3])
-                scatter_cell<1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+        for (int i = 0; i < 2 * BB; ++i) {
+            if (xpos[i % BB])
+                scatter_cell<1>(acc[i], ax_s[i % BB] * s0[i], fin[i]);
             else
-                scatter_cell<-1>(acc[i], ax_s[i & 3] * s0[i], fin[i]);
+                scatter_cell<-1>(acc[i], ax_s[i % BB] * s0[i], fin[i]);
         }
     }
 }
@@ -193,7 +196,9 @@ __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Ma
     }
 }
 
-__global__ void __launch_bounds__(rb::THREADS, 1)
+// BB = vx cells per thread (4: 256 threads, 2: 512 threads); 2 y cells each
+template <int BB>
+__global__ void __launch_bounds__(rb::threads(BB), 1)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -226,12 +231,13 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    // thread -> cells (y0 + a, vx0 + b, vy), a < 2, b < 4
+    // thread -> cells (y0 + a, vx0 + b, vy), a < 2, b < BB
     const int lane = tid & 31, warp = tid >> 5;
     const int tl = lane & 15;
     const int rg = (warp << 1) | (lane >> 4);
-    const int tj = rg >> 2, tk = rg & 3;
-    const int y0 = j0 + 2 * tj, vx0 = k0 + 4 * tk, vy = l0 + tl;
+    constexpr int NC = 2 * BB;  // cells per thread
+    const int tj = rg / (BK / BB), tk = rg % (BK / BB);
+    const int y0 = j0 + 2 * tj, vx0 = k0 + BB * tk, vy = l0 + tl;
 
     int yl = j0 - 3, yh = j0 + BJ;
     if (P.wrap_y) {
@@ -256,10 +262,10 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     }
 
     // per-thread constants
-    double ax_s[4], bvx[4];
-    bool xpos[4];
+    double ax_s[BB], bvx[BB];
+    bool xpos[BB];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < BB; ++b) {
         const double v = __ldg(P.vxc + vx0 + b);
         ax_s[b] = v * P.mhx;
         xpos[b] = v > 0.0;
@@ -269,8 +275,12 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     const double ay_s = vyv * P.mhy;
     const bool ypos = vyv > 0.0;
     const double cBvy = P.cB * vyv;
-    const double bvx_min = fmin(fmin(bvx[0], bvx[1]), fmin(bvx[2], bvx[3]));
-    const double bvx_max = fmax(fmax(bvx[0], bvx[1]), fmax(bvx[2], bvx[3]));
+    double bvx_min = bvx[0], bvx_max = bvx[0];
+#pragma unroll
+    for (int b = 1; b < BB; ++b) {
+        bvx_min = fmin(bvx_min, bvx[b]);
+        bvx_max = fmax(bvx_max, bvx[b]);
+    }
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
     const bool fold = P.fold && cL != 0.0;        // else the src operand is read at finalisation
     const double kfold = fold ? P.cfold / cL : 0.0;
@@ -279,8 +289,8 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     const int nops = P.nops;
     const double oc0 = P.opc[0], oc1 = P.opc[1];
 
-    const int off = ((2 * tj + 3) * TK + (4 * tk + 3)) * TW + (tl + 3);  // cell (a=0, b=0) in the halo tile
-    const int ooff = ((2 * tj) * BK + 4 * tk) * OPW + tl + 1;           // cell (0, 0) in an operand tile
+    const int off = ((2 * tj + 3) * TK + (BB * tk + 3)) * TW + (tl + 3);  // cell (a=0, b=0) in the halo tile
+    const int ooff = ((2 * tj) * BK + BB * tk) * OPW + tl + 1;          // cell (0, 0) in an operand tile
     const int toff = (2 * tj) * 8;                                      // table entry of row y0, plane p-1
 
     const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
@@ -289,9 +299,9 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
     long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(y0 + NG) * P2 +
                    (long long)(vx0 + NG) * P3 + (vy + NG);
 
-    double acc[8][6];
+    double acc[NC][6];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < NC; ++i)
 #pragma unroll
         for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
@@ -332,92 +342,96 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
         // D = s[vx-1]-s[vx+1]:  c4 diag(y,vy) = c4 (G(y+1) - G(y-1)),
         // -c3 diag(y,vx) = -c3 (D(y+1) - D(y-1)); each row's G and D are
         // consumed as soon as they exist (rows -1 and 2 are the y arms).
-        double s0[8];
+        double s0[NC];
 
         // ---- own rows (a = 0, 1): vy lines, vx lines, D and G -------------
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
             SCHED_FENCE();  // one row at a time
             const double *ca = c + a * KL;
-            double v[4][7];
+            double v[BB][7];
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
+            for (int b = 0; b < BB; ++b)
 #pragma unroll
                 for (int d = 0; d < 7; ++d) v[b][d] = ca[b * TW + d - 3];
-            double r0[10];  // vy-offset-0 values at vx offsets -3 .. 6
+            double r0[BB + 6];  // vy-offset-0 values at vx offsets -3 .. BB+2
             r0[0] = ca[-3 * TW];
             r0[1] = ca[-2 * TW];
             r0[2] = ca[-TW];
-            r0[7] = ca[4 * TW];
-            r0[8] = ca[5 * TW];
-            r0[9] = ca[6 * TW];
-            double G[4], D[4];
+            r0[BB + 3] = ca[BB * TW];
+            r0[BB + 4] = ca[(BB + 1) * TW];
+            r0[BB + 5] = ca[(BB + 2) * TW];
+            double G[BB], D[BB];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < BB; ++b) {
                 r0[b + 3] = v[b][3];
-                s0[a * 4 + b] = v[b][3];
+                s0[a * BB + b] = v[b][3];
                 G[b] = v[b][2] - v[b][4];
             }
 #pragma unroll
-            for (int b = 0; b < 4; ++b) D[b] = r0[b + 2] - r0[b + 4];
+            for (int b = 0; b < BB; ++b) D[b] = r0[b + 2] - r0[b + 4];
             // x-coupled corrections: cell p-1 gets c1(p-1) D(p) - c5(p-1) G(p),
             // cell p+1 gets -c1(p+1) D(p) + c5(p+1) G(p)
             const double *e0 = tb + a * 8, *e2 = e0 + 2 * BJ * 8;
             const double c1m = e0[T_C1], c5m = e0[T_C5], c1p = e2[T_C1], c5p = e2[T_C5];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int i = a * 4 + b;
+            for (int b = 0; b < BB; ++b) {
+                const int i = a * BB + b;
                 acc[i][2] = fma(c1m, D[b], fma(-c5m, G[b], acc[i][2]));
                 acc[i][4] = fma(-c1p, D[b], fma(c5p, G[b], acc[i][4]));
             }
             if (inner) {
                 // y corners of the other own row: G(0) and D(0) feed cell row 1
                 // with the minus sign, G(1) and D(1) feed row 0 with the plus sign
-                const int o = (1 - a) * 4;
+                const int o = (1 - a) * BB;
                 const double sg = a ? 1.0 : -1.0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b)
+                for (int b = 0; b < BB; ++b)
                     acc[o + b][3] = fma(sg * c4[1 - a], G[b], fma(-sg * c3[1 - a], D[b], acc[o + b][3]));
                 const double gm = ca[-TW - 1] - ca[-TW + 1];         // G at vx offset -1
-                const double gp = ca[4 * TW - 1] - ca[4 * TW + 1];   // G at vx offset 4
+                const double gp = ca[BB * TW - 1] - ca[BB * TW + 1];  // G at vx offset BB
                 const double avx = evx[a] + cBvy;                    // a_vx is independent of vx
                 const double avx_s = avx * mhvx;
                 if (avx > 0.0) {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        acc[a * 4 + b][3] = fma(avx_s, wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]),
-                                                acc[a * 4 + b][3]);
+                    for (int b = 0; b < BB; ++b)
+                        acc[a * BB + b][3] = fma(avx_s, wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]),
+                                                acc[a * BB + b][3]);
                 } else {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        acc[a * 4 + b][3] = fma(avx_s, wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]),
-                                                acc[a * 4 + b][3]);
+                    for (int b = 0; b < BB; ++b)
+                        acc[a * BB + b][3] = fma(avx_s, wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]),
+                                                acc[a * BB + b][3]);
                 }
                 // a_vy = evy - cB vx: one branch for the row when the four
                 // signs agree (always when cB == 0; fl(e + x) is monotone in x)
                 if (evy[a] + bvx_min > 0.0) {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        acc[a * 4 + b][3] = fma((evy[a] + bvx[b]) * mhvy,
-                                                wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]), acc[a * 4 + b][3]);
+                    for (int b = 0; b < BB; ++b)
+                        acc[a * BB + b][3] = fma((evy[a] + bvx[b]) * mhvy,
+                                                wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]), acc[a * BB + b][3]);
                 } else if (evy[a] + bvx_max <= 0.0) {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        acc[a * 4 + b][3] = fma((evy[a] + bvx[b]) * mhvy,
-                                                wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]), acc[a * 4 + b][3]);
+                    for (int b = 0; b < BB; ++b)
+                        acc[a * BB + b][3] = fma((evy[a] + bvx[b]) * mhvy,
+                                                wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]), acc[a * BB + b][3]);
                 } else {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
+                    for (int b = 0; b < BB; ++b) {
                         const double avy = evy[a] + bvx[b];
                         const double w = avy > 0.0 ? wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
                                                    : wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
-                        acc[a * 4 + b][3] = fma(avy * mhvy, w, acc[a * 4 + b][3]);
+                        acc[a * BB + b][3] = fma(avy * mhvy, w, acc[a * BB + b][3]);
                     }
                 }
                 // diag(vx,vy) = G(vx+1) - G(vx-1)
-                const double gr[6] = {gm, G[0], G[1], G[2], G[3], gp};
+                double gr[BB + 2];
+                gr[0] = gm;
+                gr[BB + 1] = gp;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a * 4 + b][3] = fma(mc2, gr[b + 2] - gr[b], acc[a * 4 + b][3]);
+                for (int b = 0; b < BB; ++b) gr[b + 1] = G[b];
+#pragma unroll
+                for (int b = 0; b < BB; ++b) acc[a * BB + b][3] = fma(mc2, gr[b + 2] - gr[b], acc[a * BB + b][3]);
             }
         }
 
@@ -425,14 +439,14 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
         if (inner) {
             const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < BB; ++b) {
                 SCHED_FENCE();
                 const double qm = rm[b * TW], qp = rp[b * TW];
                 const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
                 const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
                 const double Dkm = rm[(b - 1) * TW] - rm[(b + 1) * TW];
                 const double Dkp = rp[(b - 1) * TW] - rp[(b + 1) * TW];
-                const double z0 = s0[b], z1 = s0[4 + b];
+                const double z0 = s0[b], z1 = s0[BB + b];
                 double w0, w1;
                 if (ypos) {
                     const double ym3 = c[-3 * KL + b * TW], ym2 = c[-2 * KL + b * TW], y3 = c[3 * KL + b * TW];
@@ -443,80 +457,99 @@ __global__ void __launch_bounds__(rb::THREADS, 1)
                     w0 = wneg(ym2, qm, z0, z1, qp, y3);
                     w1 = wneg(qm, z0, z1, qp, y3, y4);
                 }
-                double t0 = fma(ay_s, w0, acc[b][3]), t1 = fma(ay_s, w1, acc[4 + b][3]);
+                double t0 = fma(ay_s, w0, acc[b][3]), t1 = fma(ay_s, w1, acc[BB + b][3]);
                 t0 = fma(-c4[0], Gm, fma(c3[0], Dkm, t0));  // row -1 feeds row 0 with the minus sign
                 t1 = fma(c4[1], Gp, fma(-c3[1], Dkp, t1));  // row 2 feeds row 1 with the plus sign
                 acc[b][3] = fma(kfold, z0, t0);
-                acc[4 + b][3] = fma(kfold, z1, t1);
+                acc[BB + b][3] = fma(kfold, z1, t1);
             }
         }
 
         // ---- x stencil scatter, extract cell q, slide the window -------------
-        double fin[8];
-        window_apply(acc, s0, ax_s, xpos, fin);
+        double fin[NC];
+        window_apply<BB>(acc, s0, ax_s, xpos, fin);
 
         // ---- finalise cells q: RK combination, store, non-finite, moment ----
         if (fin_q) {
             if (nops) tma::mbar_wait_s(opbar, (q - i0) & 1);  // the (q-i0)-th use of the operand barrier
             const double *op = opbuf + ooff;
-            double out[8];
+            double out[NC];
             if (nops == 0) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) out[i] = cL * fin[i];
+                for (int i = 0; i < NC; ++i) out[i] = cL * fin[i];
             } else if (nops == 1) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) out[i] = fma(cL, fin[i], oc0 * op[(i >> 2) * BK * OPW + (i & 3) * OPW]);
+                for (int i = 0; i < NC; ++i) out[i] = fma(cL, fin[i], oc0 * op[(i / BB) * BK * OPW + (i % BB) * OPW]);
             } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int oi = (i >> 2) * BK * OPW + (i & 3) * OPW;
+                for (int i = 0; i < NC; ++i) {
+                    const int oi = (i / BB) * BK * OPW + (i % BB) * OPW;
                     out[i] = fma(cL, fin[i], fma(oc1, op[OPE + oi], oc0 * op[oi]));
                 }
             }
             double *dq = P.dest + gq;
             if (fold_fb) {  // cL == 0: the src operand could not be folded
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    out[i] = fma(P.cfold, P.src[gq + (i >> 2) * P2 + (i & 3) * P3], out[i]);
+                for (int i = 0; i < NC; ++i)
+                    out[i] = fma(P.cfold, P.src[gq + (i / BB) * P2 + (i % BB) * P3], out[i]);
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) __stcs(dq + (i >> 2) * P2 + (i & 3) * P3, out[i]);
+            for (int i = 0; i < NC; ++i) __stcs(dq + (i / BB) * P2 + (i % BB) * P3, out[i]);
             if (P.nonfinite) {
                 // inf/nan propagate through the sum (a finite overflow only
                 // sends the thread to the exact per-cell scan)
-                const double sum = ((out[0] + out[1]) + (out[2] + out[3])) + ((out[4] + out[5]) + (out[6] + out[7]));
+                double sum = out[0];
+#pragma unroll
+                for (int i = 1; i < NC; ++i) sum += out[i];
                 if (!isfinite(sum)) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < NC; ++i)
                         if (!isfinite(out[i]))
                             atomicMin(P.nonfinite,
-                                      (((unsigned long long)q * P.Ny + y0 + (i >> 2)) * P.Nvx + vx0 + (i & 3)) * P.Nvy + vy);
+                                      (((unsigned long long)q * P.Ny + y0 + (i / BB)) * P.Nvx + vx0 + (i % BB)) * P.Nvy + vy);
                 }
             }
             if (P.partials) {
                 // reference fold tree over each aligned 16-wide vy chunk
-                // (fields.py:28-47): transpose-reduce the 8 rows over the 16
+                // (fields.py:28-47): transpose-reduce the NC rows over the 16
                 // vy lanes; after level k lane bit k-1 selects the row half
-                const bool o1 = tl & 1, o2 = tl & 2, o4 = tl & 4;
-                double w4[4], w2[2];
+                double w1;
+                if (NC == 8) {
+                    const bool o1 = tl & 1, o2 = tl & 2, o4 = tl & 4;
+                    double w4[4], w2[2];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const double keep = o1 ? out[2 * m + 1] : out[2 * m];
-                    const double send = o1 ? out[2 * m] : out[2 * m + 1];
-                    w4[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
-                }
+                    for (int m = 0; m < 4; ++m) {
+                        const double keep = o1 ? out[2 * m + 1] : out[2 * m];
+                        const double send = o1 ? out[2 * m] : out[2 * m + 1];
+                        w4[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                    }
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const double keep = o2 ? w4[2 * m + 1] : w4[2 * m];
-                    const double send = o2 ? w4[2 * m] : w4[2 * m + 1];
-                    w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                    for (int m = 0; m < 2; ++m) {
+                        const double keep = o2 ? w4[2 * m + 1] : w4[2 * m];
+                        const double send = o2 ? w4[2 * m] : w4[2 * m + 1];
+                        w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                    }
+                    const double keep = o4 ? w2[1] : w2[0];
+                    const double send = o4 ? w2[0] : w2[1];
+                    w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
+                } else {  // NC == 4
+                    const bool o1 = tl & 1, o2 = tl & 2;
+                    double w2[2];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const double keep = o1 ? out[2 * m + 1] : out[2 * m];
+                        const double send = o1 ? out[2 * m] : out[2 * m + 1];
+                        w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                    }
+                    const double keep = o2 ? w2[1] : w2[0];
+                    const double send = o2 ? w2[0] : w2[1];
+                    w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
                 }
-                const double keep = o4 ? w2[1] : w2[0];
-                const double send = o4 ? w2[0] : w2[1];
-                double w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
-                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
-                if (tl < 8) {  // lane tl holds row tl = 4a + b
-                    const long long pr = (((long long)q * P.Ny + y0 + (tl >> 2)) * P.Nvx + vx0 + (tl & 3));
+                if (tl < NC) {  // lane tl holds row tl = BB a + b
+                    const long long pr = (((long long)q * P.Ny + y0 + tl / BB) * P.Nvx + vx0 + tl % BB);
                     P.partials[pr * nlt + lt] = w1;
                 }
             }
@@ -625,13 +658,18 @@ static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], co
     }
     P.sj = sjk[0] > 0 ? sjk[0] : 1;
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(stage2d2v_rb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        attr = true;
+    static int bb = -1;
+    if (bb < 0) {  // vx cells per thread: 4 (256 threads) or 2 (512 threads)
+        const char *e = getenv("VPFV_RB_BB");
+        bb = (e && atoi(e) == 2) ? 2 : 4;
+        cudaFuncSetAttribute(stage2d2v_rb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(stage2d2v_rb_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     }
     const int nblocks = tma_2d2v_columns(P.Ny, P.Nvx, P.Nvy) * P.nseg;
-    stage2d2v_rb_kernel<<<nblocks, THREADS, SMEM, s>>>(maps, P);
+    if (bb == 2)
+        stage2d2v_rb_kernel<2><<<nblocks, threads(2), SMEM, s>>>(maps, P);
+    else
+        stage2d2v_rb_kernel<4><<<nblocks, threads(4), SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
 }
 

@@ -100,13 +100,17 @@ class Simulation:
         self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._graphs = {}
         self._launches = {}
-        # fused velocity moment: stages 1-3 emit the moment partials of their
-        # dest, which is the next stage's src (stage 1 of a step always runs
-        # the standalone moment, so external edits of f0 are honoured)
+        # fused velocity moment: every stage emits the moment partials of its
+        # dest, which is the next stage's src; stage 4's partials (of the new
+        # f0) serve the next step's stage 1 unless f0 was modified in place
+        # since (torch's version counter) -- then the standalone moment runs
         self.tiled = [t.fused_moment_ok(f) for t, f in zip(self.tables, self.flags)]
         self.fuse_moment = all(self.tiled)
-        self.partials = ([torch.empty(t.partials_shape(), dtype=torch.float64, device=self.device)
-                          for t in self.tables] if self.fuse_moment else None)
+        mk = lambda: ([torch.empty(t.partials_shape(), dtype=torch.float64, device=self.device)  # noqa: E731
+                       for t in self.tables] if self.fuse_moment else None)
+        self.partials = mk()       # written by stages 1-3, read by stages 2-4
+        self.partials_next = mk()  # written by stage 4 (moment of the new f0), read by the next stage 1
+        self._moment_of = None  # (data_ptr, _version) of the f0 arrays the partials describe
         self._last_E = None
         self._timing = False
         self._events = None
@@ -125,12 +129,13 @@ class Simulation:
         return (self.ctx.f0, self.ctx.f1, self.ctx.fout)
 
     # -- the stage protocol (timestepping.py:69-84 calls this) ---------------
-    def _stage(self, dest, A, B, src, ca, cb, cd, cL, t, *, dt_dev=None, cL_div=1.0, slot=None):
+    def _stage(self, dest, A, B, src, ca, cb, cd, cL, t, *, dt_dev=None, cL_div=1.0, slot=None, cached=False,
+               emit_last=True):
         stream = stream_handle(self.device)
-        use_partials = self.fuse_moment and slot is not None and slot > 0
-        emit_partials = self.fuse_moment and slot is not None and slot < 3
+        use_partials = self.fuse_moment and slot is not None and (slot > 0 or cached)
+        emit_partials = self.fuse_moment and slot is not None and (slot < 3 or emit_last)
         if use_partials:
-            E = self.fields.solve_from_partials(self.partials, stream=stream)
+            E = self.fields.solve_from_partials(self.partials if slot > 0 else self.partials_next, stream=stream)
         else:
             E = self.fields.solve(src, stream=stream)
         self._last_E = E
@@ -142,17 +147,18 @@ class Simulation:
                 self._events[slot][s][0].record()
             tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
                        dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
-                       partials=self.partials[s] if emit_partials else None, packed=self.tiled[s])
+                       partials=(self.partials if slot < 3 else self.partials_next)[s] if emit_partials else None,
+                       packed=self.tiled[s])
             if timed:
                 self._events[slot][s][1].record()
 
-    def _step_body(self, f0, f1, fout):
+    def _step_body(self, f0, f1, fout, cached=False, emit_last=True):
         bufs = {"f0": f0, "f1": f1, "fout": fout}
         start = _lib.launch_counter[0]
         self.nonfinite.fill_(-1)
         for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, None,
-                        dt_dev=self.dt_dev, cL_div=div, slot=slot)
+                        dt_dev=self.dt_dev, cL_div=div, slot=slot, cached=cached, emit_last=emit_last)
         self._launches["step"] = _lib.launch_counter[0] - start
 
     # -- in-step timing of the fused stage kernel (bench roofline) -----------
@@ -182,29 +188,37 @@ class Simulation:
         """libvpfv kernels launched per RK4 step (counted while capturing/running it)."""
         return self._launches.get("step", 0)
 
-    def _graph_for(self, bufs):
-        key = (self._timing,) + tuple(tuple(a.data_ptr() for a in b) for b in bufs)
+    def _graph_for(self, bufs, cached=False):
+        key = (self._timing, cached) + tuple(tuple(a.data_ptr() for a in b) for b in bufs)
         g = self._graphs.get(key)
         if g is None:
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
-            with torch.cuda.stream(side):  # warm-up: first launches outside capture
-                self._step_body(*bufs)
+            with torch.cuda.stream(side):  # warm-up: first launches outside capture; it must
+                self._step_body(*bufs, emit_last=False)  # leave the next-step partials untouched
             torch.cuda.current_stream(self.device).wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._step_body(*bufs)
+                self._step_body(*bufs, cached=cached)
             self._graphs[key] = g
         return g
+
+    @staticmethod
+    def _signature(arrays):
+        return tuple((a.data_ptr(), a._version) for a in arrays)
 
     def launch_step(self, dt):
         """Enqueue one RK4 step (no host sync, no rotate)."""
         self.dt_dev.fill_(float(dt))
         bufs = (self.ctx.f0, self.ctx.f1, self.ctx.fout)
+        # the partials left by the previous step's stage 4 describe f0 when f0
+        # is that step's output and nothing wrote it since
+        cached = self.fuse_moment and self._moment_of == self._signature(self.ctx.f0)
         if self.use_graphs:
-            self._graph_for(bufs).replay()
+            self._graph_for(bufs, cached).replay()
         else:
-            self._step_body(*bufs)
+            self._step_body(*bufs, cached=cached)
+        self._moment_of = self._signature(self.ctx.fout) if self.fuse_moment else None
 
     # -- timestep control -----------------------------------------------------
     def _E_host(self, arrays):

@@ -499,3 +499,26 @@ def test_1d2v_fused_path_steps_vs_c_oracle(maker):
         ref.advance(dt)
         for a, b in zip(sim.interiors(), ref.interiors()):
             assert rel_l2(a, b) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_fused_moment_cache_honours_inplace_edits():
+    """Stage 4 leaves the moment partials of the new f0 for the next step's
+    stage 1; an in-place edit of f0 in between (tensor version bump) must send
+    the next step back to the standalone moment."""
+    from oracle import cbackend as C
+
+    setup = P.make_problem(P.landau_spec(), 32, 32)
+    sim = R.Simulation(setup)
+    dt = 0.9 * sim.max_dt()
+    sim.fixed_dt = dt
+    for _ in range(2):  # the second step runs on the cached partials
+        sim.advance(dt)
+    f = sim.ctx.f0[0]
+    f[3:-3, 3:-3, 3:-3, 3:-3].mul_(1.001)  # interior edit through a view
+    start = [a.cpu().numpy().copy() for a in sim.ctx.f0]
+    ref = C.CSimulation([g for g in sim.grids], setup.species, start, dt=dt)
+    for _ in range(2):
+        sim.advance(dt)
+        ref.advance(dt)
+        assert rel_l2(sim.interiors()[0], ref.interiors()[0]) <= 1e-12
