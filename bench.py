@@ -64,7 +64,7 @@ def make_setup(name):
     raise ValueError(name)
 
 
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_tiled_v4_summary.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_rb_v5_summary.json")
 
 
 def load_traffic():
