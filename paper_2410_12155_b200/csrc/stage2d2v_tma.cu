@@ -71,25 +71,39 @@ struct Stage22 {
 };
 
 namespace rb {
-constexpr int BJ = 8, BK = 16, BL = 16, NS = 3;
-constexpr int threads(int bb) { return (BJ / 2) * (BK / bb) * BL; }  // one thread per 2 (y) x bb (vx) cells
-constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile extents (vy box starts 16 B aligned)
-constexpr int KL = TK * TW;
-constexpr int HALO = TJ * KL;
-constexpr int TAB = 3 * BJ * 8;  // packed tables of planes p-1, p, p+1
-constexpr int STAGE = HALO + TAB;
-constexpr int OPW = BL + 2;      // RK operand row (16 B aligned start)
-constexpr int OPE = BJ * BK * OPW;
-constexpr int OPS_MAX = 2;
-constexpr int HALO_BYTES = HALO * 8, CORE_BYTES = BJ * KL * 8, TAB_BYTES = TAB * 8, OP_BYTES = OPE * 8;
-constexpr int BAR_OFF = NS * STAGE * 8 + OPS_MAX * OPE * 8;  // NS stage barriers, then the operand barrier
-constexpr int SMEM = BAR_OFF + 64;
-static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
-              "TMA destinations must stay 128 B aligned");
-static_assert(SMEM <= 227 * 1024, "shared memory budget");
+constexpr int BJ = 8, BL = 16, OPS_MAX = 2;
 // packed table entry (vpfv_tables_2d_packed): evx, evy, c3, c4, c1, c5, 0, 0
 enum { T_EVX = 0, T_EVY = 1, T_C3 = 2, T_C4 = 3, T_C1 = 4, T_C5 = 5 };
+// Tile geometry: (BJ, BK, BL) column block, NS-deep stage ring, MINB CTAs
+// per SM; one thread per 2 (y) x BB (vx) cells at one vy lane.
+template <int BK_, int NS_, int MINB_>
+struct Geo {
+    static constexpr int BK = BK_, NS = NS_, MINB = MINB_, BB = 4;
+    static constexpr int THREADS = (BJ / 2) * (BK / BB) * BL;
+    static constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile (vy box starts 16 B aligned)
+    static constexpr int KL = TK * TW, HALO = TJ * KL;
+    static constexpr int TAB = 3 * BJ * 8;  // packed tables of planes p-1, p, p+1
+    static constexpr int STAGE = HALO + TAB;
+    static constexpr int OPW = BL + 2;      // RK operand row (16 B aligned start)
+    static constexpr int OPE = BJ * BK * OPW;
+    static constexpr int HALO_BYTES = HALO * 8, CORE_BYTES = BJ * KL * 8, TAB_BYTES = TAB * 8, OP_BYTES = OPE * 8;
+    static constexpr int BAR_OFF = NS * STAGE * 8 + OPS_MAX * OPE * 8;  // NS stage barriers, then the operand barrier
+    static constexpr int SMEM = BAR_OFF + 64;
+    static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
+                  "TMA destinations must stay 128 B aligned");
+    static_assert(SMEM * MINB <= 228 * 1024 - MINB * 1024, "shared memory budget");
+};
+using GeoWide = Geo<16, 3, 1>;   // (8, 16, 16) tiles, 1 CTA of 8 warps per SM
+using GeoPair = Geo<8, 2, 2>;    // (8, 8, 16) tiles, 2 CTAs of 4 warps per SM (desynchronised)
 }  // namespace rb
+
+#define RB_GEOMETRY(G)                                                                                          \
+    constexpr int BK = G::BK, NS = G::NS, BB = G::BB, TK = G::TK, TW = G::TW, KL = G::KL, HALO = G::HALO,     \
+                  STAGE = G::STAGE, OPW = G::OPW, OPE = G::OPE, HALO_BYTES = G::HALO_BYTES,                    \
+                  CORE_BYTES = G::CORE_BYTES, TAB_BYTES = G::TAB_BYTES, OP_BYTES = G::OP_BYTES,                \
+                  BAR_OFF = G::BAR_OFF;                                                                         \
+    (void)BK, (void)NS, (void)BB, (void)TK, (void)TW, (void)KL, (void)HALO, (void)STAGE, (void)OPW, (void)OPE, \
+        (void)HALO_BYTES, (void)CORE_BYTES, (void)TAB_BYTES, (void)OP_BYTES, (void)BAR_OFF
 
 struct Maps {
     CUtensorMap core, halo, op[rb::OPS_MAX], tab;
@@ -168,10 +182,12 @@ __device__ __forceinline__ void window_apply(double (&acc)[2 * BB][6], const dou
 // y-low halo / core / y-high halo.  complete_tx may land before expect_tx
 // (the transaction count may go transiently negative; the phase cannot
 // complete before part 0 arrives).  On x-halo planes only the core moves.
+template <class GEO>
 __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Maps *M, int n, int p_first,
                                                  const Stage22 &P, int i0, int i1, int l0, int k0, int j0, int cy_lo,
                                                  int cy_core, int cy_hi) {
     using namespace rb;
+    RB_GEOMETRY(GEO);
     const int s = n % NS;
     const unsigned dst = sbase + s * STAGE * 8, bar = sbase + BAR_OFF + s * 8;
     const int p = p_first + n;  // in [i0-3, i1+3)
@@ -196,11 +212,11 @@ __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Ma
     }
 }
 
-// BB = vx cells per thread (4: 256 threads, 2: 512 threads); 2 y cells each
-template <int BB>
-__global__ void __launch_bounds__(rb::threads(BB), 1)
+template <class GEO>
+__global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
+    RB_GEOMETRY(GEO);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     const double *opbuf = stages + NS * STAGE;
@@ -258,7 +274,7 @@ __global__ void __launch_bounds__(rb::threads(BB), 1)
     if (tid == 0) {
         for (int n = 0; n < NS - 1 && n < nplanes; ++n)
             for (int w = 0; w < 4; ++w)
-                issue_plane_part(w, sbase, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
+                issue_plane_part<GEO>(w, sbase, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
     }
 
     // per-thread constants
@@ -311,11 +327,15 @@ __global__ void __launch_bounds__(rb::threads(BB), 1)
         const bool fin_q = q >= i0 && q < i1;
         // producers: plane n+NS-1 into the stage freed at the end of plane n-1,
         // and this plane's RK operand tiles (cell plane q) into the operand buffer
-        if ((tid & 31) == 0) {
-            if (warp < 4 && n + NS - 1 < nplanes)
-                issue_plane_part(warp, sbase, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
-            if (warp >= 4 && warp < 4 + nops && fin_q) {
-                const int o = warp - 4;
+        // (plane parts from lane 0 of warps 0-3; operand o from lane 0 of warp
+        // 4+o, or from lane 16 of warp o when the CTA has only 4 warps)
+        constexpr int NWARPS = GEO::THREADS / 32;
+        if (lane == 0 && warp < 4 && n + NS - 1 < nplanes)
+            issue_plane_part<GEO>(warp, sbase, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
+        {
+            const int o = NWARPS >= 4 + OPS_MAX ? warp - 4 : warp;
+            const bool op_lane = NWARPS >= 4 + OPS_MAX ? lane == 0 : lane == 16;
+            if (op_lane && o >= 0 && o < nops && fin_q) {
                 if (o == 0) tma::mbar_expect_tx_s(opbar, nops * OP_BYTES);
                 tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
             }
@@ -607,26 +627,97 @@ __global__ void moment_partials_kernel(const double *__restrict__ part, double *
     if (lane == 0) n[p] = __dmul_rn(a[0], vol);
 }
 
+// Fast path for power-of-two Nvx (32..256) and chunk counts (1..16): one warp
+// per physical cell, lane L holds the Nvx/32 consecutive vx rows
+// [L*R, L*R+R) (all their chunks, 128-bit loads), folds each row's chunks and
+// then its rows in registers -- the reference tree's first levels -- and the
+// remaining levels with ascending xor shuffles (adjacent pairs first).
+template <int R, int NLT>
+__global__ void __launch_bounds__(256) moment_partials_vec_kernel(const double *__restrict__ part,
+                                                                  double *__restrict__ n, int nphys, double vol) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nphys) return;
+    constexpr int V = R * NLT;  // doubles per lane
+    const double *src = part + ((size_t)warp * 32 + lane) * V;
+    double x[V];
+    if (V % 2 == 0) {
+#pragma unroll
+        for (int t = 0; t < V; t += 2) {
+            const double2 d = __ldcs(reinterpret_cast<const double2 *>(src + t));
+            x[t] = d.x;
+            x[t + 1] = d.y;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < V; ++t) x[t] = __ldcs(src + t);
+    }
+#pragma unroll
+    for (int w = 1; w < NLT * R; w <<= 1)  // chunks of a row, then rows: adjacent pairs, level by level
+#pragma unroll
+        for (int t = 0; t < V; t += 2 * w) x[t] = __dadd_rn(x[t], x[t + w]);
+    double v = x[0];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) n[warp] = __dmul_rn(v, vol);
+}
+
+template <int R>
+static bool launch_vec_r(const double *part, double *n, int nphys, int nlt, double vol, cudaStream_t s) {
+    const int grid = (nphys + 7) / 8;
+    switch (nlt) {
+        case 1: moment_partials_vec_kernel<R, 1><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
+        case 2: moment_partials_vec_kernel<R, 2><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
+        case 4: moment_partials_vec_kernel<R, 4><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
+        case 8: moment_partials_vec_kernel<R, 8><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
+        case 16:
+            if (R <= 4) {
+                moment_partials_vec_kernel<(R <= 4 ? R : 4), 16><<<grid, 256, 0, s>>>(part, n, nphys, vol);
+                return true;
+            }
+            return false;
+        default: return false;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host side: tensor maps and launch
+
+static int tile_cfg(int Nvx, int Nvy) {
+    // 0: (8,16,16) tiles x 1 CTA/SM; 1: (8,8,16) tiles x 2 CTAs/SM, which wins
+    // when the wide tiles leave too few column blocks (measured at 64^4);
+    // VPFV_RB_CFG=0/1 overrides
+    static int env = -2;
+    if (env == -2) {
+        const char *e = getenv("VPFV_RB_CFG");
+        env = e ? atoi(e) : -1;
+    }
+    if (env == 0 || env == 1) return env;
+    return (long long)Nvx * Nvy <= 64 * 64 ? 1 : 0;
+}
+
+static int tile_bk(int Nvx, int Nvy) { return tile_cfg(Nvx, Nvy) == 1 ? rb::GeoPair::BK : rb::GeoWide::BK; }
 
 bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags) {
     if (flags & VPFV_EXACT) return false;
     if (flags & (VPFV_WRAP(2) | VPFV_WRAP(3))) return false;  // velocity ghosts must be stored
-    if (Ny % rb::BJ || Nvx % rb::BK || Nvy % rb::BL) return false;
+    if (Ny % rb::BJ || Nvx % tile_bk(Nvx, Nvy) || Nvy % rb::BL) return false;
     if (Nx < 1 || Ny < rb::BJ) return false;
     return tma_available();
 }
 
-int tma_2d2v_columns(int Ny, int Nvx, int Nvy) { return (Ny / rb::BJ) * (Nvx / rb::BK) * (Nvy / rb::BL); }
+int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
+    return (Ny / rb::BJ) * (Nvx / tile_bk(Nvx, Nvy)) * (Nvy / rb::BL);
+}
 
-static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
-                     unsigned flags, int nseg, cudaStream_t s) {
+template <class GEO>
+static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
+                      unsigned flags, int nseg, cudaStream_t s) {
     using namespace rb;
     const unsigned long long dims[4] = {(unsigned long long)P.Nvy + 6, (unsigned long long)P.Nvx + 6,
                                         (unsigned long long)P.Ny + 6, (unsigned long long)P.Nx + 6};
     const unsigned long long strides[3] = {dims[0] * 8, dims[0] * dims[1] * 8, dims[0] * dims[1] * dims[2] * 8};
-    const unsigned box_core[4] = {TW, TK, BJ, 1}, box_halo[4] = {TW, TK, 3, 1}, box_op[4] = {OPW, BK, BJ, 1};
+    const unsigned box_core[4] = {GEO::TW, GEO::TK, BJ, 1}, box_halo[4] = {GEO::TW, GEO::TK, 3, 1},
+                   box_op[4] = {GEO::OPW, GEO::BK, BJ, 1};
     Maps maps;
     if (!tma_map(src, 4, dims, strides, box_core, &maps.core) || !tma_map(src, 4, dims, strides, box_halo, &maps.halo))
         return set_error(VPFV_ECUDA, "cuTensorMapEncodeTiled failed");
@@ -658,24 +749,34 @@ static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], co
     }
     P.sj = sjk[0] > 0 ? sjk[0] : 1;
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
-    static int bb = -1;
-    if (bb < 0) {  // vx cells per thread: 4 (256 threads) or 2 (512 threads)
-        const char *e = getenv("VPFV_RB_BB");
-        bb = (e && atoi(e) == 2) ? 2 : 4;
-        cudaFuncSetAttribute(stage2d2v_rb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaFuncSetAttribute(stage2d2v_rb_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        attr = true;
     }
-    const int nblocks = tma_2d2v_columns(P.Ny, P.Nvx, P.Nvy) * P.nseg;
-    if (bb == 2)
-        stage2d2v_rb_kernel<2><<<nblocks, threads(2), SMEM, s>>>(maps, P);
-    else
-        stage2d2v_rb_kernel<4><<<nblocks, threads(4), SMEM, s>>>(maps, P);
+    const int nblocks = (P.Ny / BJ) * (P.Nvx / GEO::BK) * (P.Nvy / BL) * P.nseg;
+    stage2d2v_rb_kernel<GEO><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
+}
+
+static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
+                     unsigned flags, int nseg, cudaStream_t s) {
+    if (tile_cfg(P.Nvx, P.Nvy) == 1) return launch_geo<rb::GeoPair>(src, ops, tab, P, flags, nseg, s);
+    return launch_geo<rb::GeoWide>(src, ops, tab, P, flags, nseg, s);
 }
 
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
                                 cudaStream_t s) {
     if (nlt > 16) return set_error(VPFV_EARG, "moment partials: at most 16 vy chunks");
+    bool done = false;
+    switch (nvx) {
+        case 32: done = launch_vec_r<1>(part, n, nphys, nlt, vol, s); break;
+        case 64: done = launch_vec_r<2>(part, n, nphys, nlt, vol, s); break;
+        case 128: done = launch_vec_r<4>(part, n, nphys, nlt, vol, s); break;
+        case 256: done = launch_vec_r<8>(part, n, nphys, nlt, vol, s); break;
+        default: break;
+    }
+    if (done) return check_launch("moment_from_partials");
     const int wpb = 4;
     size_t smem = sizeof(double) * (size_t)wpb * 2 * nvx;
     static bool attr = false;

@@ -350,7 +350,8 @@ def _interior_mask(g):
     return m
 
 
-@pytest.mark.parametrize("N", [(8, 8, 16, 32), (12, 16, 32, 128), (10, 24, 16, 64)])
+@pytest.mark.parametrize("N", [(8, 8, 16, 32), (12, 16, 32, 128), (10, 24, 16, 64), (8, 8, 64, 64),
+                               (8, 8, 128, 32), (8, 8, 256, 16), (8, 8, 32, 256)])
 def test_tiled_stage_wrap_reads_interior_and_fused_moment(N):
     """With x/y read by modular index the physical ghosts may hold garbage;
     the fused epilogue's moment partials fold to the reference fold tree."""
