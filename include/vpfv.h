@@ -117,6 +117,23 @@ int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const 
                           double *moment_partials, int xsegments, void *stream);
 int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags);
 
+/* vpfv_stage_2d2v_fused restricted to the interior x cells [x_begin, x_end)
+ * (tiled path only; VPFV_EARG otherwise).  Planes x_begin-3 .. x_end+2 are
+ * read, so a slab whose x ghosts are still in flight can update its x
+ * interior [3, Nx-3) while they arrive, then [0, 3) and [Nx-3, Nx): the
+ * overlapped halo exchange of paper_2410_12155_b200.parallel.  Replaces the
+ * per-box stage of SimulatedCluster._stage (runner.py:394-437). */
+int vpfv_stage_2d2v_fused_range(double *dest, const double *A, const double *B, const double *src,
+                                double ca, double cb, double cd, double cL,
+                                const double *vxc, const double *vyc, const double *evx,
+                                const double *evy, double cB, const double *c1, double c2,
+                                const double *c3, const double *c4, const double *c5,
+                                double hx, double hy, double hvx, double hvy,
+                                int Nx, int Ny, int Nvx, int Nvy, int x_begin, int x_end,
+                                unsigned flags, const double *dt_dev, double cL_div,
+                                unsigned long long *nonfinite, const double *packed_tables,
+                                double *moment_partials, void *stream);
+
 /* 1 when vpfv_stage_2d2v_fused would take the tiled path (and so accepts
  * moment_partials) for these extents and flags, else 0. */
 int vpfv_stage_2d2v_tiled_ok(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);

@@ -337,7 +337,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             const bool op_lane = NWARPS >= 4 + OPS_MAX ? lane == 0 : lane == 16;
             if (op_lane && o >= 0 && o < nops && fin_q) {
                 if (o == 0) tma::mbar_expect_tx_s(opbar, nops * OP_BYTES);
+#ifdef VPFV_OP_EVICT_FIRST  // RK operands are read once: keep them from displacing src halos in L2
+                tma::load4d_s_hint(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG,
+                                   tma::policy_evict_first());
+#else
                 tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
+#endif
             }
         }
         // stage and parity from the plane number (loop-carried counters get spilled)
@@ -736,10 +741,8 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     if (!tma_map(tab, 3, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
     P.wrap_x = (flags & VPFV_WRAP(0)) != 0;
     P.wrap_y = (flags & VPFV_WRAP(1)) != 0;
-    P.i0 = 0;
-    P.i1 = P.Nx;
     P.nseg = nseg < 1 ? 1 : nseg;
-    P.seglen = (P.Nx + P.nseg - 1) / P.nseg;
+    P.seglen = (P.i1 - P.i0 + P.nseg - 1) / P.nseg;  // the caller set the x range [i0, i1)
     static int sjk[2] = {-1, -1};
     if (sjk[0] < 0) {
         const char *e = getenv("VPFV_SUPER");
@@ -826,22 +829,25 @@ struct Operands {
 };
 }  // namespace
 
-extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B,
-                                     const double *src, double ca, double cb, double cd, double cL,
-                                     const double *vxc, const double *vyc, const double *evx,
-                                     const double *evy, double cB, const double *c1, double c2,
-                                     const double *c3, const double *c4, const double *c5, double hx,
-                                     double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
-                                     int Nvy, unsigned flags, const double *dt_dev, double cL_div,
-                                     unsigned long long *nonfinite, const double *packed_tables,
-                                     double *moment_partials, int xsegments, void *stream) {
+static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B, const double *src, double ca,
+                                 double cb, double cd, double cL, const double *vxc, const double *vyc,
+                                 const double *evx, const double *evy, double cB, const double *c1, double c2,
+                                 const double *c3, const double *c4, const double *c5, double hx, double hy,
+                                 double hvx, double hvy, int Nx, int Ny, int Nvx, int Nvy, int x_begin, int x_end,
+                                 unsigned flags, const double *dt_dev, double cL_div, unsigned long long *nonfinite,
+                                 const double *packed_tables, double *moment_partials, int xsegments,
+                                 void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
+    if (x_begin < 0 || x_end > Nx || x_begin > x_end) return set_error(VPFV_EARG, "bad x range");
+    if (x_begin == x_end) return VPFV_OK;
+    const bool full = x_begin == 0 && x_end == Nx;
     Operands ops;
     ops.add(A, ca, src);
     ops.add(B, cb, src);
     ops.add(dest, cd, src);
     if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) || ops.n > rb::OPS_MAX) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 2D-2V path");
+        if (!full) return set_error(VPFV_EARG, "x sub-ranges need the tiled 2D-2V path");
         return vpfv_stage_2d2v_generic(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2,
                                        c3, c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev,
                                        cL_div, nonfinite, stream);
@@ -869,6 +875,8 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
     P.Ny = Ny;
     P.Nvx = Nvx;
     P.Nvy = Nvy;
+    P.i0 = x_begin;
+    P.i1 = x_end;
     P.partials = moment_partials;
     int nseg = xsegments;
     static int env_seg = -1;
@@ -880,11 +888,40 @@ extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double
     if (nseg <= 0) {  // at least ~3 waves of one CTA per SM, segments >= 8 planes
         const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
         nseg = (3 * 148 + cols - 1) / cols;
-        if (nseg > Nx / 8) nseg = Nx / 8;
+        if (nseg > (x_end - x_begin) / 8) nseg = (x_end - x_begin) / 8;
         if (nseg < 1) nseg = 1;
     }
     const double *opp[rb::OPS_MAX] = {ops.n > 0 ? ops.ptr[0] : nullptr, ops.n > 1 ? ops.ptr[1] : nullptr};
     return launch_rb(src, opp, packed_tables, P, flags, nseg, (cudaStream_t)stream);
+}
+
+extern "C" int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B,
+                                     const double *src, double ca, double cb, double cd, double cL,
+                                     const double *vxc, const double *vyc, const double *evx,
+                                     const double *evy, double cB, const double *c1, double c2,
+                                     const double *c3, const double *c4, const double *c5, double hx,
+                                     double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
+                                     int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                                     unsigned long long *nonfinite, const double *packed_tables,
+                                     double *moment_partials, int xsegments, void *stream) {
+    return stage_2d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3, c4, c5, hx,
+                                 hy, hvx, hvy, Nx, Ny, Nvx, Nvy, 0, Nx, flags, dt_dev, cL_div, nonfinite,
+                                 packed_tables, moment_partials, xsegments, stream);
+}
+
+extern "C" int vpfv_stage_2d2v_fused_range(double *dest, const double *A, const double *B,
+                                           const double *src, double ca, double cb, double cd, double cL,
+                                           const double *vxc, const double *vyc, const double *evx,
+                                           const double *evy, double cB, const double *c1, double c2,
+                                           const double *c3, const double *c4, const double *c5, double hx,
+                                           double hy, double hvx, double hvy, int Nx, int Ny, int Nvx,
+                                           int Nvy, int x_begin, int x_end, unsigned flags,
+                                           const double *dt_dev, double cL_div,
+                                           unsigned long long *nonfinite, const double *packed_tables,
+                                           double *moment_partials, void *stream) {
+    return stage_2d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3, c4, c5, hx,
+                                 hy, hvx, hvy, Nx, Ny, Nvx, Nvy, x_begin, x_end, flags, dt_dev, cL_div, nonfinite,
+                                 packed_tables, moment_partials, 0, stream);
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,

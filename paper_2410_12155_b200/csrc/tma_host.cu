@@ -1,5 +1,7 @@
 // Host side of the TMA helpers: cuTensorMapEncodeTiled through the runtime's
 // driver entry point, with a small cache keyed by (pointer, dims, box).
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -73,10 +75,19 @@ bool tma_map(const void *ptr, int rank, const unsigned long long *dims, const un
         b[i] = box[i];
     }
     for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
+    static int promo = -1;  // L2 promotion of TMA fetches (VPFV_TMA_PROMO = 0/64/128/256)
+    if (promo < 0) {
+        const char *e = getenv("VPFV_TMA_PROMO");
+        promo = e ? atoi(e) : 256;
+    }
+    const CUtensorMapL2promotion pr = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUtensorMap m;
     if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void *>(ptr), d, st, b, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
         return false;
     if (cache.size() > 512) cache.clear();
     cache.emplace(key, m);

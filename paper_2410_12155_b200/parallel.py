@@ -27,6 +27,7 @@ it with world size 2 on the CPU against the single-rank oracle.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -108,6 +109,31 @@ class SlabExchange:
                 f[:NGHOST].copy_(w[:NGHOST])
                 f[n + NGHOST:].copy_(w[n + NGHOST:])
 
+    def exchange_x_start(self, fields):
+        """Post the x-halo exchange of ``fields`` without waiting; returns a
+        handle for ``exchange_x_finish``.  With NCCL the transfers run on the
+        communicator's stream and overlap whatever the caller enqueues next on
+        its own stream (the stage's x-interior planes read neither the ghost
+        planes being received nor anything the sends still read is written).
+        The host-staged gloo path completes synchronously."""
+        if self.world == 1 or (self.host_staged and fields[0].is_cuda):
+            self.exchange_x(fields)
+            return None
+        ops = []
+        for f in fields:
+            n = f.shape[0] - 2 * NGHOST
+            ops.append(dist.P2POp(dist.isend, f[n:n + NGHOST], self._gr(self.right), self.group))
+            ops.append(dist.P2POp(dist.irecv, f[:NGHOST], self._gr(self.left), self.group))
+            ops.append(dist.P2POp(dist.isend, f[NGHOST:2 * NGHOST], self._gr(self.left), self.group))
+            ops.append(dist.P2POp(dist.irecv, f[n + NGHOST:], self._gr(self.right), self.group))
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def exchange_x_finish(handle):
+        """Make the caller's stream wait for the posted exchange."""
+        for req in handle or ():
+            req.wait()
+
     def gather_x(self, local, out):
         """All-gather slabs along dim 0: ``local`` (nloc, ...) -> ``out`` (world*nloc, ...)."""
         if self.world == 1:
@@ -156,8 +182,22 @@ class _LocalTables:
         self.x0 = x0
 
     def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
-               nonfinite=None, partials=None, packed=False):
+               nonfinite=None, partials=None, packed=False, x_range=None):
         t, g = self.t, self.lgrid
+        if x_range is not None:  # tiled 2D-2V only (see DistributedSimulation._stage)
+            h, N = g.h, g.N
+            Ny = t.grid.N[1]
+            off = self.x0 * Ny * 8
+            ptr = lambda a: a.data_ptr() + off  # noqa: E731
+            _lib.call("vpfv_stage_2d2v_fused_range", dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
+                      float(ca), float(cb), float(cd), float(cL), t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.evx),
+                      ptr(t.evy), t.cB, ptr(t.c1), t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2], h[3],
+                      N[0], N[1], N[2], N[3], int(x_range[0]), int(x_range[1]), flags,
+                      None if dt_dev is None else dt_dev.data_ptr(), float(cL_div),
+                      None if nonfinite is None else nonfinite.data_ptr(),
+                      t.packed.data_ptr() + self.x0 * Ny * 8 * 8,
+                      None if partials is None else partials.data_ptr(), stream)
+            return
         h, N = g.h, g.N
         Ny = t.grid.N[1] if t.grid.d == 2 else 1
         off = self.x0 * Ny * 8  # bytes per x row of a [Nx][Ny] fp64 table
@@ -236,6 +276,9 @@ class DistributedSimulation:
         self._events = None
         self._stage_ms = [0.0] * 4
         self._launches = 0
+        # overlapped halo exchange: tiled 2D-2V slabs wide enough for an x interior
+        self.overlap = (all(self.tiled) and all(lg.d == 2 for lg in self.lgrids) and self.nloc >= 2 * NGHOST + 1
+                        and os.environ.get("VPFV_NO_OVERLAP") is None)
         self._N_arrays = [_lib.int_array(lg.N) for lg in self.lgrids]
 
     # ------------------------------------------------------------------
@@ -273,21 +316,34 @@ class DistributedSimulation:
         return self.fields.poisson(self.fields.rho, False, stream)
 
     def _stage(self, dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=None, cL_div=1.0):
+        """One stage on the slab.  On the tiled 2D-2V path the x-halo exchange
+        overlaps the field solve and the x-interior planes [3, n-3), which read
+        no ghost plane; the two 3-plane boundary ranges run once the ghosts
+        have arrived.  Otherwise the exchange completes first."""
         stream = stream_handle(self.device)
-        self.comm.exchange_x(src)
+        overlap = self.overlap and self.world > 1
+        handle = self.comm.exchange_x_start(src) if overlap else self.comm.exchange_x(src)
         use_partials = self.fuse_moment and slot is not None and slot > 0
         emit = self.fuse_moment and slot is not None and slot < 3
         E = self._solve(src, from_partials=use_partials)
-        for s, (gt, lt) in enumerate(zip(self.gtables, self.tables)):
+        n = self.nloc
+        ranges = [(NGHOST, n - NGHOST), None, (0, NGHOST), (n - NGHOST, n)] if overlap else [None]
+        for s, gt in enumerate(self.gtables):
             gt.update(E, stream, packed=self.tiled[s])
-            nf = None if slot is None else self.nonfinite[slot, s:s + 1]
-            if self._timing and slot is not None:
-                self._events[slot][s][0].record()
-            lt.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream, dt_dev=dt_dev,
-                      cL_div=cL_div, nonfinite=nf, partials=self.partials[s] if emit else None,
-                      packed=self.tiled[s])
-            if self._timing and slot is not None:
-                self._events[slot][s][1].record()
+        timed = self._timing and slot is not None
+        for k, r in enumerate(ranges):
+            if r is None and overlap:  # the ghosts are needed from here on
+                self.comm.exchange_x_finish(handle)
+                continue
+            for s, lt in enumerate(self.tables):
+                nf = None if slot is None else self.nonfinite[slot, s:s + 1]
+                if timed and k == 0:  # (with overlap: first interior launch .. last boundary launch)
+                    self._events[slot][s][0].record()
+                lt.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream, dt_dev=dt_dev,
+                          cL_div=cL_div, nonfinite=nf, partials=self.partials[s] if emit else None,
+                          packed=self.tiled[s], x_range=r)
+                if timed and k == len(ranges) - 1:
+                    self._events[slot][s][1].record()
 
     def launch_step(self, dt):
         self.dt_dev.fill_(float(dt))

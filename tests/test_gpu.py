@@ -523,3 +523,39 @@ def test_fused_moment_cache_honours_inplace_edits():
         sim.advance(dt)
         ref.advance(dt)
         assert rel_l2(sim.interiors()[0], ref.interiors()[0]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [(16, 8, 16, 32), (12, 16, 32, 16), (16, 8, 64, 80)])
+def test_tiled_stage_x_ranges_equal_full_launch(N):
+    """vpfv_stage_2d2v_fused_range over [3, n-3), [0, 3), [n-3, n) (the
+    overlapped-exchange order) is bitwise the full launch, partials included."""
+    g, sp, src, E, rng = _tiled_case(N, 11)
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({k: dev(v) for k, v in E.items()}, stream, packed=True)
+    flags = K.wrap_flags(pg)
+    assert tab.fused_moment_ok(flags)
+    A, d_src = dev(rng.random(g.padded_shape)), dev(src)
+    d0 = dev(rng.random(g.padded_shape))
+    full, part_full = d0.clone(), torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda")
+    tab.launch(full, A, d_src, d_src, -0.125, 0.375, 0.75, 0.004, flags, stream, partials=part_full, packed=True)
+    rng_out, part_rng = d0.clone(), torch.empty_like(part_full)
+    h, n = pg.h, N[0]
+    for x0, x1 in ((3, n - 3), (0, 3), (n - 3, n)):
+        _lib.call("vpfv_stage_2d2v_fused_range", rng_out.data_ptr(), A.data_ptr(), d_src.data_ptr(),
+                  d_src.data_ptr(), -0.125, 0.375, 0.75, 0.004, tab.vxc.data_ptr(), tab.vyc.data_ptr(),
+                  tab.evx.data_ptr(), tab.evy.data_ptr(), tab.cB, tab.c1.data_ptr(), tab.c2, tab.c3.data_ptr(),
+                  tab.c4.data_ptr(), tab.c5.data_ptr(), h[0], h[1], h[2], h[3], *N, x0, x1, flags, None, 1.0,
+                  None, tab.packed.data_ptr(), part_rng.data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert torch.equal(rng_out, full)
+    assert torch.equal(part_rng, part_full)
+    with pytest.raises(ValueError):  # sub-ranges exist only on the tiled path
+        _lib.call("vpfv_stage_2d2v_fused_range", rng_out.data_ptr(), A.data_ptr(), d_src.data_ptr(),
+                  d_src.data_ptr(), 1.0, 0.0, 0.0, 0.004, tab.vxc.data_ptr(), tab.vyc.data_ptr(),
+                  tab.evx.data_ptr(), tab.evy.data_ptr(), tab.cB, tab.c1.data_ptr(), tab.c2, tab.c3.data_ptr(),
+                  tab.c4.data_ptr(), tab.c5.data_ptr(), h[0], h[1], h[2], h[3], *N, 0, 3, flags, None, 1.0,
+                  None, None, None, stream)
