@@ -111,6 +111,7 @@ class Simulation:
         self.partials = mk()       # written by stages 1-3, read by stages 2-4
         self.partials_next = mk()  # written by stage 4 (moment of the new f0), read by the next stage 1
         self._moment_of = None  # (data_ptr, _version) of the f0 arrays the partials describe
+        self._side = [torch.cuda.Stream(self.device) for _ in self.species[1:]]  # concurrent species
         self._last_E = None
         self._timing = False
         self._events = None
@@ -139,18 +140,31 @@ class Simulation:
         else:
             E = self.fields.solve(src, stream=stream)
         self._last_E = E
+        main = torch.cuda.current_stream(self.device)
+        forked = []
         for s, tab in enumerate(self.tables):
-            tab.update(E, stream, packed=self.tiled[s])
-            nf = None if slot is None else self.nonfinite[slot, s:s + 1]
-            timed = self._timing and slot is not None
-            if timed:
-                self._events[slot][s][0].record()
-            tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
-                       dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
-                       partials=(self.partials if slot < 3 else self.partials_next)[s] if emit_partials else None,
-                       packed=self.tiled[s])
-            if timed:
-                self._events[slot][s][1].record()
+            # species > 0 run on side streams forked from this one, so their
+            # stage kernels overlap (and fill each other's wave tails); the
+            # fork/join is captured into the step graph as parallel branches
+            side = self._side[s - 1] if (s > 0 and self._side) else None
+            if side is not None:
+                side.wait_stream(main)
+                forked.append(side)
+            with torch.cuda.stream(side if side is not None else main):
+                st = stream_handle(self.device)
+                tab.update(E, st, packed=self.tiled[s])
+                nf = None if slot is None else self.nonfinite[slot, s:s + 1]
+                timed = self._timing and slot is not None
+                if timed:
+                    self._events[slot][s][0].record()
+                tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], st,
+                           dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
+                           partials=(self.partials if slot < 3 else self.partials_next)[s] if emit_partials else None,
+                           packed=self.tiled[s])
+                if timed:
+                    self._events[slot][s][1].record()
+        for side in forked:
+            main.wait_stream(side)
 
     def _step_body(self, f0, f1, fout, cached=False, emit_last=True):
         bufs = {"f0": f0, "f1": f1, "fout": fout}
