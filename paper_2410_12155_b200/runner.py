@@ -305,3 +305,71 @@ class Simulation:
                 if on_row:
                     on_row(row)
         return rows
+
+
+class HostPipeline:
+    """Advance host-resident states through the device, one RK4 step each,
+    with the copies overlapped: while state k steps on the compute stream,
+    state k+1 is uploaded on one copy stream and the result of step k-1 is
+    downloaded on another (double-buffered device input and output).
+
+    This is the host-buffer entry of the library: the reference's stage and
+    step functions take host (numpy) arrays, so every call moves the state
+    both ways; a pipeline of such calls is bound by the two copy directions,
+    not by the step.  Host states are interior arrays (``grid.N``): the ghost
+    cells of the padded device buffers are frozen velocity slabs (written
+    once, never by the kernels) or periodic images read by modular index, so
+    only interiors cross PCIe.  There is no divergence rollback here -- the
+    per-stage non-finite flags of the last step remain in ``sim.nonfinite``.
+    """
+
+    def __init__(self, sim: Simulation):
+        self.sim = sim
+        dev = sim.device
+        self.din = [[a.clone() for a in sim.ctx.f0] for _ in range(2)]   # ghosts included:
+        self.dout = [[a.clone() for a in sim.ctx.f0] for _ in range(2)]  # kernels write interiors only
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
+        self.in_ready, self.step_done, self.out_done = mk(), mk(), mk()
+
+        self._inner = [g.interior_slices() for g in sim.grids]
+
+    def bytes_per_step(self):
+        return sum(math.prod(g.N) * 8 for g in self.sim.grids)
+
+    def host_state(self):
+        """Pinned host interiors of the simulation's current f0 (a valid input)."""
+        return [a[sl].cpu().contiguous().pin_memory() for a, sl in zip(self.sim.ctx.f0, self._inner)]
+
+    def run(self, host_in, host_out, dt, steps):
+        """Step ``host_in(k)`` (a list of pinned per-species arrays) into
+        ``host_out(k)`` for k < steps; returns after the last download."""
+        sim, main = self.sim, torch.cuda.current_stream(self.sim.device)
+        with torch.cuda.stream(self.h2d):
+            for d, sl, h in zip(self.din[0], self._inner, host_in(0)):
+                d[sl].copy_(h, non_blocking=True)
+            self.in_ready[0].record()
+        for k in range(steps):
+            b = k & 1
+            if k + 1 < steps:  # prefetch the next state once step k-1 no longer reads its buffer
+                if k >= 1:
+                    self.h2d.wait_event(self.step_done[1 - b])
+                with torch.cuda.stream(self.h2d):
+                    for d, sl, h in zip(self.din[1 - b], self._inner, host_in(k + 1)):
+                        d[sl].copy_(h, non_blocking=True)
+                    self.in_ready[1 - b].record()
+            main.wait_event(self.in_ready[b])
+            if k >= 2:
+                main.wait_event(self.out_done[b])  # dout[b] drained by the download of step k-2
+            sim.ctx.f0, sim.ctx.fout = self.din[b], self.dout[b]
+            sim.launch_step(dt)
+            self.step_done[b].record(main)
+            self.d2h.wait_event(self.step_done[b])
+            with torch.cuda.stream(self.d2h):
+                for h, d, sl in zip(host_out(k), self.dout[b], self._inner):
+                    h.copy_(d[sl], non_blocking=True)
+                self.out_done[b].record()
+        self.d2h.synchronize()
+        self.h2d.synchronize()
+        main.synchronize()

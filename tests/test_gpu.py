@@ -559,3 +559,24 @@ def test_tiled_stage_x_ranges_equal_full_launch(N):
                   tab.evx.data_ptr(), tab.evy.data_ptr(), tab.cB, tab.c1.data_ptr(), tab.c2, tab.c3.data_ptr(),
                   tab.c4.data_ptr(), tab.c5.data_ptr(), h[0], h[1], h[2], h[3], *N, 0, 3, flags, None, 1.0,
                   None, None, None, stream)
+
+
+@pytest.mark.gpu
+def test_host_pipeline_equals_advance():
+    """runner.HostPipeline (overlapped H2D / step / D2H of host states) gives
+    bitwise the state Simulation.advance gives for each input."""
+    setup = P.make_problem(P.landau_spec(), 32, 32)
+    sim = R.Simulation(setup)
+    dt = 0.9 * sim.max_dt()
+    sim.fixed_dt = dt
+    pipe = R.HostPipeline(sim)
+    base = pipe.host_state()[0]
+    inputs = [[(base * (1.0 + 0.01 * k)).pin_memory()] for k in range(4)]
+    outs = [[torch.empty_like(base).pin_memory()] for _ in range(4)]
+    pipe.run(lambda k: inputs[k], lambda k: outs[k], dt, 4)
+    inner = (slice(3, -3),) * 4
+    for k in range(4):
+        ref = R.Simulation(setup, dt=dt)
+        ref.ctx.f0[0][inner].copy_(inputs[k][0])
+        ref.advance(dt)
+        assert torch.equal(ref.ctx.f0[0][inner].cpu(), outs[k][0]), k
