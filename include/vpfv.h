@@ -203,7 +203,7 @@ int vpfv_tables_1d_packed(const double *Ex, double *packed, int Nx, double qmk2,
                           double t1, double den1, void *stream);
 
 /* The same 2D tables packed for the tiled kernel: packed[(Nx+2)][Ny][8] =
- * (evx, evy, c1, c3, c4, c5, 0, 0) with x rows shifted by one and periodic
+ * (evx, evy, c3, c4, c1, c5, 0, 0) with x rows shifted by one and periodic
  * ghost rows 0 (= x Nx-1) and Nx+1 (= x 0). */
 int vpfv_tables_2d_packed(const double *Ex, const double *Ey, double *packed, int Nx, int Ny,
                           double qmk2, double nqmk2, double gx, double gy,
