@@ -103,10 +103,11 @@ int vpfv_stage_2d2v_fused(double *dest, const double *A, const double *B, const 
                           double *moment_partials, int xsegments, void *stream);
 
 /* 1D-2V with the tiled x-marching kernel and optional fused moment partials
- * [Nx][Nvx][Nvy/32] (finish with vpfv_moment_partials(nphys = Nx)); tiled
+ * [Nx][Nvx][Nvy/16] (finish with vpfv_moment_partials(nphys = Nx)); tiled
  * when packed_tables (vpfv_tables_1d_packed) is given, the fast path is
- * requested, velocity ghosts are stored and Nvx % 32 == Nvy % 32 == 0;
- * otherwise the generic kernel (and moment_partials must be NULL). */
+ * requested, velocity ghosts are stored, Nvx % 32 == Nvy % 16 == 0 and at
+ * most two RK operands differ from src; otherwise the generic kernel (and
+ * moment_partials must be NULL). */
 int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const double *src,
                           double ca, double cb, double cd, double cL,
                           const double *vxc, const double *vyc, const double *evx,
@@ -116,6 +117,10 @@ int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const 
                           unsigned long long *nonfinite, const double *packed_tables,
                           double *moment_partials, int xsegments, void *stream);
 int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags);
+
+/* Width of the vy chunks of the 1D-2V moment partials (16): partials hold
+ * [Nx][Nvx][Nvy/chunk] fold-tree subtree sums. */
+int vpfv_stage_1d2v_partials_chunk(void);
 
 /* vpfv_stage_2d2v_fused restricted to the interior x cells [x_begin, x_end)
  * (tiled path only; VPFV_EARG otherwise).  Planes x_begin-3 .. x_end+2 are

@@ -54,6 +54,7 @@ SIGNATURES = {
     "vpfv_stage_1d2v_tiled_ok": (_i, [_i, _i, _i, _u]),
     "vpfv_tables_1d_packed": (_i, [_p, _p, _i, _d, _d, _d, _d, _p]),
     "vpfv_stage_2d2v_partials_chunk": (_i, []),
+    "vpfv_stage_1d2v_partials_chunk": (_i, []),
     "vpfv_moment": (_i, [_p, _p, _i, _i, _p, _d, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
     "vpfv_poisson_1d": (_i, [_p, _p, _p, _i, _p, _p, _p, _p]),

@@ -1,16 +1,32 @@
-// 1D-2V fused stage, x-marching with TMA-staged (vx, vy) halo tiles (fast path).
+// 1D-2V fused stage: x-marching, TMA-staged (vx, vy) halo tiles, 4-cell
+// register blocks (sm_100a, fast arithmetic path).
 //
 // Operator of stage_1d2v (/root/reference/pkg/src/vpfv/_kernels.py:153-197):
 //   rhs = -a_x D_x f - a_vx D_vx f - a_vy D_vy f + c1 diag(x,vx) - c2 diag(vx,vy)
-// with a_x = vxc[j], a_vx = evx[i] + cB vyc[k], a_vy = avy[j].  Same
-// organisation as the 2D-2V kernel (stage2d2v_tma.cu): a CTA owns a (vx, vy)
-// = (BK, BL) column block and marches x; per plane one TMA box brings the
-// (BK+6) x (BL+8) halo tile, up to three RK-operand core boxes and the packed
-// (evx, c1) table rows of planes p-1..p+1; each thread keeps 7 register
-// accumulators per cell (plane loop unrolled x7) and CK consecutive vx cells
-// share one vx column of registers; the x-coupled (x,vx) correction uses
-// D(p) = s[k-1] - s[k+1]; the optional epilogue emits fold-tree moment
-// partials per 32-wide vy chunk.
+//   dest = ca A + cb B + cd dest + cL rhs                 (interior cells only)
+// with a_x = vxc[j], a_vx = evx[i] + cB vyc[k], a_vy = avy[j].
+//
+// The 2D-2V kernel's design (stage2d2v_tma.cu) with no y direction:
+//  * a CTA (128 threads, 3 per SM) owns a (vx, vy) = (32, 16) column block
+//    and marches x; each thread keeps, per cell, a sliding window of 6 fp64
+//    accumulators (cells p-3..p+2) and scatters s(p) into it -- the x
+//    direction costs no shared-memory traffic;
+//  * per plane one (38, 24) halo tile, the packed (evx, c1) rows of planes
+//    p-1..p+1 and the RK operand tiles of cell plane p-3 arrive by TMA, 4
+//    stages deep on mbarrier transaction counts (a 1D-2V plane is too short
+//    a step to hide an operand load issued one plane ahead);
+//  * a thread owns 4 consecutive vx cells at one vy lane: 38 shared loads per
+//    plane, 9.5 per cell; diag(vx,vy) = G(vx+1) - G(vx-1) with
+//    G = s[vy-1] - s[vy+1], and the x-coupled correction uses
+//    D = s[vx-1] - s[vx+1];
+//  * RK operands aliasing src are folded into the accumulator (cfold/cL s);
+//  * epilogue: coalesced stores, a per-thread non-finite sum, and optionally
+//    the fold-tree moment partials over aligned 16-wide vy chunks.
+#include <cuda.h>
+
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -18,235 +34,370 @@ namespace vpfv {
 
 struct Stage12 {
     double *dest;
+    const double *src;
     double cL;
     const double *dt_dev;
     double cL_div;
     int nops;
-    double opc[3];
+    double opc[2];
+    int fold;
+    double cfold;
     unsigned long long *nonfinite;
     const double *vxc, *vyc, *avy;
-    double cB, c2, mhx, mhvx, mhvy;
+    double c2, mhx, mhvx, mhvy;
     int Nx, Nvx, Nvy;
     int wrap_x;
     int i0, i1, nseg, seglen;
-    double *partials;  // [Nx][Nvx][Nvy/BL] or nullptr
+    double *partials;  // [Nx][Nvx][Nvy/16] or nullptr
 };
+
+namespace r12 {
+constexpr int BL = 16, BB = 4, NS = 4, OPS_MAX = 2;
+template <int BK_, int MINB_>
+struct Geo {
+    static constexpr int BK = BK_, MINB = MINB_;
+    static constexpr int THREADS = (BK / BB) * BL;
+    static constexpr int TK = BK + 6, TW = BL + 8;  // halo tile (vy box starts 16 B aligned)
+    static constexpr int HALO = TK * TW;
+    static constexpr int TAB = 32;                  // 3 table rows of 8, padded to 256 B
+    static constexpr int OPW = BL + 2, OPE = BK * OPW;
+    // a stage: plane p's halo tile, its table rows, and the RK operand tiles
+    // of the cell plane p-3 that the iteration of plane p finalises
+    static constexpr int STAGE = HALO + TAB + OPS_MAX * OPE;
+    static constexpr int BAR_OFF = NS * STAGE * 8;
+    static constexpr int SMEM = BAR_OFF + 64;
+    static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
+                  "TMA destinations must stay 128 B aligned");
+};
+}  // namespace r12
 
 struct Maps12 {
-    CUtensorMap halo, op[3], tab;
+    CUtensorMap halo, op[r12::OPS_MAX], tab;
 };
 
-template <int BK, int BL, int NSTAGE>
-struct Tile12 {
-    static constexpr int K = BK + 6, L = BL + 8;
-    static constexpr int ELEMS = K * L;
-    static constexpr int OL = BL + 2;
-    static constexpr int OELEMS = BK * OL;
-    static constexpr int TELEMS = 32;  // 3 table rows of 8, padded to 256 B
-    static constexpr int STAGE_ELEMS = ELEMS + 3 * OELEMS + TELEMS;
-    static constexpr int SMEM = NSTAGE * STAGE_ELEMS * 8 + 64;
-    static_assert((ELEMS * 8) % 128 == 0 && (OELEMS * 8) % 128 == 0, "TMA destinations must stay 128 B aligned");
-};
+__device__ __forceinline__ double w12pos(double m3, double m2, double m1, double z, double p1, double p2) {
+    return fma(-3.0, p2, fma(30.0, p1, fma(20.0, z, fma(-60.0, m1, fma(15.0, m2, -2.0 * m3)))));
+}
+__device__ __forceinline__ double w12neg(double m2, double m1, double z, double p1, double p2, double p3) {
+    return fma(2.0, p3, fma(-15.0, p2, fma(60.0, p1, fma(-20.0, z, fma(-30.0, m1, 3.0 * m2)))));
+}
 
-// Copies of plane n split into parts issued by different warps (see
-// issue_part in stage2d2v_tma.cu): 0 = expect_tx + tables, 1 = halo, 2+o =
-// RK operand o.
-template <class TL>
-__device__ __forceinline__ void issue12(int w, double *stages, uint64_t *bars, const Maps12 *M, int n,
-                                        int p_first, int i0, int i1, const Stage12 &P, int l0, int k0,
-                                        int nstage) {
-    const int s = n % nstage;
-    double *dst = stages + s * TL::STAGE_ELEMS;
-    const int p = p_first + n;  // in [-3, Nx + 3)
-    int px = p;
-    if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
-    const int q = p - 3;
-    const bool ops = (q >= i0 && q < i1);
-    if (w == 0) {
-        tma::mbar_expect_tx(&bars[s], (TL::ELEMS + 24 + (ops ? P.nops * TL::OELEMS : 0)) * 8);
-        tma::load2d(dst + TL::ELEMS + 3 * TL::OELEMS, &M->tab, &bars[s], 0, px);
-    } else if (w == 1) {
-        tma::load3d(dst, &M->halo, &bars[s], l0, k0, px + NG);
-    } else if (ops && w - 2 < P.nops) {
-        const int o = w - 2;
-        tma::load3d(dst + TL::ELEMS + o * TL::OELEMS, &M->op[o], &bars[s], l0 + 2, k0 + NG, q + NG);
+// x scatter of s(p) into a cell's window (w[j] = cell p-3+j before plane p),
+// extraction of cell p-3, slide (see scatter_cell in stage2d2v_tma.cu)
+template <int SIGN>
+__device__ __forceinline__ void scatter12(double (&w)[6], double ti, double &fin) {
+    if (SIGN > 0) {
+        w[5] = fma(15.0, ti, w[5]);
+        w[4] = fma(-60.0, ti, w[4]);
+        w[3] = fma(20.0, ti, w[3]);
+        w[2] = fma(30.0, ti, w[2]);
+        w[1] = fma(-3.0, ti, w[1]);
+        fin = w[0];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) w[j] = w[j + 1];
+        w[5] = -2.0 * ti;
+    } else {
+        const double c2 = 3.0 * ti;
+        w[4] = fma(-30.0, ti, w[4]);
+        w[3] = fma(-20.0, ti, w[3]);
+        w[2] = fma(60.0, ti, w[2]);
+        w[1] = fma(-15.0, ti, w[1]);
+        fin = fma(2.0, ti, w[0]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = w[j + 1];
+        w[4] = c2;
+        w[5] = 0.0;
     }
 }
 
-template <int BK, int BL, int NSTAGE, int CK>
-__global__ void __launch_bounds__((BK / CK) * BL, 1)
-    stage1d2v_tma_kernel(const __grid_constant__ Maps12 maps, const Stage12 P) {
-    using TL = Tile12<BK, BL, NSTAGE>;
-    constexpr int L = TL::L;
+template <class GEO>
+__global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
+    stage1d2v_rb_kernel(const __grid_constant__ Maps12 maps, const Stage12 P) {
+    using namespace r12;
+    constexpr int BK = GEO::BK, TW = GEO::TW, HALO = GEO::HALO, TAB = GEO::TAB, STAGE = GEO::STAGE, OPW = GEO::OPW,
+                  OPE = GEO::OPE, BAR_OFF = GEO::BAR_OFF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + NSTAGE * TL::STAGE_ELEMS * 8);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + BAR_OFF);  // NS stage barriers
+    const unsigned sbase = tma::smem_addr(smem_raw);
 
     const int tid = threadIdx.x;
     const int nlt = P.Nvy / BL, nkt = P.Nvx / BK;
     const int ncols = nlt * nkt;
-    const int b = blockIdx.x % ncols, seg = blockIdx.x / ncols;
-    const int lt = b % nlt, kt = b / nlt;
+    const int blk = blockIdx.x % ncols, seg = blockIdx.x / ncols;
+    const int lt = blk % nlt, kt = blk / nlt;
     const int k0 = kt * BK, l0 = lt * BL;
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) return;
 
-    const int lane = tid % BL, colid = tid / BL;
-    const int kb = colid * CK;
-    const int kfirst = k0 + kb;
-    const int ll = l0 + lane;
+    // thread -> cells (vx0 + b, vy), b < 4; half-warps are 16-lane vy rows
+    const int lane = tid & 31, warp = tid >> 5;
+    const int tl = lane & 15;
+    const int tk = (warp << 1) | (lane >> 4);
+    const int vx0 = k0 + BB * tk, vy = l0 + tl;
 
     if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) tma::mbar_init(&bars[s], 1);
+        for (int s = 0; s < NS; ++s) tma::mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int p_first = i0 - 3, nplanes = i1 - i0 + 6;
     const Maps12 *M = &maps;
-    if (tid == 0)
-        for (int n = 0; n < NSTAGE - 1 && n < nplanes; ++n)
-            for (int w = 0; w < 5; ++w) issue12<TL>(w, stages, bars, M, n, p_first, i0, i1, P, l0, k0, NSTAGE);
-    const int warp = tid >> 5;
-    const bool issuer = (tid & 31) == 0 && warp < 2 + P.nops;
-
-    double ax_s[CK], avy_s[CK];
-    bool xpos[CK], vypos[CK];
-#pragma unroll
-    for (int i = 0; i < CK; ++i) {
-        const double v = __ldg(P.vxc + kfirst + i);
-        ax_s[i] = v * P.mhx;
-        xpos[i] = v > 0.0;
-        const double ay = __ldg(P.avy + kfirst + i);
-        avy_s[i] = ay * P.mhvy;
-        vypos[i] = ay > 0.0;
-    }
-    const double cBvy = __ldg(P.vyc + P.Nvy) * __ldg(P.vyc + ll);  // cB rides in vyc[Nvy] (_kernels.py:166)
-    const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
-    const double mc2 = -P.c2, mhvx = P.mhvx;
     const int nops = P.nops;
-    const double oc0 = P.opc[0], oc1 = P.opc[1], oc2 = P.opc[2];
-    const int off = (kb + 3) * L + lane + 3;
-    const int ooff = TL::ELEMS + kb * TL::OL + lane + 1;
+    auto issue_plane = [&](int n) {  // plane n (+ operands of cell plane n-3) into stage n % NS
+        const int s = n % NS;
+        const unsigned dst = sbase + s * STAGE * 8, bar = sbase + BAR_OFF + s * 8;
+        int px = p_first + n;
+        if (P.wrap_x) px = px < 0 ? px + P.Nx : (px >= P.Nx ? px - P.Nx : px);
+        const int q = p_first + n - 3;
+        const int nop = (q >= i0 && q < i1) ? nops : 0;
+        tma::mbar_expect_tx_s(bar, (HALO + 24 + nop * OPE) * 8);
+        tma::load3d_s(dst, &M->halo, bar, l0, k0, px + NG);
+        tma::load2d_s(dst + HALO * 8, &M->tab, bar, 0, px);
+        for (int o = 0; o < nop; ++o)
+            tma::load3d_s(dst + (HALO + TAB + o * OPE) * 8, &M->op[o], bar, l0 + 2, k0 + NG, q + NG);
+    };
+    if (tid == 0)
+        for (int n = 0; n < NS - 1 && n < nplanes; ++n) issue_plane(n);
+
+    double ax_s[BB], avy_s[BB];
+    bool xpos[BB], ypos[BB];
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+        const double v = __ldg(P.vxc + vx0 + b);
+        ax_s[b] = v * P.mhx;
+        xpos[b] = v > 0.0;
+        const double ay = __ldg(P.avy + vx0 + b);
+        avy_s[b] = ay * P.mhvy;
+        ypos[b] = ay > 0.0;
+    }
+    const bool ypos_all = ypos[0] && ypos[1] && ypos[2] && ypos[3];
+    const bool yneg_all = !ypos[0] && !ypos[1] && !ypos[2] && !ypos[3];
+    const double cBvy = __ldg(P.vyc + P.Nvy) * __ldg(P.vyc + vy);  // cB rides in vyc[Nvy] (_kernels.py:166)
+    const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
+    const bool fold = P.fold && cL != 0.0;
+    const double kfold = fold ? P.cfold / cL : 0.0;
+    const bool fold_fb = P.fold && !fold;
+    const double mc2 = -P.c2, mhvx = P.mhvx;
+    const double oc0 = P.opc[0], oc1 = P.opc[1];
+    const int off = (BB * tk + 3) * TW + tl + 3;
+    const int ooff = BB * tk * OPW + tl + 1;
     const long long P2 = P.Nvy + 2 * NG, P1 = (long long)(P.Nvx + 2 * NG) * P2;
-    long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(kfirst + NG) * P2 + (ll + NG);
+    long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(vx0 + NG) * P2 + (vy + NG);
 
-    double acc[CK][7];
+    double acc[BB][6];
 #pragma unroll
-    for (int i = 0; i < CK; ++i)
+    for (int i = 0; i < BB; ++i)
 #pragma unroll
-        for (int m = 0; m < 7; ++m) acc[i][m] = 0.0;
-    int stage_s = 0;
-    unsigned stage_par = 0;
+        for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
-    for (int blk = 0; blk < nplanes; blk += 7) {
+    for (int n = 0; n < nplanes; ++n) {
+        const int p = p_first + n, q = p - 3;
+        const bool inner = p >= i0 && p < i1;
+        const bool fin_q = q >= i0 && q < i1;
+        if (tid == 0 && n + NS - 1 < nplanes) issue_plane(n + NS - 1);
+        const int nq = n / NS, stage_s = n - nq * NS;
+        tma::mbar_wait_s(sbase + BAR_OFF + stage_s * 8, nq & 1);
+        const double *stage = stages + stage_s * STAGE;
+        const double *c = stage + off;
+        const double *tb = stage + HALO;  // table rows p-1, p, p+1: (evx, c1)
+        const double evx = tb[8], c1m = tb[1], c1p = tb[17];
+
+        double v[BB][7];
 #pragma unroll
-        for (int r = 0; r < 7; ++r) {
-            const int n = blk + r;
-            if (n >= nplanes) break;
-            const int p = p_first + n;
-            if (issuer && n + NSTAGE - 1 < nplanes)
-                issue12<TL>(warp, stages, bars, M, n + NSTAGE - 1, p_first, i0, i1, P, l0, k0, NSTAGE);
-            const int s = stage_s;
-            tma::mbar_wait(&bars[s], stage_par);
-            if (++stage_s == NSTAGE) {
-                stage_s = 0;
-                stage_par ^= 1u;
-            }
-            const double *stage = stages + s * TL::STAGE_ELEMS;
-            const double *c0 = stage + off;
-            const double *tb = stage + TL::ELEMS + 3 * TL::OELEMS;  // rows p-1, p, p+1: (evx, c1)
-            const double evx = tb[8], c1m = tb[1], c1p = tb[17];
-            const double avx = evx + cBvy;
-            const double avx_s = avx * mhvx;
-            const bool vxpos = avx > 0.0;
-            double col[CK + 6];
+        for (int b = 0; b < BB; ++b)
 #pragma unroll
-            for (int m = 0; m < CK + 6; ++m) col[m] = c0[(m - 3) * L];
+            for (int d = 0; d < 7; ++d) v[b][d] = c[b * TW + d - 3];
+        double r0[BB + 6];  // vy-offset-0 values at vx offsets -3 .. BB+2
+        r0[0] = c[-3 * TW];
+        r0[1] = c[-2 * TW];
+        r0[2] = c[-TW];
+        r0[BB + 3] = c[BB * TW];
+        r0[BB + 4] = c[(BB + 1) * TW];
+        r0[BB + 5] = c[(BB + 2) * TW];
+        double s0[BB], G[BB];
 #pragma unroll
-            for (int i = 0; i < CK; ++i) {
-                const double *c = c0 + i * L;
-                const double t = ax_s[i] * col[i + 3];
-                if (xpos[i]) {
-                    acc[i][(r + 10) % 7] = fma(-2.0, t, acc[i][(r + 10) % 7]);
-                    acc[i][(r + 9) % 7] = fma(15.0, t, acc[i][(r + 9) % 7]);
-                    acc[i][(r + 8) % 7] = fma(-60.0, t, acc[i][(r + 8) % 7]);
-                    acc[i][r] = fma(20.0, t, acc[i][r]);
-                    acc[i][(r + 6) % 7] = fma(30.0, t, acc[i][(r + 6) % 7]);
-                    acc[i][(r + 5) % 7] = fma(-3.0, t, acc[i][(r + 5) % 7]);
-                } else {
-                    acc[i][(r + 9) % 7] = fma(3.0, t, acc[i][(r + 9) % 7]);
-                    acc[i][(r + 8) % 7] = fma(-30.0, t, acc[i][(r + 8) % 7]);
-                    acc[i][r] = fma(-20.0, t, acc[i][r]);
-                    acc[i][(r + 6) % 7] = fma(60.0, t, acc[i][(r + 6) % 7]);
-                    acc[i][(r + 5) % 7] = fma(-15.0, t, acc[i][(r + 5) % 7]);
-                    acc[i][(r + 4) % 7] = fma(2.0, t, acc[i][(r + 4) % 7]);
-                }
-                const double D = col[i + 2] - col[i + 4];
-                acc[i][(r + 6) % 7] = fma(c1m, D, acc[i][(r + 6) % 7]);
-                acc[i][(r + 1) % 7] = fma(-c1p, D, acc[i][(r + 1) % 7]);
-                double wvx, wvy;
-                if (vxpos)
-                    wvx = (fma(15.0, col[i + 1], -2.0 * col[i]) + fma(20.0, col[i + 3], -60.0 * col[i + 2])) +
-                          fma(-3.0, col[i + 5], 30.0 * col[i + 4]);
-                else
-                    wvx = (fma(-30.0, col[i + 2], 3.0 * col[i + 1]) + fma(60.0, col[i + 4], -20.0 * col[i + 3])) +
-                          fma(2.0, col[i + 6], -15.0 * col[i + 5]);
-                if (vypos[i])
-                    wvy = (fma(15.0, c[-2], -2.0 * c[-3]) + fma(20.0, c[0], -60.0 * c[-1])) + fma(-3.0, c[2], 30.0 * c[1]);
-                else
-                    wvy = (fma(-30.0, c[-1], 3.0 * c[-2]) + fma(60.0, c[1], -20.0 * c[0])) + fma(2.0, c[3], -15.0 * c[2]);
-                const double dvv = (c[L - 1] + c[-L + 1]) - (c[L + 1] + c[-L - 1]);
-                acc[i][r] = fma(avx_s, wvx, fma(avy_s[i], wvy, fma(mc2, dvv, acc[i][r])));
-            }
-            const int q = p - 3;
-            if (q >= i0 && q < i1) {
-                const double *op = stage + ooff;
-                double out[CK];
-#pragma unroll
-                for (int i = 0; i < CK; ++i) {
-                    double rk = oc0 * op[i * TL::OL];
-                    if (nops > 1) rk = fma(oc1, op[TL::OELEMS + i * TL::OL], rk);
-                    if (nops > 2) rk = fma(oc2, op[2 * TL::OELEMS + i * TL::OL], rk);
-                    out[i] = fma(cL, acc[i][(r + 4) % 7], rk);
-                    P.dest[gq + i * P2] = out[i];
-                }
-                if (P.nonfinite) {
-#pragma unroll
-                    for (int i = 0; i < CK; ++i)
-                        if (!isfinite(out[i]))
-                            atomicMin(P.nonfinite, ((unsigned long long)q * P.Nvx + kfirst + i) * P.Nvy + ll);
-                }
-                if (P.partials) {
-                    const long long pb = (long long)q * P.Nvx + kfirst;
-                    const bool odd = lane & 1;
-#pragma unroll
-                    for (int i = 0; i < CK; i += 2) {
-                        const double keep = odd ? out[i + 1] : out[i];
-                        const double send = odd ? out[i] : out[i + 1];
-                        double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1, BL));
-#pragma unroll
-                        for (int o = 2; o < BL; o <<= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o, BL));
-                        if (lane < 2) P.partials[(pb + i + lane) * nlt + lt] = v;
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < CK; ++i) acc[i][(r + 4) % 7] = 0.0;
-            gq += P1;
-            __syncthreads();
+        for (int b = 0; b < BB; ++b) {
+            r0[b + 3] = v[b][3];
+            s0[b] = v[b][3];
+            G[b] = v[b][2] - v[b][4];
         }
+        // x-coupled correction c1 diag(x,vx): D(p) = s[vx-1] - s[vx+1] feeds cells p-1 and p+1
+#pragma unroll
+        for (int b = 0; b < BB; ++b) {
+            const double D = r0[b + 2] - r0[b + 4];
+            acc[b][2] = fma(c1m, D, acc[b][2]);
+            acc[b][4] = fma(-c1p, D, acc[b][4]);
+        }
+        if (inner) {
+            const double avx = evx + cBvy;  // independent of vx
+            const double avx_s = avx * mhvx;
+            if (avx > 0.0) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    acc[b][3] = fma(avx_s, w12pos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]), acc[b][3]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    acc[b][3] = fma(avx_s, w12neg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]),
+                                    acc[b][3]);
+            }
+            if (ypos_all) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    acc[b][3] = fma(avy_s[b], w12pos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]), acc[b][3]);
+            } else if (yneg_all) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    acc[b][3] = fma(avy_s[b], w12neg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]), acc[b][3]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) {
+                    const double w = ypos[b] ? w12pos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
+                                             : w12neg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
+                    acc[b][3] = fma(avy_s[b], w, acc[b][3]);
+                }
+            }
+            // -c2 diag(vx,vy) = -c2 (G(vx+1) - G(vx-1)); fold of the src operand
+            const double gm = c[-TW - 1] - c[-TW + 1], gp = c[BB * TW - 1] - c[BB * TW + 1];
+            double gr[BB + 2];
+            gr[0] = gm;
+            gr[BB + 1] = gp;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) gr[b + 1] = G[b];
+#pragma unroll
+            for (int b = 0; b < BB; ++b) acc[b][3] = fma(kfold, s0[b], fma(mc2, gr[b + 2] - gr[b], acc[b][3]));
+        }
+
+        // x stencil scatter, extract cell q, slide
+        double fin[BB];
+        if (xpos[0] && xpos[BB - 1]) {
+#pragma unroll
+            for (int b = 0; b < BB; ++b) scatter12<1>(acc[b], ax_s[b] * s0[b], fin[b]);
+        } else if (!xpos[0] && !xpos[BB - 1]) {
+#pragma unroll
+            for (int b = 0; b < BB; ++b) scatter12<-1>(acc[b], ax_s[b] * s0[b], fin[b]);
+        } else {
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                if (xpos[b])
+                    scatter12<1>(acc[b], ax_s[b] * s0[b], fin[b]);
+                else
+                    scatter12<-1>(acc[b], ax_s[b] * s0[b], fin[b]);
+            }
+        }
+
+        if (fin_q) {
+            const double *op = stage + HALO + TAB + ooff;
+            double out[BB];
+            if (nops == 0) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) out[b] = cL * fin[b];
+            } else if (nops == 1) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) out[b] = fma(cL, fin[b], oc0 * op[b * OPW]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) out[b] = fma(cL, fin[b], fma(oc1, op[OPE + b * OPW], oc0 * op[b * OPW]));
+            }
+            if (fold_fb) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) out[b] = fma(P.cfold, P.src[gq + b * P2], out[b]);
+            }
+            double *dq = P.dest + gq;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) __stcs(dq + b * P2, out[b]);
+            if (P.nonfinite) {
+                const double sum = (out[0] + out[1]) + (out[2] + out[3]);
+                if (!isfinite(sum)) {
+#pragma unroll
+                    for (int b = 0; b < BB; ++b)
+                        if (!isfinite(out[b]))
+                            atomicMin(P.nonfinite, ((unsigned long long)q * P.Nvx + vx0 + b) * P.Nvy + vy);
+                }
+            }
+            if (P.partials) {
+                // reference fold tree (fields.py:28-47) over each aligned
+                // 16-wide vy chunk: transpose-reduce the 4 rows over the lanes
+                const bool o1 = tl & 1, o2 = tl & 2;
+                double w2[2];
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const double keep = o1 ? out[2 * m + 1] : out[2 * m];
+                    const double send = o1 ? out[2 * m] : out[2 * m + 1];
+                    w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                }
+                const double keep = o2 ? w2[1] : w2[0];
+                const double send = o2 ? w2[0] : w2[1];
+                double w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
+                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
+                if (tl < BB) P.partials[((long long)q * P.Nvx + vx0 + tl) * nlt + lt] = w1;  // lane tl: row tl
+            }
+        }
+        gq += P1;
+        __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
 }
 
-constexpr int T12K = 32, T12L = 32, T12NS = 3, T12CK = 2;
-using Tile12Cfg = Tile12<T12K, T12L, T12NS>;
+// Geometry (VPFV_R12_CFG): 1 = (32, 16) tiles, 128 threads, <=168 registers,
+// 3 CTAs per SM (default; measured best at 256^3), 0 = the same at 2 CTAs
+// per SM, 2 = (64, 16) tiles at 1 CTA per SM.
+static int geo12_cfg() {
+    static int c = -1;
+    if (c < 0) {
+        const char *e = getenv("VPFV_R12_CFG");
+        c = e ? atoi(e) : 1;
+        if (c < 0 || c > 2) c = 1;
+    }
+    return c;
+}
 
 bool tma_1d2v_eligible(int Nx, int Nvx, int Nvy, unsigned flags) {
     if (flags & VPFV_EXACT) return false;
     if (flags & (VPFV_WRAP(1) | VPFV_WRAP(2))) return false;
-    if (Nvx % T12K || Nvy % T12L || Nx < 1 || Nvy / T12L > 16) return false;
+    if (Nvx % 32 || Nvy % r12::BL || Nx < 1 || Nvy / r12::BL > 16) return false;
     return tma_available();
+}
+
+template <class GEO>
+static int launch12(const double *src, const double *const ops[r12::OPS_MAX], const double *tab, Stage12 P,
+                    int xsegments, cudaStream_t s) {
+    using namespace r12;
+    const int cols = (P.Nvx / GEO::BK) * (P.Nvy / BL);
+    int nseg = xsegments;
+    if (nseg <= 0) {  // ~6 waves at 2 CTAs per SM, segments >= 8 planes
+        nseg = (6 * 148 + cols - 1) / cols;
+        if (nseg > P.Nx / 8) nseg = P.Nx / 8;
+        if (nseg < 1) nseg = 1;
+    }
+    P.nseg = nseg;
+    P.seglen = (P.i1 - P.i0 + nseg - 1) / nseg;
+    Maps12 maps;
+    const unsigned long long dims[3] = {(unsigned long long)P.Nvy + 6, (unsigned long long)P.Nvx + 6,
+                                        (unsigned long long)P.Nx + 6};
+    const unsigned long long strides[2] = {dims[0] * 8, dims[0] * dims[1] * 8};
+    const unsigned bh[3] = {GEO::TW, GEO::TK, 1}, bo[3] = {GEO::OPW, GEO::BK, 1};
+    if (!tma_map(src, 3, dims, strides, bh, &maps.halo)) return set_error(VPFV_ECUDA, "tensor map failed");
+    for (int o = 0; o < OPS_MAX; ++o) {
+        if (o < P.nops) {
+            if (!tma_map(ops[o], 3, dims, strides, bo, &maps.op[o])) return set_error(VPFV_ECUDA, "tensor map failed");
+        } else {
+            maps.op[o] = maps.halo;
+        }
+    }
+    const unsigned long long tdims[2] = {8, (unsigned long long)P.Nx + 2};
+    const unsigned long long tstr[1] = {64};
+    const unsigned tbox[2] = {8, 3};
+    if (!tma_map(tab, 2, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(stage1d2v_rb_kernel<GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        attr = true;
+    }
+    stage1d2v_rb_kernel<GEO><<<cols * nseg, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    return check_launch("stage_1d2v_tma");
 }
 
 }  // namespace vpfv
@@ -262,8 +413,31 @@ extern "C" int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags
     return tma_1d2v_eligible(Nx, Nvx, Nvy, flags) ? 1 : 0;
 }
 
-extern "C" int vpfv_tables_1d_packed(const double *Ex, double *packed, int Nx, double qmk2, double g,
-                                     double t1, double den1, void *stream);
+extern "C" int vpfv_stage_1d2v_partials_chunk(void) { return r12::BL; }
+
+namespace {
+struct Operands12 {  // ca A + cb B + cd dest grouped by array; the src part is folded
+    const double *ptr[3];
+    double coef[3];
+    int n = 0, fold = 0;
+    double cfold = 0.0;
+    void add(const double *p, double c, const double *src) {
+        if (c == 0.0) return;
+        if (p == src) {
+            cfold += c;
+            fold = 1;
+            return;
+        }
+        for (int i = 0; i < n; ++i)
+            if (ptr[i] == p) {
+                coef[i] += c;
+                return;
+            }
+        ptr[n] = p;
+        coef[n++] = c;
+    }
+};
+}  // namespace
 
 extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const double *src,
                                      double ca, double cb, double cd, double cL, const double *vxc,
@@ -273,35 +447,25 @@ extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double
                                      unsigned long long *nonfinite, const double *packed_tables,
                                      double *moment_partials, int xsegments, void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
-    if (!packed_tables || !tma_1d2v_eligible(Nx, Nvx, Nvy, flags)) {
+    Operands12 ops;
+    ops.add(A, ca, src);
+    ops.add(B, cb, src);
+    ops.add(dest, cd, src);
+    if (!packed_tables || !tma_1d2v_eligible(Nx, Nvx, Nvy, flags) || ops.n > r12::OPS_MAX) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 1D-2V path");
         return vpfv_stage_1d2v(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, avy, c1, c2, hx, hvx, hvy, Nx,
                                Nvx, Nvy, flags, dt_dev, cL_div, nonfinite, stream);
     }
     Stage12 P{};
     P.dest = dest;
+    P.src = src;
     P.cL = cL;
     P.dt_dev = dt_dev;
     P.cL_div = cL_div;
-    const double *ops[3] = {nullptr, nullptr, nullptr};
-    int nops = 0;
-    if (ca != 0.0 || (cb != 0.0 && B == A)) {
-        ops[nops] = A;
-        P.opc[nops++] = (B == A) ? ca + cb : ca;
-    }
-    if (cb != 0.0 && B != A) {
-        ops[nops] = B;
-        P.opc[nops++] = cb;
-    }
-    if (cd != 0.0) {
-        ops[nops] = dest;
-        P.opc[nops++] = cd;
-    }
-    if (nops == 0) {
-        ops[nops] = src;
-        P.opc[nops++] = 0.0;
-    }
-    P.nops = nops;
+    P.nops = ops.n;
+    for (int o = 0; o < ops.n; ++o) P.opc[o] = ops.coef[o];
+    P.fold = ops.fold;
+    P.cfold = ops.cfold;
     P.nonfinite = nonfinite;
     P.vxc = vxc;
     P.vyc = vyc;
@@ -317,35 +481,10 @@ extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double
     P.partials = moment_partials;
     P.i0 = 0;
     P.i1 = Nx;
-    const int cols = (Nvx / T12K) * (Nvy / T12L);
-    int nseg = xsegments;
-    if (nseg <= 0) {
-        nseg = (4 * 148 + cols - 1) / cols;
-        if (nseg > Nx / 8) nseg = Nx / 8;
-        if (nseg < 1) nseg = 1;
-    }
-    P.nseg = nseg;
-    P.seglen = (Nx + nseg - 1) / nseg;
-    Maps12 maps;
-    const unsigned long long dims[3] = {(unsigned long long)Nvy + 6, (unsigned long long)Nvx + 6,
-                                        (unsigned long long)Nx + 6};
-    const unsigned long long strides[2] = {dims[0] * 8, dims[0] * dims[1] * 8};
-    const unsigned bh[3] = {T12L + 8, T12K + 6, 1}, bo[3] = {T12L + 2, T12K, 1};
-    if (!tma_map(src, 3, dims, strides, bh, &maps.halo)) return set_error(VPFV_ECUDA, "tensor map failed");
-    for (int o = 0; o < nops; ++o)
-        if (!tma_map(ops[o], 3, dims, strides, bo, &maps.op[o])) return set_error(VPFV_ECUDA, "tensor map failed");
-    for (int o = nops; o < 3; ++o) maps.op[o] = maps.halo;
-    const unsigned long long tdims[2] = {8, (unsigned long long)Nx + 2};
-    const unsigned long long tstr[1] = {64};
-    const unsigned tbox[2] = {8, 3};
-    if (!tma_map(packed_tables, 2, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
-    auto kern = stage1d2v_tma_kernel<T12K, T12L, T12NS, T12CK>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tile12Cfg::SMEM);
-        attr = true;
-    }
-    const int nblocks = cols * nseg;
-    kern<<<nblocks, (T12K / T12CK) * T12L, Tile12Cfg::SMEM, (cudaStream_t)stream>>>(maps, P);
-    return check_launch("stage_1d2v_tma");
+    const double *opp[r12::OPS_MAX] = {ops.n > 0 ? ops.ptr[0] : nullptr, ops.n > 1 ? ops.ptr[1] : nullptr};
+    cudaStream_t st = (cudaStream_t)stream;
+    const int cfg = geo12_cfg();
+    if (cfg == 2 && Nvx % 64 == 0) return launch12<r12::Geo<64, 1>>(src, opp, packed_tables, P, xsegments, st);
+    if (cfg == 1) return launch12<r12::Geo<32, 3>>(src, opp, packed_tables, P, xsegments, st);
+    return launch12<r12::Geo<32, 2>>(src, opp, packed_tables, P, xsegments, st);
 }

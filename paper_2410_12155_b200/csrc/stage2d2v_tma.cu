@@ -642,25 +642,32 @@ __global__ void __launch_bounds__(256) moment_partials_vec_kernel(const double *
                                                                   double *__restrict__ n, int nphys, double vol) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= nphys) return;
-    constexpr int V = R * NLT;  // doubles per lane
-    const double *src = part + ((size_t)warp * 32 + lane) * V;
-    double x[V];
-    if (V % 2 == 0) {
+    const double *src = part + ((size_t)warp * 32 + lane) * (R * NLT);
+    double rows[R];
 #pragma unroll
-        for (int t = 0; t < V; t += 2) {
-            const double2 d = __ldcs(reinterpret_cast<const double2 *>(src + t));
-            x[t] = d.x;
-            x[t + 1] = d.y;
+    for (int r = 0; r < R; ++r) {  // one vx row: its NLT chunks, folded in registers
+        double x[NLT];
+        if (NLT % 2 == 0) {
+#pragma unroll
+            for (int t = 0; t < NLT; t += 2) {
+                const double2 d = __ldcs(reinterpret_cast<const double2 *>(src + r * NLT + t));
+                x[t] = d.x;
+                x[t + 1] = d.y;
+            }
+        } else {
+            x[0] = __ldcs(src + r * NLT);
         }
-    } else {
 #pragma unroll
-        for (int t = 0; t < V; ++t) x[t] = __ldcs(src + t);
+        for (int w = 1; w < NLT; w <<= 1)
+#pragma unroll
+            for (int t = 0; t < NLT; t += 2 * w) x[t] = __dadd_rn(x[t], x[t + w]);
+        rows[r] = x[0];
     }
 #pragma unroll
-    for (int w = 1; w < NLT * R; w <<= 1)  // chunks of a row, then rows: adjacent pairs, level by level
+    for (int w = 1; w < R; w <<= 1)  // the lane's rows, adjacent pairs level by level
 #pragma unroll
-        for (int t = 0; t < V; t += 2 * w) x[t] = __dadd_rn(x[t], x[t + w]);
-    double v = x[0];
+        for (int t = 0; t < R; t += 2 * w) rows[t] = __dadd_rn(rows[t], rows[t + w]);
+    double v = rows[0];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
     if (lane == 0) n[warp] = __dmul_rn(v, vol);
@@ -674,12 +681,7 @@ static bool launch_vec_r(const double *part, double *n, int nphys, int nlt, doub
         case 2: moment_partials_vec_kernel<R, 2><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
         case 4: moment_partials_vec_kernel<R, 4><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
         case 8: moment_partials_vec_kernel<R, 8><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
-        case 16:
-            if (R <= 4) {
-                moment_partials_vec_kernel<(R <= 4 ? R : 4), 16><<<grid, 256, 0, s>>>(part, n, nphys, vol);
-                return true;
-            }
-            return false;
+        case 16: moment_partials_vec_kernel<R, 16><<<grid, 256, 0, s>>>(part, n, nphys, vol); return true;
         default: return false;
     }
 }

@@ -117,6 +117,14 @@ __device__ __forceinline__ void load3d_s(unsigned dst, const CUtensorMap *map, u
         : "memory");
 }
 
+__device__ __forceinline__ void load2d_s(unsigned dst, const CUtensorMap *map, unsigned bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

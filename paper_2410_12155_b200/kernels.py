@@ -101,7 +101,7 @@ class StageTables:
         g = self.grid
         if (g.d, g.v) == (2, 2):
             return (g.N[0], g.N[1], g.N[2], g.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk())
-        return (g.N[0], g.N[1], g.N[2] // 32)
+        return (g.N[0], g.N[1], g.N[2] // _lib.load().vpfv_stage_1d2v_partials_chunk())
 
     # -- per-stage tables from E (device arrays on the physical grid) ---------
     def update(self, E, stream, packed=False):
