@@ -45,6 +45,14 @@ WORKLOADS = {
     "ep2d2v-64": "2D2V electron-proton m_r=1836, 64^4 per species (BASELINE config 5, per GPU)",
 }
 
+KERNEL_OF = {  # the dominant (stage) kernel of each workload
+    "landau2d-128": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
+    "landau2d-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
+    "ep2d2v-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
+    "weibel-256": "stage1d2v_rb_kernel (fused 1D-2V RHS + RK4 update, TMA-tiled)",
+    "twostream-1024": "stage_1d1v_kernel (fused 1D-1V RHS + RK4 update)",
+}
+
 STAGE_BYTES = (16, 24, 24, 32)  # algorithmic bytes/cell of RK stages 1..4
 
 
@@ -287,7 +295,7 @@ def run_b200(args, rank, world, device):
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": sum(b * cells_local for b in STAGE_BYTES) / 4,
-                     "kernel": "vpfv stage_2d2v (fused RHS + RK4 update)",
+                     "kernel": KERNEL_OF[args.workload],
                      "algorithmic_bytes_per_cell_per_step": sum(STAGE_BYTES),
                      "stage_ms_per_step": [m / args.steps for m in stage_ms],
                      "share_of_step": share, "peak_kind": peak_kind},
