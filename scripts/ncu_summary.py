@@ -29,13 +29,27 @@ KEYS = {
 }
 
 
+SCALE = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3,  # -> GB
+         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,           # -> ms
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+
+
 def raw(report):
+    """Metric values of the first profiled launch, bytes in GB and times in ms."""
     out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = csv.reader(io.StringIO(out))
     h = next(r)
-    next(r)
+    units = next(r)
     vals = next(r)
-    return dict(zip(h, vals))
+    d = {}
+    for k, u, v in zip(h, units, vals):
+        if u in SCALE and v not in ("", "n/a"):
+            try:
+                v = str(float(v.replace(",", "")) * SCALE[u])
+            except ValueError:
+                pass
+        d[k] = v
+    return d
 
 
 def stalls(d, n=6):
