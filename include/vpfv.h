@@ -171,6 +171,16 @@ int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, 
 int vpfv_moment(const double *f, double *n, int d, int v, const int *N, double vol,
                 void *stream);
 
+/* Momentum / kinetic-energy velocity sums per physical cell with the
+ * midpoint-to-average lift of higher_moments (fields.py:131-161):
+ * out[p][2k] = sum_v (v_c f + h_k^2/12 df/dv_k),
+ * out[p][2k+1] = sum_v ((v_c^2 + h_k^2/12) f + h_k^2/6 v_c df/dv_k) for each
+ * velocity dim k (centres vc0 / vc1, widths h0 / h1); p runs over the physical
+ * grid in C order.  Needs the velocity ghosts (frozen values) in f.  Used by
+ * the device diagnostics rows (conserved_quantities, diagnostics.py:85-122). */
+int vpfv_higher_moments(const double *f, int d, int v, const int *N, const double *vc0,
+                        const double *vc1, double h0, double h1, double *out, void *stream);
+
 /* rho = sum_s q[s] * n[s*nphys + p], then rho -= mean(rho)
  * (fields.py:164-169; the mean is a fixed-order tree sum / nphys). */
 int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,

@@ -139,3 +139,70 @@ def fit_growth_rate(ts, amps, t_min=None, t_max=None, peaks=False):
     if len(idx) < 2:
         raise ValueError("not enough samples in the fit window")
     return float(np.polyfit(ts[idx], np.log(a[idx]), 1)[0])
+
+
+class DeviceDiagnostics:
+    """``conserved_quantities`` from the device state without copying f to
+    the host: per species the fold-tree velocity moment
+    with unit volume (``vpfv_moment``, so the mass stays bitwise the
+    reference's fold over all axes once the host folds the physical axes) and
+    the momentum / kinetic-energy velocity sums (``vpfv_higher_moments``); only
+    physical-grid arrays cross PCIe, and the host finishes in the reference's
+    order of operations (diagnostics.py:85-122, fields.py:131-161)."""
+
+    def __init__(self, grids, device):
+        import torch
+
+        from . import _lib
+
+        self._lib = _lib
+        self.grids = tuple(grids)
+        self.device = device
+        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)  # noqa: E731
+        self.vc = [[dev(g.centers(k)) for k in g.velocity_dims] for g in self.grids]
+        self.N = [_lib.int_array(g.N) for g in self.grids]
+        self.n_raw = [torch.empty(tuple(g.N[:g.d]), dtype=torch.float64, device=device) for g in self.grids]
+        self.hm = [torch.empty(tuple(g.N[:g.d]) + (2 * g.v,), dtype=torch.float64, device=device)
+                   for g in self.grids]
+
+    def row(self, arrays, species, E, t, dt, stream):
+        """One DiagnosticsRow from the padded device arrays (velocity ghosts
+        stored) and the host E dict of the same instant."""
+        lib = self._lib
+        for s, (g, f) in enumerate(zip(self.grids, arrays)):
+            lib.call("vpfv_moment", f.data_ptr(), self.n_raw[s].data_ptr(), g.d, g.v, self.N[s], 1.0, stream)
+            vcs = self.vc[s]
+            hv = [g.h[k] for k in g.velocity_dims]
+            lib.call("vpfv_higher_moments", f.data_ptr(), g.d, g.v, self.N[s], vcs[0].data_ptr(),
+                     vcs[1].data_ptr() if len(vcs) > 1 else None, hv[0], hv[1] if len(hv) > 1 else 0.0,
+                     self.hm[s].data_ptr(), stream)
+        n_raw = [a.cpu().numpy() for a in self.n_raw]
+        hm = [a.cpu().numpy() for a in self.hm]
+        masses = []
+        mom_tot = None
+        kinetic = 0.0
+        for g, sp, n0, h in zip(self.grids, species, n_raw, hm):
+            cellvol = 1.0
+            for w in g.h:
+                cellvol *= w
+            masses.append((sp.name, float(fold_tree_sum(n0, tuple(range(g.d)))) * cellvol))
+            vol = 1.0
+            for k in g.velocity_dims:
+                vol *= g.h[k]
+            mom = [h[..., 2 * k] * vol for k in range(g.v)]
+            kin = 0.0
+            for k in range(g.v):
+                kin = kin + h[..., 2 * k + 1] * vol
+            kin = 0.5 * kin
+            physvol = 1.0
+            for k in range(g.d):
+                physvol *= g.h[k]
+            if mom_tot is None:
+                mom_tot = [0.0] * len(mom)
+            for k, mk in enumerate(mom):
+                mom_tot[k] += sp.m * float(np.sum(mk)) * physvol
+            kinetic += sp.m * float(np.sum(kin)) * physvol
+        U = 0.5 * field_amplitude(E, self.grids[0]) ** 2
+        return DiagnosticsRow(t=t, dt=dt, mass=tuple(masses), momentum=math.sqrt(sum(p * p for p in mom_tot)),
+                              field_energy=U, kinetic_energy=kinetic, total_energy=U + kinetic,
+                              field_amplitude=field_amplitude(E, self.grids[0]))

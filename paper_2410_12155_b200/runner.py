@@ -112,6 +112,7 @@ class Simulation:
         self.partials_next = mk()  # written by stage 4 (moment of the new f0), read by the next stage 1
         self._moment_of = None  # (data_ptr, _version) of the f0 arrays the partials describe
         self._side = [torch.cuda.Stream(self.device) for _ in self.species[1:]]  # concurrent species
+        self._diag = None
         self._last_E = None
         self._timing = False
         self._events = None
@@ -284,6 +285,17 @@ class Simulation:
         return FieldState.solve(dists, self.species, self.schedule)
 
     def diagnostics_row(self, dt):
+        """conserved_quantities of the current state (diagnostics.py:85-122),
+        computed on the device: only physical-grid arrays reach the host."""
+        from .diagnostics import DeviceDiagnostics
+
+        if self._diag is None:
+            self._diag = DeviceDiagnostics(self.grids, self.device)
+        E = self._E_host(self.ctx.f0)
+        return self._diag.row(self.ctx.f0, self.species, E, self.ctx.t, dt, stream_handle(self.device))
+
+    def diagnostics_row_host(self, dt):
+        """The same row from a host copy of the state (the reference path)."""
         E = self._E_host(self.ctx.f0)
         return conserved_quantities(self._host_state(), self.grids, self.species, E, self.ctx.t, dt)
 

@@ -580,3 +580,25 @@ def test_host_pipeline_equals_advance():
         ref.ctx.f0[0][inner].copy_(inputs[k][0])
         ref.advance(dt)
         assert torch.equal(ref.ctx.f0[0][inner].cpu(), outs[k][0]), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maker", ["landau2d", "lhdi", "landau1d", "ep"])
+def test_device_diagnostics_row_matches_host_row(maker):
+    """Simulation.diagnostics_row (device velocity sums)
+    equals the host mirror of conserved_quantities (diagnostics.py:85-122) on
+    the same state: mass bitwise (fold tree), the rest to rounding."""
+    mk = {"landau2d": lambda: P.make_problem(P.landau_spec(), 16, 32),
+          "lhdi": lambda: P.make_problem(P.ProblemSpec("lhdi"), 16, 32),
+          "landau1d": lambda: P.make_landau_1d(P.landau_spec(alpha=0.01), 32, 64),
+          "ep": lambda: P.make_electron_proton_2d2v(16, 32)}[maker]
+    sim = R.Simulation(mk())
+    dt = 0.9 * sim.max_dt()
+    sim.advance(dt)
+    dev, host = sim.diagnostics_row(dt), sim.diagnostics_row_host(dt)
+    assert dev.mass == host.mass
+    scale = max(abs(host.kinetic_energy), abs(host.total_energy), 1.0)
+    assert abs(dev.kinetic_energy - host.kinetic_energy) <= 1e-12 * scale
+    assert abs(dev.total_energy - host.total_energy) <= 1e-12 * scale
+    assert dev.field_energy == host.field_energy and dev.field_amplitude == host.field_amplitude
+    assert abs(dev.momentum - host.momentum) <= 1e-12 * scale
