@@ -294,6 +294,36 @@ class Simulation:
         E = self._E_host(self.ctx.f0)
         return self._diag.row(self.ctx.f0, self.species, E, self.ctx.t, dt, stream_handle(self.device))
 
+    def checkpoint(self, directory, tag="ckpt"):
+        """Write the current state as one VPFV snapshot per species
+        (diagnostics.py:187-203 format; file name ``{tag}_{species}.vpfv``),
+        streamed from the device a few x planes at a time."""
+        import os
+
+        from .snapshot import save_device
+
+        os.makedirs(directory, exist_ok=True)
+        paths = []
+        for a, g, name in zip(self.ctx.f0, self.grids, self._names):
+            path = os.path.join(directory, f"{tag}_{name}.vpfv")
+            save_device(path, a, g, name, self.ctx.t)
+            paths.append(path)
+        return paths
+
+    def restore(self, directory, tag="ckpt"):
+        """Load the interiors written by ``checkpoint`` (the frozen velocity
+        ghosts stay this set-up's t = 0 values, as in the reference) and the
+        time; the next step recomputes the moment (tensor versions changed)."""
+        import os
+
+        from .snapshot import load_device
+
+        t = None
+        for a, g, name in zip(self.ctx.f0, self.grids, self._names):
+            _, t = load_device(os.path.join(directory, f"{tag}_{name}.vpfv"), a, g)
+        self.ctx.t = t
+        return t
+
     def diagnostics_row_host(self, dt):
         """The same row from a host copy of the state (the reference path)."""
         E = self._E_host(self.ctx.f0)

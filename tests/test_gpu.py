@@ -602,3 +602,29 @@ def test_device_diagnostics_row_matches_host_row(maker):
     assert abs(dev.total_energy - host.total_energy) <= 1e-12 * scale
     assert dev.field_energy == host.field_energy and dev.field_amplitude == host.field_amplitude
     assert abs(dev.momentum - host.momentum) <= 1e-12 * scale
+
+
+@pytest.mark.gpu
+def test_checkpoint_restore_streams_bitwise(tmp_path):
+    """Simulation.checkpoint streams f0 interiors to VPFV snapshots (the
+    reference reader's format); restore into a fresh Simulation continues
+    bitwise."""
+    from paper_2410_12155_b200 import snapshot as S
+
+    setup = P.make_electron_proton_2d2v(16, 32)
+    sim = R.Simulation(setup)
+    dt = 0.9 * sim.max_dt()
+    sim.fixed_dt = dt
+    for _ in range(2):
+        sim.advance(dt)
+    paths = sim.checkpoint(str(tmp_path), tag="c")
+    for p, want in zip(paths, sim.interiors()):
+        f, t = S.read_snapshot(p)
+        assert t == sim.t
+        assert np.array_equal(f.data[f.grid.interior_slices()], want)
+    other = R.Simulation(P.make_electron_proton_2d2v(16, 32), dt=dt)
+    assert other.restore(str(tmp_path), tag="c") == sim.t
+    sim.advance(dt)
+    other.advance(dt)
+    for a, b in zip(sim.interiors(), other.interiors()):
+        assert np.array_equal(a, b)

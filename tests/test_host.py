@@ -1,6 +1,7 @@
 """CPU-side tests: the C ABI library, host API mirror and set-ups (no GPU)."""
 
 import math
+import os
 import re
 
 import numpy as np
@@ -145,3 +146,29 @@ def test_synthetic_setups_shapes():
     assert [sp.name for sp in s5.species] == ["i", "e"]
     assert s5.species[1].m == pytest.approx(1 / 1836.0)
     assert s5.dists[0].grid.N[:2] == s5.dists[1].grid.N[:2]
+
+
+def test_snapshot_matches_reference_writer_bytes_and_round_trip(tmp_path):
+    """write_snapshot / read_snapshot against a file the reference wrote
+    (tests/golden/make_snapshot_golden.py; diagnostics.py:187-234)."""
+    import numpy as np
+
+    from paper_2410_12155_b200 import snapshot as S
+    from paper_2410_12155_b200.grid import DistField, make_grid
+
+    ref = os.path.join(os.path.dirname(__file__), "golden", "snapshot_ref.vpfv")
+    f, t = S.read_snapshot(ref)
+    N = (8, 8, 16)
+    assert t == 1.25 and f.species == "e-" and tuple(f.grid.N) == N and (f.grid.d, f.grid.v) == (1, 2)
+    want = 1.0 + 0.3 * np.random.default_rng(2024).random(N)
+    assert np.array_equal(f.data[f.grid.interior_slices()], want)
+    g = make_grid(1, 2, N, (0.0, -4.0, -5.0), (2 * np.pi, 4.0, 5.0))
+    mine = DistField(g, species="e-")
+    mine.data[g.interior_slices()] = want
+    out = tmp_path / "mine.vpfv"
+    S.write_snapshot(str(out), mine, 1.25)
+    assert out.read_bytes() == open(ref, "rb").read()
+    with pytest.raises(ValueError):
+        bad = tmp_path / "bad.vpfv"
+        bad.write_bytes(b"XXXX" + out.read_bytes()[4:])
+        S.read_snapshot(str(bad))
