@@ -315,6 +315,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(y0 + NG) * P2 +
                    (long long)(vx0 + NG) * P3 + (vy + NG);
 
+    // moment partials of row (y0 + tl/BB, vx0 + tl%BB) for the cell plane of the
+    // first iteration (lanes tl >= NC never store), advanced one plane per iteration
+    const long long pstep = (long long)P.Ny * P.Nvx * nlt;
+    double *ppart = P.partials + (long long)(p_first - 3) * pstep +
+                    ((long long)(y0 + (tl % NC) / BB) * P.Nvx + vx0 + (tl % NC) % BB) * nlt + lt;
+
     double acc[NC][6];
 #pragma unroll
     for (int i = 0; i < NC; ++i)
@@ -520,20 +526,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             }
 #pragma unroll
             for (int i = 0; i < NC; ++i) __stcs(dq + (i / BB) * P2 + (i % BB) * P3, out[i]);
-            if (P.nonfinite) {
-                // inf/nan propagate through the sum (a finite overflow only
-                // sends the thread to the exact per-cell scan)
-                double sum = out[0];
-#pragma unroll
-                for (int i = 1; i < NC; ++i) sum += out[i];
-                if (!isfinite(sum)) {
-#pragma unroll
-                    for (int i = 0; i < NC; ++i)
-                        if (!isfinite(out[i]))
-                            atomicMin(P.nonfinite,
-                                      (((unsigned long long)q * P.Ny + y0 + (i / BB)) * P.Nvx + vx0 + (i % BB)) * P.Nvy + vy);
-                }
-            }
+            bool bad = false;
             if (P.partials) {
                 // reference fold tree over each aligned 16-wide vy chunk
                 // (fields.py:28-47): transpose-reduce the NC rows over the 16
@@ -573,13 +566,30 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                     w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
                     w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
                 }
-                if (tl < NC) {  // lane tl holds row tl = BB a + b
-                    const long long pr = (((long long)q * P.Ny + y0 + tl / BB) * P.Nvx + vx0 + tl % BB);
-                    P.partials[pr * nlt + lt] = w1;
+                if (tl < NC) __stcs(ppart, w1);  // lane tl holds row tl = BB a + b
+                bad = !isfinite(w1);  // every output of the half-warp reached some lane's row sum
+            }
+            if (P.nonfinite) {
+                // the partials' row sums cover every output (inf/nan propagate;
+                // a finite overflow only sends the warp to the exact scan);
+                // without partials, one sum per thread
+                if (!P.partials) {
+                    double sum = out[0];
+#pragma unroll
+                    for (int i = 1; i < NC; ++i) sum += out[i];
+                    bad = !isfinite(sum);
+                }
+                if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+                    for (int i = 0; i < NC; ++i)
+                        if (!isfinite(out[i]))
+                            atomicMin(P.nonfinite,
+                                      (((unsigned long long)q * P.Ny + y0 + (i / BB)) * P.Nvx + vx0 + (i % BB)) * P.Nvy + vy);
                 }
             }
         }
         gq += P1;
+        ppart += pstep;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
 }

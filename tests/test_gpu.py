@@ -628,3 +628,33 @@ def test_checkpoint_restore_streams_bitwise(tmp_path):
     other.advance(dt)
     for a, b in zip(sim.interiors(), other.interiors()):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("with_partials", [True, False])
+def test_tiled_stage_nonfinite_index(with_partials):
+    """A NaN in src on the tiled path: the reported index is the smallest flat
+    interior index of a non-finite output (fused_stage's FloatingPointError
+    contract, _kernels.py:368-373), whether detection rides on the moment
+    partials' row sums or on the per-thread sum."""
+    N = (12, 16, 32, 48)
+    g, sp, src, E, rng = _tiled_case(N, 5)
+    src = src.copy()
+    src[3 + 7, 3 + 5, 3 + 11, 3 + 20] = np.nan
+    want = np.zeros(g.padded_shape)
+    O.fused_stage(want, src, src, src, 1.0, 0.0, 0.0, 0.02, g, sp, E, check=False)
+    bad = ~np.isfinite(want[g.inner()])
+    expect = int(np.flatnonzero(bad.ravel())[0])
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({k: dev(v) for k, v in E.items()}, stream, packed=True)
+    flags = K.wrap_flags(pg)
+    assert tab.fused_moment_ok(flags)
+    part = torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda") if with_partials else None
+    nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    d_src = dev(src)
+    tab.launch(torch.zeros_like(d_src), d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, nonfinite=nf,
+               partials=part, packed=True)
+    assert int(nf.item()) == expect
