@@ -39,6 +39,7 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     # name: (config description, builder args)
     "landau2d-128": "2D2V Landau damping 128^2 x 128^2, single electron species (BASELINE config 4)",
+    "landau1d-128": "1D1V Landau damping 128 x 128, alpha = 0.01 (BASELINE config 1)",
     "landau2d-64": "2D2V Landau damping 64^2 x 64^2 (reduced, for quick runs)",
     "twostream-1024": "1D1V two-stream 1024 x 1024 (BASELINE config 2)",
     "weibel-256": "1D2V bi-Maxwellian 256^3 (BASELINE config 3)",
@@ -51,6 +52,7 @@ KERNEL_OF = {  # the dominant (stage) kernel of each workload
     "ep2d2v-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "weibel-256": "stage1d2v_rb_kernel (fused 1D-2V RHS + RK4 update, TMA-tiled)",
     "twostream-1024": "stage_1d1v_kernel (fused 1D-1V RHS + RK4 update)",
+    "landau1d-128": "stage_1d1v_kernel (fused 1D-1V RHS + RK4 update)",
 }
 
 STAGE_BYTES = (16, 24, 24, 32)  # algorithmic bytes/cell of RK stages 1..4
@@ -61,6 +63,8 @@ def make_setup(name):
 
     if name == "landau2d-128":
         return P.make_problem(P.landau_spec(), 128, 128)
+    if name == "landau1d-128":
+        return P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128)
     if name == "landau2d-64":
         return P.make_problem(P.landau_spec(), 64, 64)
     if name == "twostream-1024":

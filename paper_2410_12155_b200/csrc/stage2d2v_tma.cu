@@ -700,16 +700,16 @@ static bool launch_vec_r(const double *part, double *n, int nphys, int nlt, doub
 // host side: tensor maps and launch
 
 static int tile_cfg(int Nvx, int Nvy) {
-    // 0: (8,16,16) tiles x 1 CTA/SM; 1: (8,8,16) tiles x 2 CTAs/SM, which wins
-    // when the wide tiles leave too few column blocks (measured at 64^4);
-    // VPFV_RB_CFG=0/1 overrides
+    // 0: (8,16,16) tiles x 1 CTA/SM (default: measured best at 128^4 and, with
+    // the species of a 64^4 run launched concurrently, at 64^4); 1: (8,8,16)
+    // tiles x 2 CTAs/SM (VPFV_RB_CFG=1, or when Nvx is not a multiple of 16)
     static int env = -2;
     if (env == -2) {
         const char *e = getenv("VPFV_RB_CFG");
         env = e ? atoi(e) : -1;
     }
     if (env == 0 || env == 1) return env;
-    return (long long)Nvx * Nvy <= 64 * 64 ? 1 : 0;
+    return Nvx % 16 ? 1 : 0;
 }
 
 static int tile_bk(int Nvx, int Nvy) { return tile_cfg(Nvx, Nvy) == 1 ? rb::GeoPair::BK : rb::GeoWide::BK; }
@@ -897,9 +897,9 @@ static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B,
         env_seg = e ? atoi(e) : 0;
     }
     if (nseg <= 0 && env_seg > 0) nseg = env_seg;
-    if (nseg <= 0) {  // at least ~3 waves of one CTA per SM, segments >= 8 planes
+    if (nseg <= 0) {  // ~1.5 waves of one CTA per SM, segments >= 8 planes (each adds 6 x-halo planes)
         const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
-        nseg = (3 * 148 + cols - 1) / cols;
+        nseg = (3 * 148 / 2 + cols - 1) / cols;
         if (nseg > (x_end - x_begin) / 8) nseg = (x_end - x_begin) / 8;
         if (nseg < 1) nseg = 1;
     }

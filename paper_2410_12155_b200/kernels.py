@@ -138,7 +138,7 @@ class StageTables:
 
     # -- launch ---------------------------------------------------------------
     def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
-               nonfinite=None, partials=None, packed=False):
+               nonfinite=None, partials=None, packed=False, xsegments=0):
         g, h, N = self.grid, self.grid.h, self.grid.N
         common_tail = (flags, _ptr(dt_dev), float(cL_div), _ptr(nonfinite), stream)
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
@@ -162,7 +162,7 @@ class StageTables:
             if packed or partials is not None:
                 _lib.call("vpfv_stage_2d2v_fused", *args, flags, _ptr(dt_dev), float(cL_div),
                           _ptr(nonfinite), self.packed.data_ptr() if packed else None,
-                          _ptr(partials), 0, stream)
+                          _ptr(partials), int(xsegments), stream)
             else:
                 _lib.call("vpfv_stage_2d2v", *args, *common_tail)
 

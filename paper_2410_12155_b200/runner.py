@@ -161,7 +161,7 @@ class Simulation:
                 tab.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], st,
                            dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
                            partials=(self.partials if slot < 3 else self.partials_next)[s] if emit_partials else None,
-                           packed=self.tiled[s])
+                           packed=self.tiled[s], xsegments=1 if len(self.tables) > 1 else 0)
                 if timed:
                     self._events[slot][s][1].record()
         for side in forked:
