@@ -1,4 +1,5 @@
-// DFMA latency/throughput probe: k independent dependent-chains per thread
+// DFMA latency / throughput probe (k independent dependent chains per thread).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o dfma_lat dfma_lat.cu && ./dfma_lat
 #include <cstdio>
 #include <cuda_runtime.h>
 template <int K>
