@@ -181,6 +181,15 @@ int vpfv_moment(const double *f, double *n, int d, int v, const int *N, double v
 int vpfv_higher_moments(const double *f, int d, int v, const int *N, const double *vc0,
                         const double *vc1, double h0, double h1, double *out, void *stream);
 
+/* Richardson error of a refinement (richardson_error, diagnostics.py:163-180)
+ * on padded device arrays: coarse interior N[0..D-1], fine interior 2N; each
+ * of nblocks CTAs writes the sum of |coarse - mean of its 2^D fine children|
+ * over its share of the coarse cells to partials[block]; the error is the
+ * in-order sum of the partials divided by prod(N).  Feeds the convergence
+ * ladders of paper_2410_12155_b200.convergence (cli.py:144-181). */
+int vpfv_richardson_partials(const double *coarse, const double *fine, int D, const int *N,
+                             double *partials, int nblocks, void *stream);
+
 /* rho = sum_s q[s] * n[s*nphys + p], then rho -= mean(rho)
  * (fields.py:164-169; the mean is a fixed-order tree sum / nphys). */
 int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,

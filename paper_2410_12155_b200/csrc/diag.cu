@@ -86,3 +86,69 @@ extern "C" int vpfv_higher_moments(const double *f, int d, int v, const int *N, 
         higher_moments_kernel<2><<<grid, 256, 0, s>>>(f0, xstride, ystride, N[d], N[d + 1], P[d + 1], M, out);
     return check_launch("higher_moments");
 }
+
+// ---------------------------------------------------------------------------
+// Richardson error of a refinement (diagnostics.py:163-180): the fine field
+// aggregated exactly onto the coarse cells (arithmetic mean of the 2^D
+// children) and the L1 difference, summed per CTA (the host adds the partial
+// sums in order and divides by the coarse cell count).
+
+struct Dims4 {
+    int n[4];       // coarse interior extents (1 for unused dims)
+    long long sa[4], sb[4];  // padded strides of the coarse / fine arrays
+    int D;
+};
+
+__global__ void __launch_bounds__(256) richardson_kernel(const double *__restrict__ a, const double *__restrict__ b,
+                                                         Dims4 g, long long total, double *__restrict__ part) {
+    double acc = 0.0;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < total;
+         c += (long long)gridDim.x * blockDim.x) {
+        long long r = c, oa = 0, ob = 0;
+        int idx[4];
+        for (int k = g.D - 1; k >= 0; --k) {
+            idx[k] = (int)(r % g.n[k]);
+            r /= g.n[k];
+        }
+        for (int k = 0; k < g.D; ++k) {
+            oa += (idx[k] + NG) * g.sa[k];
+            ob += (2 * idx[k] + NG) * g.sb[k];
+        }
+        double s = 0.0;
+        const int nch = 1 << g.D;
+        for (int m = 0; m < nch; ++m) {
+            long long o = ob;
+            for (int k = 0; k < g.D; ++k)
+                if (m & (1 << (g.D - 1 - k))) o += g.sb[k];
+            s += b[o];
+        }
+        acc += fabs(a[oa] - s / (double)nch);
+    }
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x += red[w];
+        part[blockIdx.x] = x;
+    }
+}
+
+extern "C" int vpfv_richardson_partials(const double *coarse, const double *fine, int D, const int *N,
+                                        double *partials, int nblocks, void *stream) {
+    if (D < 1 || D > 4 || nblocks < 1) return set_error(VPFV_EARG, "richardson: bad arguments");
+    Dims4 g{};
+    g.D = D;
+    long long total = 1, sa = 1, sb = 1;
+    for (int k = D - 1; k >= 0; --k) {
+        g.n[k] = N[k];
+        g.sa[k] = sa;
+        g.sb[k] = sb;
+        sa *= N[k] + 2 * NG;
+        sb *= 2 * N[k] + 2 * NG;
+        total *= N[k];
+    }
+    richardson_kernel<<<nblocks, 256, 0, (cudaStream_t)stream>>>(coarse, fine, g, total, partials);
+    return check_launch("richardson");
+}

@@ -206,3 +206,18 @@ class DeviceDiagnostics:
         return DiagnosticsRow(t=t, dt=dt, mass=tuple(masses), momentum=math.sqrt(sum(p * p for p in mom_tot)),
                               field_energy=U, kinetic_energy=kinetic, total_energy=U + kinetic,
                               field_amplitude=field_amplitude(E, self.grids[0]))
+
+
+def richardson_error(f_N, f_2N):
+    """Volume-weighted L1 difference between a field and its refinement
+    (diagnostics.py:163-180): the fine field aggregated exactly onto the
+    coarse cells (mean of the 2^D children) before differencing."""
+    a = np.asarray(f_N, dtype=float)
+    b = np.asarray(f_2N, dtype=float)
+    if a.ndim != b.ndim or any(2 * na != nb for na, nb in zip(a.shape, b.shape)):
+        raise ValueError(f"refinement shape {b.shape} is not double of {a.shape} everywhere")
+    shape = []
+    for na in a.shape:
+        shape += [na, 2]
+    coarse = b.reshape(shape).mean(axis=tuple(range(1, 2 * a.ndim, 2)))
+    return float(np.mean(np.abs(a - coarse)))

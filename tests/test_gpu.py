@@ -658,3 +658,35 @@ def test_tiled_stage_nonfinite_index(with_partials):
     tab.launch(torch.zeros_like(d_src), d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, nonfinite=nf,
                partials=part, packed=True)
     assert int(nf.item()) == expect
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [(8, 12), (8, 8, 12), (8, 8, 8, 10)])
+def test_richardson_error_device_matches_host(N):
+    from paper_2410_12155_b200 import convergence as CV
+    from paper_2410_12155_b200.diagnostics import richardson_error
+
+    rng = np.random.default_rng(len(N))
+    pad = lambda n: tuple(k + 6 for k in n)  # noqa: E731
+    coarse = rng.random(pad(N))
+    fine = rng.random(pad(tuple(2 * k for k in N)))
+    g = make_grid(1 if len(N) < 4 else 2, len(N) - (1 if len(N) < 4 else 2), N, (0.0,) * len(N), (1.0,) * len(N))
+    got = CV.richardson_error_device(torch.from_numpy(coarse).cuda(), torch.from_numpy(fine).cuda(), g)
+    inner = lambda n: tuple(slice(3, 3 + k) for k in n)  # noqa: E731
+    want = richardson_error(coarse[inner(N)], fine[inner(tuple(2 * k for k in N))])
+    assert abs(got - want) <= 1e-13 * want
+
+
+@pytest.mark.gpu
+def test_convergence_ladder_fourth_order(tmp_path):
+    """A 1D-1V Landau ladder (fixed dt shared by the levels, cli.py:144-181):
+    the observed spatial order of the fourth-order scheme."""
+    from paper_2410_12155_b200 import convergence as CV
+
+    mk = lambda f: P.make_landau_1d(P.landau_spec(alpha=0.1), 16 * f, 16 * f)  # noqa: E731
+    sizes, errors, orders = CV.run_ladder(mk, 4, dt=0.01, t_end=0.2, csv_path=str(tmp_path / "c.csv"))
+    assert sizes == [16, 32, 64, 128]
+    assert all(e > 0 for e in errors) and errors[0] > errors[1] > errors[2]
+    assert orders[-1] > 3.5, orders
+    lines = (tmp_path / "c.csv").read_text().strip().split("\n")
+    assert lines[0] == "N,error,observed_order" and len(lines) == 4

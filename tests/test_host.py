@@ -172,3 +172,17 @@ def test_snapshot_matches_reference_writer_bytes_and_round_trip(tmp_path):
         bad = tmp_path / "bad.vpfv"
         bad.write_bytes(b"XXXX" + out.read_bytes()[4:])
         S.read_snapshot(str(bad))
+
+
+def test_richardson_error_mirror():
+    """The host mirror against the reference's own cases (test_diagnostics.py:134-154)."""
+    import numpy as np
+
+    from paper_2410_12155_b200.diagnostics import richardson_error
+
+    a = np.arange(16.0).reshape(4, 4)
+    fine = np.repeat(np.repeat(a, 2, axis=0), 2, axis=1)
+    assert richardson_error(a, fine) == 0.0
+    assert richardson_error(a + 2.0, fine) == 2.0
+    with pytest.raises(ValueError):
+        richardson_error(np.zeros((8, 8)), np.zeros((8, 16)))
