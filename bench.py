@@ -224,7 +224,7 @@ def run_b200(args, rank, world, device):
     if world > 1:
         from paper_2410_12155_b200.parallel import DistributedSimulation
 
-        sim = DistributedSimulation(setup, dt=None, device=device)
+        sim = DistributedSimulation(setup, dt=None, device=device, velocity_parts=args.velocity_parts)
         dt = 0.9 * sim.max_dt()
         sim.fixed_dt = dt
     else:
@@ -294,7 +294,8 @@ def run_b200(args, rank, world, device):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                    "cells": cells_global, "dt": dt, "l2": "inputs larger than L2 (2.58 GB/buffer)",
-                   "parallelism": f"x-slab x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"x-slab x{world // args.velocity_parts}, vx x{args.velocity_parts}"
+                                   if world > 1 else "single GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_source": traffic_src,
@@ -396,6 +397,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--velocity-parts", type=int, default=1,
+                    help="multi-GPU: partitions of the first velocity dim (ranks = x-slabs x this)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -195,6 +195,11 @@ int vpfv_richardson_partials(const double *coarse, const double *fine, int D, co
 int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int nphys,
                         double *rho, void *stream);
 
+/* x[i] = x[i] * a, i < n (one rounding, __dmul_rn): the velocity volume
+ * applied to fold-tree sums gathered across velocity partitions, so that
+ * n = fold * vol exactly as the single-box moment (fields.py:99-111). */
+int vpfv_scale(double *x, double a, long long n, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Spectral Poisson solve (fields.py:172-213), hand-written fp64 FFT.
  * Host-precomputed tables (numpy, bitwise the reference's k arrays):

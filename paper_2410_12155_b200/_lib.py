@@ -58,6 +58,7 @@ SIGNATURES = {
     "vpfv_moment": (_i, [_p, _p, _i, _i, _p, _d, _p]),
     "vpfv_higher_moments": (_i, [_p, _i, _i, _p, _p, _p, _d, _d, _p, _p]),
     "vpfv_richardson_partials": (_i, [_p, _p, _i, _p, _p, _i, _p]),
+    "vpfv_scale": (_i, [_p, _d, ctypes.c_longlong, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
     "vpfv_poisson_1d": (_i, [_p, _p, _p, _i, _p, _p, _p, _p]),
     "vpfv_poisson_2d": (_i, [_p] * 4 + [_i, _i] + [_p] * 7 + [_p]),

@@ -270,3 +270,17 @@ extern "C" int vpfv_check_device(int dev) {
 }
 
 extern "C" const char *vpfv_last_error(void) { return g_err; }
+
+// x[i] *= a (the velocity volume applied to gathered fold sums: n = fold * vol,
+// the same single rounding as the fused moment kernels)
+__global__ void scale_kernel(double *__restrict__ x, double a, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = __dmul_rn(x[i], a);
+}
+
+extern "C" int vpfv_scale(double *x, double a, long long n, void *stream) {
+    if (n <= 0) return VPFV_OK;
+    const int grid = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+    scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, a, n);
+    return check_launch("scale");
+}

@@ -52,9 +52,11 @@ def slab_bounds(Nx, world, rank):
     return rank * nloc, nloc
 
 
-def local_grid(g, x0, nloc):
-    """Slab grid: non-periodic in x (filled by exchange), global widths kept
-    verbatim (partition.py:177-196)."""
+def local_grid(g, x0, nloc, v0=0, nv=None):
+    """Box grid: an x-slab [x0, x0+nloc) and a range [v0, v0+nv) of the first
+    velocity dim, non-periodic in x (filled by exchange), global widths kept
+    verbatim (partition.py:177-196).  Kernels take the velocity centres from
+    the global tables sliced at v0, never from this grid's lo/hi."""
     lo = list(g.lo)
     hi = list(g.hi)
     lo[0] = g.lo[0] + x0 * g.h[0]
@@ -63,16 +65,42 @@ def local_grid(g, x0, nloc):
     periodic[0] = False
     N = list(g.N)
     N[0] = nloc
+    if nv is not None and nv != g.N[g.d]:
+        k = g.d
+        lo[k] = g.lo[k] + v0 * g.h[k]
+        hi[k] = g.lo[k] + (v0 + nv) * g.h[k]
+        N[k] = nv
     return make_grid(g.d, g.v, N, lo, hi, periodic=periodic, spacing=g.h)
 
 
-class SlabExchange:
-    """x-halo exchange and density all-gather among the ranks of a group."""
+def fold_pairs(parts):
+    """The reference fold tree over a list (adjacent pairs level by level, an
+    odd tail carried; fields.py:28-41): combining the subtree sums of
+    aligned power-of-two velocity blocks reproduces the global fold."""
+    parts = list(parts)
+    while len(parts) > 1:
+        nxt = [parts[i] + parts[i + 1] for i in range(0, len(parts) - 1, 2)]
+        if len(parts) % 2:
+            nxt.append(parts[-1])
+        parts = nxt
+    return parts[0]
 
-    def __init__(self, rank, world, group=None):
+
+class SlabExchange:
+    """Halo exchanges and density gathers among the ranks of a group laid
+    out as ``world // vparts`` x-slabs times ``vparts`` partitions of the
+    first velocity dim (rank = ix * vparts + iv)."""
+
+    def __init__(self, rank, world, group=None, vparts=1):
+        if vparts < 1 or world % vparts:
+            raise ValueError(f"{vparts} velocity partitions do not divide {world} ranks")
         self.rank, self.world, self.group = rank, world, group
-        self.left = (rank - 1) % world
-        self.right = (rank + 1) % world
+        self.pv, self.px = vparts, world // vparts
+        self.ix, self.iv = divmod(rank, vparts)
+        self.left = ((self.ix - 1) % self.px) * vparts + self.iv
+        self.right = ((self.ix + 1) % self.px) * vparts + self.iv
+        self.vlo = rank - 1 if self.iv > 0 else None             # velocity neighbours (velocity is
+        self.vhi = rank + 1 if self.iv < vparts - 1 else None    # not periodic: frozen at the edges)
         # gloo moves host memory only: CUDA tensors are staged through the host
         # (used by the single-box multi-process tests; NCCL sends device memory)
         self.host_staged = world > 1 and dist.get_backend(group) == "gloo"
@@ -80,13 +108,75 @@ class SlabExchange:
     def _gr(self, r):
         return r if self.group is None else dist.get_global_rank(self.group, r)
 
+    def exchange_v(self, fields, vdim):
+        """Fill the inner-boundary ghost rows of velocity dim ``vdim`` from the
+        velocity neighbours: faces of 3 rows over the slab's x interior and
+        every other index (ghosts included), packed contiguous.  Run after the
+        local frozen / periodic fill and before exchange_x, whose full padded
+        planes then carry these rows to the x neighbours."""
+        if self.pv == 1:
+            return
+        ops, unpack = [], []
+        for f in fields:
+            nv = f.shape[vdim] - 2 * NGHOST
+            nx = f.shape[0] - 2 * NGHOST
+
+            def face(r0):
+                idx = [slice(None)] * f.ndim
+                idx[0] = slice(NGHOST, NGHOST + nx)
+                idx[vdim] = slice(r0, r0 + NGHOST)
+                return tuple(idx)
+
+            staged = self.host_staged and f.is_cuda
+            for peer, send_rows, recv_rows in ((self.vhi, nv, nv + NGHOST), (self.vlo, NGHOST, 0)):
+                if peer is None:
+                    continue
+                out = f[face(send_rows)].contiguous()
+                inb = torch.empty_like(out)
+                if staged:
+                    out, inb = out.cpu(), inb.cpu()
+                ops.append(dist.P2POp(dist.isend, out, self._gr(peer), self.group))
+                ops.append(dist.P2POp(dist.irecv, inb, self._gr(peer), self.group))
+                unpack.append((f, face(recv_rows), inb))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for f, idx, inb in unpack:
+            f[idx].copy_(inb)
+
+    def gather_density(self, sub, out):
+        """Global zeroth-moment fold sums from per-rank subtree sums: ``sub``
+        (S, nloc, ...) holds this rank's fold over its velocity block (unit
+        volume); the velocity partitions of each x-slab are combined in the
+        reference tree order (fold_pairs) and the slabs concatenated into
+        ``out`` (S, Nx, ...).  The caller applies the velocity volume."""
+        if self.world == 1:
+            out.copy_(sub)
+            return out
+        gathered = torch.empty((self.world,) + tuple(sub.shape), dtype=sub.dtype, device=sub.device)
+        self.gather_x(sub.unsqueeze(0), gathered)
+        slabs = [fold_pairs(gathered[ix * self.pv + iv] for iv in range(self.pv)) for ix in range(self.px)]
+        out.copy_(torch.cat(slabs, dim=1))
+        return out
+
+    def gather_state(self, local, out, vdim):
+        """Global interior array from the per-rank box interiors."""
+        if self.world == 1:
+            out.copy_(local)
+            return out
+        gathered = torch.empty((self.world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+        self.gather_x(local.unsqueeze(0), gathered)
+        rows = [torch.cat([gathered[ix * self.pv + iv] for iv in range(self.pv)], dim=vdim)
+                for ix in range(self.px)]
+        out.copy_(torch.cat(rows, dim=0))
+        return out
+
     def exchange_x(self, fields):
         """Fill the 3 low/high x-ghost planes of every padded array in
         ``fields`` from the periodic x neighbours.  Order per peer pair:
         (my last planes -> right's low ghosts, recv my low ghosts from left),
         then (my first planes -> left's high ghosts, recv my high ghosts from
         right) -- consistent even when left == right (world size 2)."""
-        if self.world == 1:
+        if self.px == 1:
             for f in fields:
                 n = f.shape[0] - 2 * NGHOST
                 f[:NGHOST].copy_(f[n:n + NGHOST])
@@ -116,7 +206,7 @@ class SlabExchange:
         its own stream (the stage's x-interior planes read neither the ghost
         planes being received nor anything the sends still read is written).
         The host-staged gloo path completes synchronously."""
-        if self.world == 1 or (self.host_staged and fields[0].is_cuda):
+        if self.px == 1 or (self.host_staged and fields[0].is_cuda):
             self.exchange_x(fields)
             return None
         ops = []
@@ -176,21 +266,23 @@ class _LocalTables:
     """A StageTables view launching on the local slab with table pointers
     offset to the slab's first x row of the global tables."""
 
-    def __init__(self, tables: StageTables, lgrid, x0):
+    def __init__(self, tables: StageTables, lgrid, x0, v0=0):
         self.t = tables
         self.lgrid = lgrid
         self.x0 = x0
+        self.v0 = v0  # first index of the box along the first velocity dim
 
     def launch(self, dest, A, B, src, ca, cb, cd, cL, flags, stream, dt_dev=None, cL_div=1.0,
                nonfinite=None, partials=None, packed=False, x_range=None):
         t, g = self.t, self.lgrid
+        vo = self.v0 * 8  # byte offset of the box's velocity centres in the global tables
         if x_range is not None:  # tiled 2D-2V only (see DistributedSimulation._stage)
             h, N = g.h, g.N
             Ny = t.grid.N[1]
             off = self.x0 * Ny * 8
             ptr = lambda a: a.data_ptr() + off  # noqa: E731
             _lib.call("vpfv_stage_2d2v_fused_range", dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
-                      float(ca), float(cb), float(cd), float(cL), t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.evx),
+                      float(ca), float(cb), float(cd), float(cL), t.vxc.data_ptr() + vo, t.vyc.data_ptr(), ptr(t.evx),
                       ptr(t.evy), t.cB, ptr(t.c1), t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2], h[3],
                       N[0], N[1], N[2], N[3], int(x_range[0]), int(x_range[1]), flags,
                       None if dt_dev is None else dt_dev.data_ptr(), float(cL_div),
@@ -207,11 +299,11 @@ class _LocalTables:
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
                 float(ca), float(cb), float(cd), float(cL))
         if (g.d, g.v) == (1, 1):
-            _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr(), ptr(t.e), ptr(t.c1), h[0], h[1],
+            _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr() + vo, ptr(t.e), ptr(t.c1), h[0], h[1],
                       N[0], N[1], *tail, stream)
         elif (g.d, g.v) == (1, 2):
-            args = (*head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.e), t.avy.data_ptr(), ptr(t.c1), t.c2,
-                    h[0], h[1], h[2], N[0], N[1], N[2])
+            args = (*head, t.vxc.data_ptr() + vo, t.vyc.data_ptr(), ptr(t.e), t.avy.data_ptr() + vo, ptr(t.c1),
+                    t.c2, h[0], h[1], h[2], N[0], N[1], N[2])
             if packed or partials is not None:
                 pk = t.packed.data_ptr() + self.x0 * 8 * 8 if packed else None
                 _lib.call("vpfv_stage_1d2v_fused", *args, *tail, pk,
@@ -219,7 +311,7 @@ class _LocalTables:
             else:
                 _lib.call("vpfv_stage_1d2v", *args, *tail, stream)
         else:
-            args = (*head, t.vxc.data_ptr(), t.vyc.data_ptr(), ptr(t.evx), ptr(t.evy), t.cB, ptr(t.c1),
+            args = (*head, t.vxc.data_ptr() + vo, t.vyc.data_ptr(), ptr(t.evx), ptr(t.evy), t.cB, ptr(t.c1),
                     t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2], h[3], N[0], N[1], N[2], N[3])
             if packed or partials is not None:
                 # packed rows of the global table: local row r <-> global row x0 + r
@@ -235,24 +327,28 @@ class DistributedSimulation:
     each): x-slab decomposition, NCCL halo exchange, replicated Poisson."""
 
     def __init__(self, setup, cfl_fraction=0.9, dt=None, corrections=True, sigma=DEFAULT_SIGMA, *,
-                 device=None, exact=False, group=None):
+                 device=None, exact=False, group=None, velocity_parts=1):
         self.device = require_cuda(device)
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.comm = SlabExchange(self.rank, self.world, group)
+        self.comm = SlabExchange(self.rank, self.world, group, vparts=velocity_parts)
         self.species = tuple(setup.species)
         self.grids = tuple(f.grid for f in setup.dists)  # global grids
         self.cfl_fraction, self.fixed_dt, self.sigma = cfl_fraction, dt, sigma
         self.corrections, self.exact = corrections, exact
         self._names = [f.species for f in setup.dists]
         g0 = self.grids[0]
-        self.x0, self.nloc = slab_bounds(g0.N[0], self.world, self.rank)
-        self.lgrids = tuple(local_grid(g, self.x0, self.nloc) for g in self.grids)
+        self.vdim = g0.d  # the first velocity dim is the one split across velocity partitions
+        self.x0, self.nloc = slab_bounds(g0.N[0], self.comm.px, self.comm.ix)
+        self.vbox = [slab_bounds(g.N[self.vdim], self.comm.pv, self.comm.iv) for g in self.grids]
+        self.lgrids = tuple(local_grid(g, self.x0, self.nloc, v0, nv) for g, (v0, nv) in zip(self.grids, self.vbox))
         f0 = []
-        for f in setup.dists:
+        for f, (v0, nv) in zip(setup.dists, self.vbox):
             data, _ = _host_filled(f)  # global padded, ghosts filled (scatter_field semantics)
-            f0.append(torch.from_numpy(np.ascontiguousarray(data[self.x0:self.x0 + self.nloc + 2 * NGHOST]))
-                      .to(self.device))
+            idx = [slice(None)] * data.ndim
+            idx[0] = slice(self.x0, self.x0 + self.nloc + 2 * NGHOST)
+            idx[self.vdim] = slice(v0, v0 + nv + 2 * NGHOST)
+            f0.append(torch.from_numpy(np.ascontiguousarray(data[tuple(idx)])).to(self.device))
         self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
         # tables and the field solve on the GLOBAL grid (replicated), launches on the slab
         self.gtables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
@@ -261,12 +357,11 @@ class DistributedSimulation:
         self.flags = [base | sum(_lib.VPFV_WRAP(k) for k in range(1, lg.ndim) if lg.periodic[k])
                       for lg in self.lgrids]
         self.tiled = [_GridView(t, lg).fused_moment_ok(fl) for t, lg, fl in zip(self.gtables, self.lgrids, self.flags)]
-        self.tables = [_LocalTables(t, lg, self.x0) for t, lg in zip(self.gtables, self.lgrids)]
+        self.tables = [_LocalTables(t, lg, self.x0, v0) for t, lg, (v0, _) in zip(self.gtables, self.lgrids, self.vbox)]
         self.fields = FieldSolver(self.grids, self.species, self.device)
         S = len(self.species)
         phys_loc = (self.nloc,) + tuple(g0.N[1:g0.d])
-        self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)
-        self._n_gather = torch.empty((self.world, S) + phys_loc, dtype=torch.float64, device=self.device)
+        self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)  # unit-volume folds
         self.fuse_moment = all(self.tiled)
         self.partials = ([torch.empty(_GridView(t, lg).partials_shape(), dtype=torch.float64, device=self.device)
                           for t, lg in zip(self.gtables, self.lgrids)] if self.fuse_moment else None)
@@ -294,20 +389,20 @@ class DistributedSimulation:
         return self.ctx.step
 
     def _densities(self, srcs, from_partials, stream):
-        """Local slab densities -> all-gathered global n in self.fields.n."""
+        """Box fold sums (unit volume) -> gathered, combined across the
+        velocity partitions in fold-tree order, times the velocity volume:
+        the global n in self.fields.n, bitwise the single-GPU moment."""
         for s, (lg, f) in enumerate(zip(self.lgrids, srcs)):
             if from_partials:
                 _lib.call("vpfv_moment_partials", self.partials[s].data_ptr(), self.n_local[s].data_ptr(),
-                          int(np.prod(lg.N[:lg.d])), lg.N[lg.d], self.partials[s].shape[-1],
-                          self.fields.vols[s], stream)
+                          int(np.prod(lg.N[:lg.d])), lg.N[lg.d], self.partials[s].shape[-1], 1.0, stream)
             else:
                 _lib.call("vpfv_moment", f.data_ptr(), self.n_local[s].data_ptr(), lg.d, lg.v,
-                          self._N_arrays[s], self.fields.vols[s], stream)
-        self.comm.gather_x(self.n_local.unsqueeze(0).reshape((1,) + tuple(self.n_local.shape)),
-                           self._n_gather)
-        # (world, S, nloc, ...) -> (S, Nx, ...)
-        S = len(self.species)
-        self.fields.n.copy_(self._n_gather.transpose(0, 1).reshape((S,) + tuple(self.fields.n.shape[1:])))
+                          self._N_arrays[s], 1.0, stream)
+        self.comm.gather_density(self.n_local, self.fields.n)
+        per = int(np.prod(self.fields.n.shape[1:]))
+        for s in range(len(self.species)):
+            _lib.call("vpfv_scale", self.fields.n[s].data_ptr(), self.fields.vols[s], per, stream)
 
     def _solve(self, srcs, from_partials=False):
         stream = stream_handle(self.device)
@@ -321,7 +416,8 @@ class DistributedSimulation:
         no ghost plane; the two 3-plane boundary ranges run once the ghosts
         have arrived.  Otherwise the exchange completes first."""
         stream = stream_handle(self.device)
-        overlap = self.overlap and self.world > 1
+        overlap = self.overlap and self.comm.px > 1
+        self.comm.exchange_v(src, self.vdim)  # velocity faces first: the x planes sent next carry them
         handle = self.comm.exchange_x_start(src) if overlap else self.comm.exchange_x(src)
         use_partials = self.fuse_moment and slot is not None and slot > 0
         emit = self.fuse_moment and slot is not None and slot < 3
@@ -410,5 +506,5 @@ class DistributedSimulation:
         lg, g = self.lgrids[s], self.grids[s]
         local = self.ctx.f0[s][lg.interior_slices()].contiguous()
         out = torch.empty(tuple(g.N), dtype=torch.float64, device=self.device)
-        self.comm.gather_x(local, out)
+        self.comm.gather_state(local, out, self.vdim)
         return out.cpu().numpy()

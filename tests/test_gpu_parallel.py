@@ -29,6 +29,8 @@ def _setup(name):
         return P.make_problem(P.ProblemSpec("two-stream"), 64, 64)
     if name == "lhdi":
         return P.make_problem(P.ProblemSpec("lhdi"), 16, 32)
+    if name == "lhdi64":  # velocity boxes of 32 after a 2-way velocity split: tiled 1D-2V kernel on both sides
+        return P.make_problem(P.ProblemSpec("lhdi"), 16, 64)
     return P.make_electron_proton_2d2v(16, 32)
 
 
@@ -49,7 +51,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, names, dts, steps, q):
+def _worker(rank, world, port, names, dts, steps, q, vparts=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -59,7 +61,7 @@ def _worker(rank, world, port, names, dts, steps, q):
         torch.cuda.set_device(0)
         out = {}
         for name, dt in zip(names, dts):
-            sim = PL.DistributedSimulation(_setup(name), dt=dt, device="cuda:0")
+            sim = PL.DistributedSimulation(_setup(name), dt=dt, device="cuda:0", velocity_parts=vparts)
             for _ in range(steps):
                 sim.advance(dt)
             out[name] = [sim.gather(s) for s in range(len(sim.species))]
@@ -92,6 +94,30 @@ def test_two_ranks_same_gpu_equal_simulation():
     for p in procs:
         p.start()
     got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for n in names:
+        for a, b in zip(got[n], refs[n][1]):
+            assert np.array_equal(a, b), n
+
+
+@pytest.mark.parametrize("world,vparts", [(2, 2), (4, 2)])
+def test_velocity_partitions_same_gpu_equal_simulation(world, vparts):
+    """x-slabs x velocity partitions on the GPU kernels (velocity faces
+    exchanged, fold-tree subtree sums combined across the partitions, the
+    overlapped x exchange when there are two slabs): bitwise the single-GPU
+    run."""
+    names = ["landau2d", "twostream", "lhdi64", "ep"]
+    refs = {n: _reference(n, 2) for n in names}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, names, [refs[n][0] for n in names], 2, q, vparts))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

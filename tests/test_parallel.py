@@ -132,3 +132,131 @@ def test_local_grid_keeps_global_widths():
     lg = PL.local_grid(g, 8, 8)
     assert lg.h == g.h and lg.periodic == (False, True, False, False)
     assert lg.centers(2).tolist() == g.centers(2).tolist()
+
+
+# ---------------------------------------------------------------------------
+# x-slabs x velocity partitions (the north star's "allreduce of the charge
+# density across velocity partitions", here a deterministic gather + fold)
+
+
+def _box_cases():
+    """Cases whose first velocity dim splits into two spans of >= 8 (and x
+    into two when four ranks are used)."""
+    out = []
+    for name in ("twostream", "landau1d"):  # 1D-1V 16 x 16
+        c = G.step_case(name)
+        out.append((name, c["grids"], c["species"], c["init"], c["dt"]))
+    sp = [O.Species("i", 1.0, 1.0, 1.0, 0.1, 1.0, (0.0, 0.01)), O.Species("e", -1.0, 0.04, 1.0, 0.1, 1.0, (0.0, 0.01))]
+    rng = np.random.default_rng(12)
+    grids, init = [], []
+    for vmax in (3.0, 6.0):  # 2D-2V, two species, Nvx = 16
+        g = O.Grid(2, 2, (16, 8, 16, 8), (0.0, 0.0, -vmax, -vmax), (4 * np.pi, 4 * np.pi, vmax, vmax))
+        a = 1.0 + 0.2 * rng.random(g.padded_shape)
+        grids.append(g)
+        init.append(O.fill_ghosts(a, g, O.capture_frozen(a, g)))
+    out.append(("2d2v-2sp-v16", grids, sp, init, 0.01))
+    sp12 = [O.Species("e", -1.0, 1.0, 1.2, 0.4, 1.0, (0.0, 0.0))]  # 1D-2V with a magnetic field (cB != 0)
+    g = O.Grid(1, 2, (16, 16, 12), (0.0, -4.0, -5.0), (2 * np.pi, 4.0, 5.0))
+    a = 1.0 + 0.2 * np.random.default_rng(13).random(g.padded_shape)
+    out.append(("1d2v-B", [g], sp12, [O.fill_ghosts(a, g, O.capture_frozen(a, g))], 0.01))
+    return out
+
+
+def _slice_v(T, g, v0, nv):
+    """Velocity-centre tables sliced to the box's range of the first velocity dim."""
+    out = dict(T)
+    keys = {(1, 1): ("ax",), (1, 2): ("vxc", "avy"), (2, 2): ("vxc",)}[(g.d, g.v)]
+    for k in keys:
+        out[k] = np.asarray(out[k])[v0:v0 + nv]
+    return out
+
+
+def _run_boxes(rank, world, vparts, grids, species, init, dt, steps):
+    comm = PL.SlabExchange(rank, world, vparts=vparts)
+    g0 = grids[0]
+    vd = g0.d
+    x0, nloc = PL.slab_bounds(g0.N[0], comm.px, comm.ix)
+    lgrids, f0, boxes = [], [], []
+    for g, d in zip(grids, init):
+        v0, nv = PL.slab_bounds(g.N[vd], comm.pv, comm.iv)
+        boxes.append((v0, nv))
+        lgrids.append(O.grid_from(PL.local_grid(g, x0, nloc, v0, nv)))
+        filled = O.fill_ghosts(np.array(d), g, O.capture_frozen(d, g))
+        idx = [slice(None)] * g.ndim
+        idx[0] = slice(x0, x0 + nloc + 2 * NGHOST)
+        idx[vd] = slice(v0, v0 + nv + 2 * NGHOST)
+        f0.append(torch.from_numpy(np.ascontiguousarray(filled[tuple(idx)])))
+    local_frozen = [O.capture_frozen(f.numpy(), lg) for f, lg in zip(f0, lgrids)]
+    ctx = O.StepContext(f0=f0, f1=[t.clone() for t in f0], fout=[t.clone() for t in f0])
+    S = len(species)
+
+    def stage(dest, A, B, src, ca, cb, cd, cL, t):
+        for s in range(S):
+            O.fill_ghosts(src[s].numpy(), lgrids[s], local_frozen[s])
+        comm.exchange_v(src, vd)
+        comm.exchange_x(src)
+        sub = torch.from_numpy(np.stack([O.fold_tree_sum(src[s].numpy()[lgrids[s].inner()], lgrids[s].velocity_dims)
+                                         for s in range(S)]))
+        full = torch.empty((S, g0.N[0]) + tuple(sub.shape[2:]), dtype=torch.float64)
+        comm.gather_density(sub, full)
+        dens = [full[s].numpy() * O.velocity_volume(grids[s]) for s in range(S)]
+        _, E = O.poisson_solve(O.charge_density(dens, species), g0)
+        for s in range(S):
+            T = _slice_v(O.slice_tables(O.stage_tables(grids[s], species[s], E), x0, nloc), grids[s], *boxes[s])
+            O.fused_stage(dest[s].numpy(), A[s].numpy(), B[s].numpy(), src[s].numpy(), ca, cb, cd, cL,
+                          lgrids[s], species[s], E, check=False, tables=T)
+
+    for _ in range(steps):
+        O.rk4_38_low_storage_step(ctx, dt, stage)
+        ctx.rotate()
+    out = []
+    for s in range(S):
+        local = torch.from_numpy(np.ascontiguousarray(ctx.f0[s].numpy()[lgrids[s].inner()]))
+        full = torch.empty(tuple(grids[s].N), dtype=torch.float64)
+        comm.gather_state(local, full, vd)
+        out.append(full.numpy())
+    return out
+
+
+def _box_worker(rank, world, vparts, port, steps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for name, grids, species, init, dt in _box_cases():
+            res[name] = _run_boxes(rank, world, vparts, grids, species, init, dt, steps)
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,vparts", [(2, 2), (4, 2)])
+def test_velocity_partitions_equal_single_rank_bitwise(world, vparts):
+    """x-slabs x partitions of the first velocity dim: faces exchanged along
+    velocity, subtree sums of the fold tree combined across the velocity
+    partitions -- bitwise the single-rank run (power-of-two spans,
+    /root/reference/pkg/tests/test_partition.py:736-767)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_box_worker, args=(r, world, vparts, port, 2, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for name, grids, species, init, dt in _box_cases():
+        ref = O.OracleSimulation(grids, species, init, dt=dt, rhs="fused")
+        for _ in range(2):
+            ref.advance(dt)
+        for a, b in zip(got[name], ref.interiors()):
+            assert np.array_equal(a, b), name
+
+
+def test_fold_pairs_is_the_fold_tree():
+    x = np.random.default_rng(3).random(12)
+    for n in (1, 2, 3, 4, 5, 8):
+        assert PL.fold_pairs(list(x[:n])) == O.fold_tree_sum(x[:n], (0,))
