@@ -86,6 +86,36 @@ def fold_pairs(parts):
     return parts[0]
 
 
+def _box_args(f, idx):
+    """(strides, origin, extents) of the box ``idx`` (slices) of a contiguous array."""
+    strides = _lib.ll_array(f.stride())
+    origin = _lib.int_array([sl.start or 0 for sl in idx])
+    ext = _lib.int_array([(sl.stop if sl.stop is not None else n) - (sl.start or 0) for sl, n in zip(idx, f.shape)])
+    return strides, origin, ext
+
+
+def _pack(f, idx):
+    """The box ``idx`` of ``f`` as a contiguous array (vpfv_box_copy on the device)."""
+    if not f.is_cuda:
+        return f[idx].contiguous()
+    ss, so, ext = _box_args(f, idx)
+    shape = tuple(ext)
+    out = torch.empty(shape, dtype=f.dtype, device=f.device)
+    _lib.call("vpfv_box_copy", out.data_ptr(), _lib.ll_array(out.stride()), _lib.int_array([0] * f.ndim),
+              f.data_ptr(), ss, so, f.ndim, ext, stream_handle(f.device))
+    return out
+
+
+def _unpack(f, idx, buf):
+    """Write the contiguous ``buf`` into the box ``idx`` of ``f``."""
+    if not f.is_cuda:
+        f[idx].copy_(buf)
+        return
+    ds, do, ext = _box_args(f, idx)
+    _lib.call("vpfv_box_copy", f.data_ptr(), ds, do, buf.data_ptr(), _lib.ll_array(buf.stride()),
+              _lib.int_array([0] * f.ndim), f.ndim, ext, stream_handle(f.device))
+
+
 class SlabExchange:
     """Halo exchanges and density gathers among the ranks of a group laid
     out as ``world // vparts`` x-slabs times ``vparts`` partitions of the
@@ -131,7 +161,7 @@ class SlabExchange:
             for peer, send_rows, recv_rows in ((self.vhi, nv, nv + NGHOST), (self.vlo, NGHOST, 0)):
                 if peer is None:
                     continue
-                out = f[face(send_rows)].contiguous()
+                out = _pack(f, face(send_rows))
                 inb = torch.empty_like(out)
                 if staged:
                     out, inb = out.cpu(), inb.cpu()
@@ -141,7 +171,7 @@ class SlabExchange:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
         for f, idx, inb in unpack:
-            f[idx].copy_(inb)
+            _unpack(f, idx, inb.to(f.device) if inb.device != f.device else inb)
 
     def gather_density(self, sub, out):
         """Global zeroth-moment fold sums from per-rank subtree sums: ``sub``

@@ -45,6 +45,26 @@ def _reference(name, steps):
     return dt, sim.interiors()
 
 
+def _collect(q, procs, timeout):
+    """The rank-0 result, failing fast when any worker dies (instead of
+    waiting out the queue timeout while the survivors block in a collective)."""
+    import queue
+    import time
+
+    t0 = time.time()
+    while time.time() - t0 < timeout:
+        try:
+            return q.get(timeout=2)
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                raise AssertionError(f"a worker failed (exit codes {dead})")
+    raise AssertionError("workers timed out")
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -93,7 +113,7 @@ def test_two_ranks_same_gpu_equal_simulation():
              for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got = _collect(q, procs, 600)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -117,7 +137,7 @@ def test_velocity_partitions_same_gpu_equal_simulation(world, vparts):
              for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=900)
+    got = _collect(q, procs, 900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

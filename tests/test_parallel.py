@@ -22,6 +22,25 @@ from paper_2410_12155_b200 import parallel as PL
 from paper_2410_12155_b200.grid import NGHOST
 
 
+def _collect(q, procs, timeout):
+    """The rank-0 result, failing fast when any worker dies."""
+    import queue
+    import time
+
+    t0 = time.time()
+    while time.time() - t0 < timeout:
+        try:
+            return q.get(timeout=2)
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                raise AssertionError(f"a worker failed (exit codes {dead})")
+    raise AssertionError("workers timed out")
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -105,7 +124,7 @@ def test_two_rank_slabs_equal_single_rank_bitwise():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, 2, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=300)
+    got = _collect(q, procs, 300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -244,7 +263,7 @@ def test_velocity_partitions_equal_single_rank_bitwise(world, vparts):
     procs = [ctx.Process(target=_box_worker, args=(r, world, vparts, port, 2, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got = _collect(q, procs, 600)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
