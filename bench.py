@@ -307,9 +307,25 @@ def run_b200(args, rank, world, device):
         "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
                           "frac": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9 / peak},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "nvlink": nvlink_line(sim, world, ms / args.steps),
         "clocks": clocks.summary(),
     }
     return line
+
+
+def nvlink_line(sim, world, ms_per_step):
+    """Halo traffic of the multi-GPU step against the NVLink 5 roofline
+    (900 GB/s per direction per GPU, B200_PROFILING.md): the bytes each rank
+    sends per step and the rate they would need if the exchange were not
+    overlapped with compute (a lower bound on the link share of the step)."""
+    if world == 1 or not hasattr(sim, "traffic_report"):
+        return None
+    t = sim.traffic_report()
+    per_step = 4 * t["total_bytes"]
+    gbs = per_step / (ms_per_step / 1e3) / 1e9
+    return {"bytes_per_rank_per_step": per_step, "x_halo_bytes_per_stage": t["x_halo_bytes"],
+            "v_face_bytes_per_stage": t["v_face_bytes"], "density_bytes_per_stage": t["density_bytes"],
+            "rate_at_step_time_GBs": gbs, "peak_GBs": 900.0, "frac": gbs / 900.0}
 
 
 def e2e_measure(sim, dt, steps, device, cells):

@@ -407,6 +407,25 @@ class DistributedSimulation:
         self._N_arrays = [_lib.int_array(lg.N) for lg in self.lgrids]
 
     # ------------------------------------------------------------------
+    def traffic_report(self):
+        """Bytes this rank sends per RK4 stage (the TrafficLog / comm_volumes
+        accounting of partition.py:217-252, :555-596 for this decomposition):
+        x halos (3 full padded planes to each x neighbour), velocity faces
+        (3 rows over the x interior to each velocity neighbour) and the
+        density gather (this box's fold sums to every other rank)."""
+        x_halo = v_face = 0
+        for lg in self.lgrids:
+            P = [n + 2 * NGHOST for n in lg.N]
+            plane = int(np.prod(P[1:]))
+            if self.comm.px > 1:
+                x_halo += 2 * NGHOST * plane * 8
+            nbrs = (self.comm.vlo is not None) + (self.comm.vhi is not None)
+            face = self.nloc * NGHOST * int(np.prod([p for k, p in enumerate(P) if k not in (0, self.vdim)]))
+            v_face += nbrs * face * 8
+        dens = (self.world - 1) * int(self.n_local.numel()) * 8 if self.world > 1 else 0
+        return {"x_halo_bytes": x_halo, "v_face_bytes": v_face, "density_bytes": dens,
+                "total_bytes": x_halo + v_face + dens, "per": "rank and RK4 stage (sent)"}
+
     def local_cells(self):
         return sum(int(np.prod(lg.N)) for lg in self.lgrids)
 

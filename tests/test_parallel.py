@@ -279,3 +279,27 @@ def test_fold_pairs_is_the_fold_tree():
     x = np.random.default_rng(3).random(12)
     for n in (1, 2, 3, 4, 5, 8):
         assert PL.fold_pairs(list(x[:n])) == O.fold_tree_sum(x[:n], (0,))
+
+
+def test_traffic_report_counts_halo_bytes():
+    """The per-stage byte accounting of a (2 x-slabs, 2 velocity partitions)
+    box layout, from shapes alone (no communication)."""
+
+    class _Comm:
+        px, pv, vlo, vhi = 2, 2, None, 3
+
+    class _Sim:
+        pass
+
+    from paper_2410_12155_b200.grid import make_grid
+
+    g = make_grid(2, 2, (8, 8, 16, 8), (0, 0, -1, -1), (1, 1, 1, 1))
+    sim = _Sim()
+    sim.lgrids = [PL.local_grid(g, 0, 8, 0, 8)]
+    sim.comm, sim.nloc, sim.vdim, sim.world = _Comm(), 8, 2, 4
+    sim.n_local = torch.empty((1, 8, 8), dtype=torch.float64)
+    t = PL.DistributedSimulation.traffic_report(sim)
+    plane = 14 * 14 * 14
+    assert t["x_halo_bytes"] == 2 * 3 * plane * 8
+    assert t["v_face_bytes"] == 1 * 8 * 3 * 14 * 14 * 8
+    assert t["density_bytes"] == 3 * 64 * 8
