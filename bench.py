@@ -76,7 +76,7 @@ def make_setup(name):
     raise ValueError(name)
 
 
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_rb_v5_summary.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_rb_final_summary.json")
 
 
 def load_traffic():
