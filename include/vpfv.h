@@ -61,6 +61,17 @@ int vpfv_stage_1d1v(double *dest, const double *A, const double *B, const double
                     unsigned flags, const double *dt_dev, double cL_div,
                     unsigned long long *nonfinite, void *stream);
 
+/* 1D-1V stage with the fused velocity-moment epilogue (fast path, Nv % 128
+ * == 0): as vpfv_stage_1d1v, and moment_partials[x][0][c] receives the
+ * fold-tree subtree sum of the new dest over the aligned 128-wide v chunk c
+ * (finish with vpfv_moment_partials(nphys = Nx, Nvx = 1, nchunks = Nv/128)).
+ * moment_partials == NULL is vpfv_stage_1d1v. */
+int vpfv_stage_1d1v_fused(double *dest, const double *A, const double *B, const double *src,
+                          double ca, double cb, double cd, double cL, const double *ax,
+                          const double *avx, const double *c1, double hx, double hv, int Nx, int Nv,
+                          unsigned flags, const double *dt_dev, double cL_div,
+                          unsigned long long *nonfinite, double *moment_partials, void *stream);
+
 int vpfv_stage_1d2v(double *dest, const double *A, const double *B, const double *src,
                     double ca, double cb, double cd, double cL,
                     const double *vxc, const double *vyc /* Nvy+1, last = cB */,
@@ -199,6 +210,21 @@ int vpfv_charge_density(const double *n, const double *q_host, int nspecies, int
  * applied to fold-tree sums gathered across velocity partitions, so that
  * n = fold * vol exactly as the single-box moment (fields.py:99-111). */
 int vpfv_scale(double *x, double a, long long n, void *stream);
+
+/* The whole 1D field chain of a stage in one CTA: when partials != NULL,
+ * n[s] = vols[s] * fold(partials[s]) (as vpfv_moment_partials, partials[s]
+ * [Nx][rows[s]][chunks[s]], chunks <= 16), else n is given; then
+ * rho = sum_s q_s n_s - mean (n: [nspecies][Nx]), the spectral solve for Ex (as vpfv_poisson_1d), then
+ * each species' line tables from Ex -- plain e[s]/c1[s] (vpfv_tables_1d) or
+ * packed[s] rows (vpfv_tables_1d_packed) when packed[s] != NULL, with c1 = 0
+ * when corrections[s] == 0.  Bitwise the separate charge / Poisson / tables
+ * calls (shared block-level code); replaces three launches per stage of
+ * Simulation._stage (runner.py:183-191) for d = 1. */
+int vpfv_field_1d(const double *const *partials, const int *rows, const int *chunks, const double *vols,
+                  double *n, const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
+                  const double *tw, const double *k2, const double *kd, double *const *e,
+                  double *const *c1, double *const *packed, const double *qmk2, const double *g,
+                  const double *t1, const double *den1, const int *corrections, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Spectral Poisson solve (fields.py:172-213), hand-written fp64 FFT.

@@ -38,6 +38,7 @@ _p = ctypes.c_void_p
 # (name, restype, argtypes) -- must match include/vpfv.h
 SIGNATURES = {
     "vpfv_stage_1d1v": (_i, [_p] * 4 + [_d] * 4 + [_p] * 3 + [_d, _d, _i, _i, _u, _p, _d, _p, _p]),
+    "vpfv_stage_1d1v_fused": (_i, [_p] * 4 + [_d] * 4 + [_p] * 3 + [_d, _d, _i, _i, _u, _p, _d, _p, _p, _p]),
     "vpfv_stage_1d2v": (_i, [_p] * 4 + [_d] * 4 + [_p] * 5 + [_d] * 4 + [_i] * 3 + [_u, _p, _d, _p, _p]),
     "vpfv_stage_2d2v": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d, _p, _d] + [_p] * 3 + [_d] * 4
                         + [_i] * 4 + [_u, _p, _d, _p, _p]),
@@ -59,6 +60,7 @@ SIGNATURES = {
     "vpfv_higher_moments": (_i, [_p, _i, _i, _p, _p, _p, _d, _d, _p, _p]),
     "vpfv_richardson_partials": (_i, [_p, _p, _i, _p, _p, _i, _p]),
     "vpfv_scale": (_i, [_p, _d, ctypes.c_longlong, _p]),
+    "vpfv_field_1d": (_i, [_p, _p, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
     "vpfv_poisson_1d": (_i, [_p, _p, _p, _i, _p, _p, _p, _p]),
     "vpfv_poisson_2d": (_i, [_p] * 4 + [_i, _i] + [_p] * 7 + [_p]),
@@ -134,6 +136,10 @@ def int_array(vals):
 
 def ll_array(vals):
     return (ctypes.c_longlong * len(vals))(*[int(v) for v in vals])
+
+
+def ptr_array(vals):
+    return (ctypes.c_void_p * len(vals))(*[int(v) if v else None for v in vals])
 
 
 def dbl_array(vals):

@@ -3,6 +3,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "field.cuh"
 
 namespace vpfv {
 
@@ -31,10 +32,7 @@ __global__ void tables1d_kernel(const double *__restrict__ E, double *__restrict
                                 double den1) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double Ei = E[i];
-    const double dE = __dsub_rn(E[i + 1 < n ? i + 1 : 0], E[i > 0 ? i - 1 : n - 1]);
-    e[i] = __dadd_rn(__dmul_rn(qmk2, Ei), g);
-    c1[i] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, dE), den1));
+    table1d_row(E, i, n, qmk2, g, t1, den1, e[i], c1[i]);
 }
 
 __global__ void tables2d_kernel(const double *__restrict__ Ex, const double *__restrict__ Ey,
@@ -67,10 +65,8 @@ __global__ void tables1d_packed_kernel(const double *__restrict__ E, double *__r
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n + 2) return;
     const int i = r == 0 ? n - 1 : (r == n + 1 ? 0 : r - 1);
-    const double dE = __dsub_rn(E[i + 1 < n ? i + 1 : 0], E[i > 0 ? i - 1 : n - 1]);
     double *o = tab + (size_t)r * 8;
-    o[0] = __dadd_rn(__dmul_rn(qmk2, E[i]), g);
-    o[1] = __dadd_rn(t1, __ddiv_rn(__dmul_rn(qmk2, dE), den1));
+    table1d_row(E, i, n, qmk2, g, t1, den1, o[0], o[1]);
     for (int k = 2; k < 8; ++k) o[k] = 0.0;
 }
 
@@ -103,29 +99,10 @@ __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const doub
 // ---------------------------------------------------------------------------
 // charge density: rho = sum_s q_s n_s - mean (one CTA, fixed-order sums)
 
-struct Charges {
-    double q[8];
-};
-
 __global__ void charge_kernel(const double *__restrict__ n, Charges q, int ns, int nphys,
                               double *__restrict__ rho) {
     __shared__ double part[1024];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    double acc = 0.0;
-    for (int p = tid; p < nphys; p += nt) {
-        double r = __dmul_rn(q.q[0], n[p]);
-        for (int s = 1; s < ns; ++s) r = __dadd_rn(r, __dmul_rn(q.q[s], n[(long long)s * nphys + p]));
-        rho[p] = r;
-        acc = __dadd_rn(acc, r);
-    }
-    part[tid] = acc;
-    __syncthreads();
-    for (int w = 1; w < nt; w <<= 1) {  // adjacent-pair tree over thread partials
-        if ((tid % (2 * w)) == 0 && tid + w < nt) part[tid] = __dadd_rn(part[tid], part[tid + w]);
-        __syncthreads();
-    }
-    const double mean = __ddiv_rn(part[0], (double)nphys);
-    for (int p = tid; p < nphys; p += nt) rho[p] = __dsub_rn(rho[p], mean);
+    charge_block(n, q, ns, nphys, rho, part);
 }
 
 // ---------------------------------------------------------------------------

@@ -11,6 +11,7 @@
 // 1D: one CTA does the whole solve.  2D: row pass -> column pass (with the
 // spectral multiply and both inverse column transforms) -> inverse row pass.
 #include "common.cuh"
+#include "field.cuh"
 
 namespace vpfv {
 
@@ -69,11 +70,10 @@ __device__ __forceinline__ void put(double2 *a, double2 *tmp, int m, double2 v, 
 // ---------------------------------------------------------------------------
 // 1D: single CTA
 
-__global__ void poisson1d_kernel(const double *__restrict__ rho, double *__restrict__ Ex,
-                                 double *__restrict__ phi, int n, const double2 *__restrict__ tw,
-                                 const double *__restrict__ k2, const double *__restrict__ kd,
-                                 int pow2, int logn) {
-    extern __shared__ double2 sm2[];
+// the 1D solve by one CTA; sm2 holds 3 n double2
+__device__ void poisson1d_block(const double *__restrict__ rho, double *__restrict__ Ex, double *__restrict__ phi,
+                                int n, const double2 *__restrict__ tw, const double *__restrict__ k2,
+                                const double *__restrict__ kd, int pow2, int logn, double2 *sm2) {
     double2 *a = sm2, *tmp = sm2 + n, *ph = sm2 + 2 * n;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int m = tid; m < n; m += nt) put(a, tmp, m, make_double2(rho[m], 0.0), pow2, logn);
@@ -98,6 +98,73 @@ __global__ void poisson1d_kernel(const double *__restrict__ rho, double *__restr
         double *out = pass == 0 ? phi : Ex;
         for (int m = tid; m < n; m += nt) out[m] = a[m].x * inv;
         __syncthreads();
+    }
+}
+
+__global__ void poisson1d_kernel(const double *__restrict__ rho, double *__restrict__ Ex,
+                                 double *__restrict__ phi, int n, const double2 *__restrict__ tw,
+                                 const double *__restrict__ k2, const double *__restrict__ kd,
+                                 int pow2, int logn) {
+    extern __shared__ double2 sm2[];
+    poisson1d_block(rho, Ex, phi, n, tw, k2, kd, pow2, logn, sm2);
+}
+
+// The whole 1D field chain of a stage in one CTA (the per-stage
+// "moments -> charge -> Poisson -> tables" of Simulation._stage,
+// runner.py:183-191): rho from the species densities, the spectral solve,
+// then every species' line tables (plain e/c1 or the packed rows of the
+// tiled 1D-2V kernel) -- bitwise the separate charge / Poisson / tables
+// kernels, whose block-level code it shares (field.cuh).
+struct Tables1D {
+    int ns;
+    const double *part[8];  // moment partials [Nx][rows][chunks] of each species, or none (n given)
+    int rows[8], chunks[8];
+    double vol[8];
+    double *e[8], *c1[8], *packed[8];
+    double qmk2[8], g[8], t1[8], den1[8];
+    int corrections[8];
+};
+
+__global__ void field1d_kernel(double *__restrict__ n, Charges q, int ns, int nx, double *__restrict__ rho,
+                               double *__restrict__ Ex, const double2 *__restrict__ tw,
+                               const double *__restrict__ k2, const double *__restrict__ kd, int pow2, int logn,
+                               Tables1D T) {
+    extern __shared__ double2 sm2[];
+    if (T.part[0]) {  // n_s from the last stage's fused moment partials (vpfv_moment_partials)
+        const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int s = 0; s < T.ns; ++s) {
+            double *bufA = reinterpret_cast<double *>(sm2) + (size_t)warp * 2 * T.rows[s];
+            for (int p = warp; p < nx; p += nw) {
+                const double x = moment_cell_warp(T.part[s] + (size_t)p * T.rows[s] * T.chunks[s], T.rows[s],
+                                                  T.chunks[s], bufA, bufA + T.rows[s]);
+                if ((threadIdx.x & 31) == 0) n[(size_t)s * nx + p] = __dmul_rn(x, T.vol[s]);
+            }
+        }
+        __syncthreads();
+    }
+    double *part = reinterpret_cast<double *>(sm2 + 3 * nx);
+    charge_block(n, q, ns, nx, rho, part);
+    __syncthreads();
+    poisson1d_block(rho, Ex, nullptr, nx, tw, k2, kd, pow2, logn, sm2);
+    for (int s = 0; s < T.ns; ++s) {
+        if (T.packed[s]) {
+            for (int r = threadIdx.x; r < nx + 2; r += blockDim.x) {  // rows shifted by one, periodic ghosts
+                const int i = r == 0 ? nx - 1 : (r == nx + 1 ? 0 : r - 1);
+                double *o = T.packed[s] + (size_t)r * 8;
+                double e, c1;
+                table1d_row(Ex, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
+                o[0] = e;
+                o[1] = T.corrections[s] ? c1 : 0.0;
+                for (int k = 2; k < 8; ++k) o[k] = 0.0;
+            }
+        } else {
+            for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+                double e, c1;
+                table1d_row(Ex, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
+                T.e[s][i] = e;
+                T.c1[s][i] = T.corrections[s] ? c1 : 0.0;
+            }
+        }
     }
 }
 
@@ -204,6 +271,51 @@ extern "C" int vpfv_poisson_1d(const double *rho, double *Ex, double *phi, int N
     poisson1d_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(
         rho, Ex, phi, N, (const double2 *)tw, k2, kd, logn >= 0, logn < 0 ? 0 : logn);
     return check_launch("poisson_1d");
+}
+
+extern "C" int vpfv_field_1d(const double *const *partials, const int *rows, const int *chunks, const double *vols,
+                             double *n, const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
+                             const double *tw, const double *k2, const double *kd, double *const *e,
+                             double *const *c1, double *const *packed, const double *qmk2, const double *g,
+                             const double *t1, const double *den1, const int *corrections, void *stream) {
+    if (nspecies < 1 || nspecies > 8) return set_error(VPFV_EARG, "field_1d: 1..8 species");
+    if (Nx < 2) return set_error(VPFV_EARG, "field_1d: Nx < 2");
+    const int logn = ilog2_if_pow2(Nx);
+    size_t smem = sizeof(double2) * 3 * (size_t)Nx + sizeof(double) * 1024;
+    for (int s = 0; partials && s < nspecies; ++s) {
+        if (!partials[s] || rows[s] < 1 || chunks[s] < 1 || chunks[s] > 16)
+            return set_error(VPFV_EARG, "field_1d: bad moment partials");
+        const size_t fin = sizeof(double) * 32 * 2 * (size_t)rows[s];
+        if (fin > smem) smem = fin;
+    }
+    if (smem > 200 * 1024) return set_error(VPFV_EARG, "field_1d: Nx too large for one CTA");
+    static bool once = false;
+    if (!once) {
+        allow_smem((const void *)field1d_kernel);
+        once = true;
+    }
+    Charges q;
+    Tables1D T{};
+    T.ns = nspecies;
+    for (int s = 0; s < 8; ++s) q.q[s] = s < nspecies ? q_host[s] : 0.0;
+    for (int s = 0; s < nspecies; ++s) {
+        T.part[s] = partials ? partials[s] : nullptr;
+        T.rows[s] = partials ? rows[s] : 0;
+        T.chunks[s] = partials ? chunks[s] : 0;
+        T.vol[s] = partials ? vols[s] : 0.0;
+        T.e[s] = e ? e[s] : nullptr;
+        T.c1[s] = c1 ? c1[s] : nullptr;
+        T.packed[s] = packed ? packed[s] : nullptr;
+        T.qmk2[s] = qmk2[s];
+        T.g[s] = g[s];
+        T.t1[s] = t1[s];
+        T.den1[s] = den1[s];
+        T.corrections[s] = corrections[s];
+        if (!T.packed[s] && !(T.e[s] && T.c1[s])) return set_error(VPFV_EARG, "field_1d: no table outputs");
+    }
+    field1d_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, (const double2 *)tw, k2,
+                                                           kd, logn >= 0, logn < 0 ? 0 : logn, T);
+    return check_launch("field_1d");
 }
 
 extern "C" int vpfv_poisson_2d(const double *rho, double *Ex, double *Ey, double *phi, int Nx,

@@ -134,8 +134,8 @@ struct Update {
 };
 
 template <bool EXACT>
-__device__ __forceinline__ void finish(const Update &u, const double *src, long long c, double rhs,
-                                       unsigned long long flat) {
+__device__ __forceinline__ double finish(const Update &u, const double *src, long long c, double rhs,
+                                         unsigned long long flat) {
     double cL = u.dt_dev ? __ddiv_rn(*u.dt_dev, u.cL_div) : u.cL;
     double s0 = 0.0;
     if (u.a_is_src || u.b_is_src) s0 = ldg(src + c);
@@ -155,6 +155,7 @@ __device__ __forceinline__ void finish(const Update &u, const double *src, long 
     }
     u.dest[c] = out;
     if (u.nonfinite && !isfinite(out)) atomicMin(u.nonfinite, flat);
+    return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -165,9 +166,14 @@ struct T11 {
     double hx, hv, mhx, mhv;
 };
 
+// partials (fast path, Nv % 128 == 0, 128-thread blocks): the fold-tree
+// subtree sum of the new dest over each aligned 128-wide v chunk
+// (fields.py:28-47: shuffle levels 1-5, then the 4 warp sums pairwise),
+// partials[i][0][chunk] -- finished by vpfv_moment_partials(nvx = 1).
 template <bool EXACT>
 __global__ void __launch_bounds__(256) stage_1d1v_kernel(Update u, const double *__restrict__ src,
-                                                         T11 t, int Nx, int Nv, unsigned wrap) {
+                                                         T11 t, int Nx, int Nv, unsigned wrap,
+                                                         double *__restrict__ partials) {
     const int i = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Nv) return;
@@ -178,7 +184,17 @@ __global__ void __launch_bounds__(256) stage_1d1v_kernel(Update u, const double 
     double rhs = flux_first<EXACT>(src, c, X, a_x, t.hx, t.mhx);
     rhs = flux_next<EXACT>(rhs, src, c, V, a_v, t.hv, t.mhv);
     rhs = corr_add<EXACT>(rhs, c1, diag<EXACT>(src, c, X, V));
-    finish<EXACT>(u, src, c, rhs, (unsigned long long)i * Nv + j);
+    double out = finish<EXACT>(u, src, c, rhs, (unsigned long long)i * Nv + j);
+    if (!EXACT && partials) {
+        __shared__ double wsum[4];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) out = __dadd_rn(out, __shfl_xor_sync(0xffffffffu, out, off));
+        if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = out;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            partials[(long long)i * gridDim.x + blockIdx.x] =
+                __dadd_rn(__dadd_rn(wsum[0], wsum[1]), __dadd_rn(wsum[2], wsum[3]));
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -301,10 +317,28 @@ extern "C" int vpfv_stage_1d1v(double *dest, const double *A, const double *B, c
     dim3 block(128), grid((Nv + 127) / 128, Nx);
     cudaStream_t s = (cudaStream_t)stream;
     if (flags & VPFV_EXACT)
-        stage_1d1v_kernel<true><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags);
+        stage_1d1v_kernel<true><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags, nullptr);
     else
-        stage_1d1v_kernel<false><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags);
+        stage_1d1v_kernel<false><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags, nullptr);
     return check_launch("stage_1d1v");
+}
+
+extern "C" int vpfv_stage_1d1v_fused(double *dest, const double *A, const double *B, const double *src,
+                                     double ca, double cb, double cd, double cL, const double *ax,
+                                     const double *avx, const double *c1, double hx, double hv, int Nx,
+                                     int Nv, unsigned flags, const double *dt_dev, double cL_div,
+                                     unsigned long long *nonfinite, double *moment_partials, void *stream) {
+    if (!moment_partials)
+        return vpfv_stage_1d1v(dest, A, B, src, ca, cb, cd, cL, ax, avx, c1, hx, hv, Nx, Nv, flags, dt_dev, cL_div,
+                               nonfinite, stream);
+    if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
+    if ((flags & VPFV_EXACT) || Nv % 128 || Nx < 1)
+        return set_error(VPFV_EARG, "1D-1V moment partials need the fast path and Nv % 128 == 0");
+    Update u = make_update(dest, A, B, src, ca, cb, cd, cL, dt_dev, cL_div, nonfinite);
+    T11 t{ax, avx, c1, hx, hv, -1.0 / (60.0 * hx), -1.0 / (60.0 * hv)};
+    dim3 block(128), grid(Nv / 128, Nx);
+    stage_1d1v_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(u, src, t, Nx, Nv, flags, moment_partials);
+    return check_launch("stage_1d1v_fused");
 }
 
 extern "C" int vpfv_stage_1d2v(double *dest, const double *A, const double *B, const double *src,

@@ -46,6 +46,7 @@
 
 #include "common.cuh"
 #include "tma.cuh"
+#include "field.cuh"
 
 namespace vpfv {
 
@@ -598,48 +599,16 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
 // moment from partials: per physical cell, fold over the vy chunks of every
 // vx row (chunk sums are exact subtrees), then over vx, times vol.
 
-__device__ double fold_small(double *x, int n) {  // single thread, in place
-    while (n > 1) {
-        int m = n >> 1;
-        for (int t = 0; t < m; ++t) x[t] = __dadd_rn(x[2 * t], x[2 * t + 1]);
-        if (n & 1) {
-            x[m] = x[n - 1];
-            n = m + 1;
-        } else {
-            n = m;
-        }
-    }
-    return x[0];
-}
-
 __global__ void moment_partials_kernel(const double *__restrict__ part, double *__restrict__ n,
                                        int nphys, int nvx, int nlt, double vol) {
     extern __shared__ double sm[];  // per warp: two buffers of nvx
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const int p = blockIdx.x * wpb + warp;
     if (p >= nphys) return;
-    double *bufA = sm + (size_t)warp * 2 * nvx, *bufB = bufA + nvx;
-    const double *src = part + (size_t)p * nvx * nlt;
-    for (int k = lane; k < nvx; k += 32) {
-        double tmp[16];
-        for (int t = 0; t < nlt; ++t) tmp[t] = src[(size_t)k * nlt + t];
-        bufA[k] = fold_small(tmp, nlt);
-    }
-    __syncwarp();
-    int len = nvx;
-    double *a = bufA, *b = bufB;
-    while (len > 1) {
-        const int m = len >> 1;
-        for (int t = lane; t < m; t += 32) b[t] = __dadd_rn(a[2 * t], a[2 * t + 1]);
-        if ((len & 1) && lane == 0) b[m] = a[len - 1];
-        __syncwarp();
-        len = m + (len & 1);
-        double *tmp = a;
-        a = b;
-        b = tmp;
-    }
-    if (lane == 0) n[p] = __dmul_rn(a[0], vol);
+    double *bufA = sm + (size_t)warp * 2 * nvx;
+    const double x = moment_cell_warp(part + (size_t)p * nvx * nlt, nvx, nlt, bufA, bufA + nvx);
+    if ((threadIdx.x & 31) == 0) n[p] = __dmul_rn(x, vol);
 }
 
 // Fast path for power-of-two Nvx (32..256) and chunk counts (1..16): one warp

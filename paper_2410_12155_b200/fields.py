@@ -82,7 +82,47 @@ class FieldSolver:
             self.kx, self.ky, self.kxd, self.kyd = dev(kx), dev(ky), dev(kxd), dev(kyd)
             self.scratch = torch.empty(8 * self.nphys, **f64)
 
+        self._field1d_args = {}
+
     # ------------------------------------------------------------------
+    def field_1d_ok(self, partial_rows=()):
+        """The fused 1D chain fits one CTA (poisson.cu vpfv_field_1d)."""
+        if self.d != 1 or len(self.species) > 8:
+            return False
+        smem = 48 * self.phys_shape[0] + 8 * 1024
+        return max([smem] + [512 * r for r in partial_rows]) <= 200 * 1024
+
+    def field_and_tables_1d(self, tables, packed, partials=None, stream=None):
+        """Moments-from-partials (when given) -> rho -> Ex -> every species'
+        line tables in one launch (vpfv_field_1d), bitwise the chain
+        moments_from_partials / charge / poisson / StageTables.update.
+        ``packed[s]``: species s gets the packed rows (1D-2V tiled kernel)."""
+        stream = stream_handle(self.device) if stream is None else stream
+        key = (tuple(id(t) for t in tables), tuple(packed),
+               None if partials is None else tuple(p.data_ptr() for p in partials))
+        args = self._field1d_args.get(key)
+        if args is None:
+            S = len(tables)
+            pk = [bool(packed[s]) and tables[s].grid.v == 2 for s in range(S)]
+            if partials is None:
+                part = (None, None, None, None)
+            else:
+                part = (_lib.ptr_array([p.data_ptr() for p in partials]),
+                        _lib.int_array([p.shape[-2] for p in partials]),
+                        _lib.int_array([p.shape[-1] for p in partials]), _lib.dbl_array(self.vols))
+            args = part + (
+                self.n.data_ptr(), self.q_host, S, self.phys_shape[0], self.rho.data_ptr(),
+                self.E["Ex"].data_ptr(), self.tw.data_ptr(), self.k2.data_ptr(), self.kd.data_ptr(),
+                _lib.ptr_array([0 if pk[s] else t.e.data_ptr() for s, t in enumerate(tables)]),
+                _lib.ptr_array([0 if pk[s] else t.c1.data_ptr() for s, t in enumerate(tables)]),
+                _lib.ptr_array([t.packed.data_ptr() if pk[s] else 0 for s, t in enumerate(tables)]),
+                _lib.dbl_array([t.qmk2 for t in tables]), _lib.dbl_array([t.gx for t in tables]),
+                _lib.dbl_array([t.t1 for t in tables]), _lib.dbl_array([t.den1 for t in tables]),
+                _lib.int_array([1 if t.corrections else 0 for t in tables]))
+            self._field1d_args[key] = args
+        _lib.call("vpfv_field_1d", *args, stream)
+        return self.E
+
     def moments(self, srcs, stream=None):
         stream = stream_handle(self.device) if stream is None else stream
         for s, (g, f) in enumerate(zip(self.grids, srcs)):
@@ -97,7 +137,7 @@ class FieldSolver:
             if part is None:
                 raise ValueError("species without fused moment partials")
             _lib.call("vpfv_moment_partials", part.data_ptr(), self.n[s].data_ptr(), self.nphys,
-                      g.N[g.d], part.shape[-1], self.vols[s], stream)
+                      part.shape[-2], part.shape[-1], self.vols[s], stream)  # partials [phys][rows][chunks]
         return self.n
 
     def solve_from_partials(self, partials, stream=None):

@@ -91,6 +91,8 @@ class StageTables:
         g = self.grid
         if flags & _lib.VPFV_EXACT:
             return False
+        if (g.d, g.v) == (1, 1):
+            return g.N[1] % 128 == 0
         if (g.d, g.v) == (2, 2):
             return bool(_lib.load().vpfv_stage_2d2v_tiled_ok(*g.N, flags))
         if (g.d, g.v) == (1, 2):
@@ -101,6 +103,8 @@ class StageTables:
         g = self.grid
         if (g.d, g.v) == (2, 2):
             return (g.N[0], g.N[1], g.N[2], g.N[3] // _lib.load().vpfv_stage_2d2v_partials_chunk())
+        if (g.d, g.v) == (1, 1):
+            return (g.N[0], 1, g.N[1] // 128)
         return (g.N[0], g.N[1], g.N[2] // _lib.load().vpfv_stage_1d2v_partials_chunk())
 
     # -- per-stage tables from E (device arrays on the physical grid) ---------
@@ -110,7 +114,7 @@ class StageTables:
         g = self.grid
         if g.d == 1:
             Ex = E["Ex"]
-            if packed:
+            if packed and g.v == 2:  # the 1D-1V kernels read the plain tables
                 _lib.call("vpfv_tables_1d_packed", Ex.data_ptr(), self.packed.data_ptr(), g.N[0],
                           self.qmk2, self.gx, self.t1, self.den1, stream)
                 if not self.corrections:
@@ -144,8 +148,13 @@ class StageTables:
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
                 float(ca), float(cb), float(cd), float(cL))
         if (g.d, g.v) == (1, 1):
-            _lib.call("vpfv_stage_1d1v", *head, self.ax.data_ptr(), self.e.data_ptr(),
-                      self.c1.data_ptr(), h[0], h[1], N[0], N[1], *common_tail)
+            if partials is not None:
+                _lib.call("vpfv_stage_1d1v_fused", *head, self.ax.data_ptr(), self.e.data_ptr(),
+                          self.c1.data_ptr(), h[0], h[1], N[0], N[1], flags, _ptr(dt_dev), float(cL_div),
+                          _ptr(nonfinite), partials.data_ptr(), stream)
+            else:
+                _lib.call("vpfv_stage_1d1v", *head, self.ax.data_ptr(), self.e.data_ptr(),
+                          self.c1.data_ptr(), h[0], h[1], N[0], N[1], *common_tail)
         elif (g.d, g.v) == (1, 2):
             args = (*head, self.vxc.data_ptr(), self.vyc.data_ptr(), self.e.data_ptr(),
                     self.avy.data_ptr(), self.c1.data_ptr(), self.c2, h[0], h[1], h[2], N[0], N[1], N[2])

@@ -329,8 +329,12 @@ class _LocalTables:
         head = (dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
                 float(ca), float(cb), float(cd), float(cL))
         if (g.d, g.v) == (1, 1):
-            _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr() + vo, ptr(t.e), ptr(t.c1), h[0], h[1],
-                      N[0], N[1], *tail, stream)
+            if partials is not None:
+                _lib.call("vpfv_stage_1d1v_fused", *head, t.ax.data_ptr() + vo, ptr(t.e), ptr(t.c1), h[0], h[1],
+                          N[0], N[1], *tail, partials.data_ptr(), stream)
+            else:
+                _lib.call("vpfv_stage_1d1v", *head, t.ax.data_ptr() + vo, ptr(t.e), ptr(t.c1), h[0], h[1],
+                          N[0], N[1], *tail, stream)
         elif (g.d, g.v) == (1, 2):
             args = (*head, t.vxc.data_ptr() + vo, t.vyc.data_ptr(), ptr(t.e), t.avy.data_ptr() + vo, ptr(t.c1),
                     t.c2, h[0], h[1], h[2], N[0], N[1], N[2])
@@ -444,7 +448,8 @@ class DistributedSimulation:
         for s, (lg, f) in enumerate(zip(self.lgrids, srcs)):
             if from_partials:
                 _lib.call("vpfv_moment_partials", self.partials[s].data_ptr(), self.n_local[s].data_ptr(),
-                          int(np.prod(lg.N[:lg.d])), lg.N[lg.d], self.partials[s].shape[-1], 1.0, stream)
+                          int(np.prod(lg.N[:lg.d])), self.partials[s].shape[-2], self.partials[s].shape[-1], 1.0,
+                          stream)
             else:
                 _lib.call("vpfv_moment", f.data_ptr(), self.n_local[s].data_ptr(), lg.d, lg.v,
                           self._N_arrays[s], 1.0, stream)

@@ -20,6 +20,7 @@ epilogue flag, read back once per step, with the reference's rollback.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -111,6 +112,10 @@ class Simulation:
         self.partials = mk()       # written by stages 1-3, read by stages 2-4
         self.partials_next = mk()  # written by stage 4 (moment of the new f0), read by the next stage 1
         self._moment_of = None  # (data_ptr, _version) of the f0 arrays the partials describe
+        # d = 1: moments-from-partials, rho, Ex and every species' tables in
+        # one single-CTA launch per stage instead of 2 + 2S small ones
+        rows = [t.partials_shape()[-2] for t in self.tables] if self.fuse_moment else []
+        self.fuse_field = self.fields.field_1d_ok(rows) and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
         self._side = [torch.cuda.Stream(self.device) for _ in self.species[1:]]  # concurrent species
         self._diag = None
         self._last_E = None
@@ -136,7 +141,14 @@ class Simulation:
         stream = stream_handle(self.device)
         use_partials = self.fuse_moment and slot is not None and (slot > 0 or cached)
         emit_partials = self.fuse_moment and slot is not None and (slot < 3 or emit_last)
-        if use_partials:
+        if self.fuse_field:
+            if use_partials:
+                part = self.partials if slot > 0 else self.partials_next
+            else:
+                part = None
+                self.fields.moments(src, stream)
+            E = self.fields.field_and_tables_1d(self.tables, self.tiled, part, stream=stream)
+        elif use_partials:
             E = self.fields.solve_from_partials(self.partials if slot > 0 else self.partials_next, stream=stream)
         else:
             E = self.fields.solve(src, stream=stream)
@@ -153,7 +165,8 @@ class Simulation:
                 forked.append(side)
             with torch.cuda.stream(side if side is not None else main):
                 st = stream_handle(self.device)
-                tab.update(E, st, packed=self.tiled[s])
+                if not self.fuse_field:
+                    tab.update(E, st, packed=self.tiled[s])
                 nf = None if slot is None else self.nonfinite[slot, s:s + 1]
                 timed = self._timing and slot is not None
                 if timed:

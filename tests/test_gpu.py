@@ -690,3 +690,70 @@ def test_convergence_ladder_fourth_order(tmp_path):
     assert orders[-1] > 3.5, orders
     lines = (tmp_path / "c.csv").read_text().strip().split("\n")
     assert lines[0] == "N,error,observed_order" and len(lines) == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [(16, 128), (12, 384)])
+def test_1d1v_fused_moment_partials_fold_tree(N):
+    """vpfv_stage_1d1v_fused: the stage output equals vpfv_stage_1d1v and the
+    partials fold to the reference fold-tree moment of the new dest bitwise."""
+    g = O.Grid(1, 1, N, (0.0, -6.0), (2 * np.pi, 6.0), (True, False))
+    rng = np.random.default_rng(sum(N))
+    src = 1.0 + 0.3 * rng.random(g.padded_shape)
+    O.fill_ghosts(src, g, O.capture_frozen(src, g))
+    E = {"Ex": 0.2 * np.sin(g.centers(0))}
+    sp = O.Species("e", -1.0, 1.0, 1.0, 0.0, 0.0, (0.0, 0.0))
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({"Ex": dev(E["Ex"])}, stream)
+    flags = K.wrap_flags(pg)
+    assert tab.fused_moment_ok(flags)
+    d_src = dev(src)
+    plain, fused = torch.zeros_like(d_src), torch.zeros_like(d_src)
+    part = torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda")
+    tab.launch(plain, d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream)
+    tab.launch(fused, d_src, d_src, d_src, 1.0, 0.0, 0.0, 0.02, flags, stream, partials=part)
+    assert torch.equal(plain, fused)
+    n = torch.empty(N[0], dtype=torch.float64, device="cuda")
+    _lib.call("vpfv_moment_partials", part.data_ptr(), n.data_ptr(), N[0], 1, part.shape[-1],
+              O.velocity_volume(g), stream)
+    assert np.array_equal(n.cpu().numpy(), O.zeroth_moment(fused.cpu().numpy(), g))
+
+
+@pytest.mark.parametrize("problem,N,Nv", [("two-stream", 16, 16), ("two-stream", 32, 128), ("lhdi", 8, 8),
+                                          ("lhdi", 16, 32), ("dgh", 16, 32), ("weibel", 16, 32)])
+def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
+    """vpfv_field_1d (moments-from-partials + charge + Poisson + every
+    species' tables in one CTA) reproduces the separate launches bitwise over
+    a few steps, with and without the fused moment partials."""
+    def run(split):
+        monkeypatch.setenv("VPFV_FIELD_SPLIT", "1" if split else "0")
+        sim = R.Simulation(P.make_problem(P.ProblemSpec(problem), N, Nv), dt=1e-3)
+        assert sim.fuse_field is (not split)
+        for _ in range(3):
+            sim.advance(1e-3)
+        return sim
+    a, b = run(False), run(True)
+    for x, y in zip(a.interiors(), b.interiors()):
+        assert np.array_equal(x, y)
+    assert torch.equal(a.fields.E["Ex"], b.fields.E["Ex"])
+    for ta, tb, tiled in zip(a.tables, b.tables, a.tiled):
+        if tiled and ta.grid.v == 2:
+            assert torch.equal(ta.packed, tb.packed)
+        else:
+            assert torch.equal(ta.e, tb.e) and torch.equal(ta.c1, tb.c1)
+
+
+def test_fused_field_1d_corrections_off(monkeypatch):
+    """corrections=False zeroes c1 in the fused tables too."""
+    out = []
+    for split in (False, True):
+        monkeypatch.setenv("VPFV_FIELD_SPLIT", "1" if split else "0")
+        sim = R.Simulation(P.make_problem(P.ProblemSpec("dgh"), 16, 32), dt=1e-3, corrections=False)
+        sim.advance(1e-3)
+        out.append(sim)
+    assert torch.equal(out[0].tables[0].packed, out[1].tables[0].packed)
+    assert float(out[0].tables[0].packed[:, 1].abs().max()) == 0.0
+    assert np.array_equal(out[0].interiors()[0], out[1].interiors()[0])
