@@ -133,6 +133,14 @@ __global__ void field1d_kernel(double *__restrict__ n, Charges q, int ns, int nx
     if (T.part[0]) {  // n_s from the last stage's fused moment partials (vpfv_moment_partials)
         const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
         for (int s = 0; s < T.ns; ++s) {
+            if (T.rows[s] == 1) {  // 1D-1V: one thread per cell folds its chunks
+                for (int p = threadIdx.x; p < nx; p += blockDim.x) {
+                    double tmp[16];
+                    for (int t = 0; t < T.chunks[s]; ++t) tmp[t] = T.part[s][(size_t)p * T.chunks[s] + t];
+                    n[(size_t)s * nx + p] = __dmul_rn(fold_small(tmp, T.chunks[s]), T.vol[s]);
+                }
+                continue;
+            }
             double *bufA = reinterpret_cast<double *>(sm2) + (size_t)warp * 2 * T.rows[s];
             for (int p = warp; p < nx; p += nw) {
                 const double x = moment_cell_warp(T.part[s] + (size_t)p * T.rows[s] * T.chunks[s], T.rows[s],

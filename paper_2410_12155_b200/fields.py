@@ -85,12 +85,21 @@ class FieldSolver:
         self._field1d_args = {}
 
     # ------------------------------------------------------------------
-    def field_1d_ok(self, partial_rows=()):
+    def field_1d_ok(self):
         """The fused 1D chain fits one CTA (poisson.cu vpfv_field_1d)."""
-        if self.d != 1 or len(self.species) > 8:
+        return self.d == 1 and len(self.species) <= 8 and 48 * self.phys_shape[0] + 8 * 1024 <= 200 * 1024
+
+    def finish_in_field_1d(self, partial_shapes):
+        """Fold the moment partials inside vpfv_field_1d too?  Only when they
+        are small (one CTA reads them all): 1D-1V rows, or a few thousand
+        doubles -- a 1D-2V 256^3 run's 8 MB of partials stay with the
+        grid-wide vpfv_moment_partials."""
+        if not partial_shapes:
             return False
-        smem = 48 * self.phys_shape[0] + 8 * 1024
-        return max([smem] + [512 * r for r in partial_rows]) <= 200 * 1024
+        if all(sh[-2] == 1 for sh in partial_shapes):
+            return True
+        total = sum(int(np.prod(sh)) for sh in partial_shapes)
+        return total <= 32768 and max(512 * sh[-2] for sh in partial_shapes) <= 200 * 1024
 
     def field_and_tables_1d(self, tables, packed, partials=None, stream=None):
         """Moments-from-partials (when given) -> rho -> Ex -> every species'

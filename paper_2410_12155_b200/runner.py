@@ -114,8 +114,9 @@ class Simulation:
         self._moment_of = None  # (data_ptr, _version) of the f0 arrays the partials describe
         # d = 1: moments-from-partials, rho, Ex and every species' tables in
         # one single-CTA launch per stage instead of 2 + 2S small ones
-        rows = [t.partials_shape()[-2] for t in self.tables] if self.fuse_moment else []
-        self.fuse_field = self.fields.field_1d_ok(rows) and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
+        self.fuse_field = self.fields.field_1d_ok() and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
+        self._finish_in_field = self.fuse_moment and self.fields.finish_in_field_1d(
+            [t.partials_shape() for t in self.tables])
         self._side = [torch.cuda.Stream(self.device) for _ in self.species[1:]]  # concurrent species
         self._diag = None
         self._last_E = None
@@ -144,6 +145,9 @@ class Simulation:
         if self.fuse_field:
             if use_partials:
                 part = self.partials if slot > 0 else self.partials_next
+                if not self._finish_in_field:
+                    self.fields.moments_from_partials(part, stream)
+                    part = None
             else:
                 part = None
                 self.fields.moments(src, stream)

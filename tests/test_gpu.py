@@ -723,7 +723,8 @@ def test_1d1v_fused_moment_partials_fold_tree(N):
 
 
 @pytest.mark.parametrize("problem,N,Nv", [("two-stream", 16, 16), ("two-stream", 32, 128), ("lhdi", 8, 8),
-                                          ("lhdi", 16, 32), ("dgh", 16, 32), ("weibel", 16, 32)])
+                                          ("lhdi", 16, 32), ("dgh", 16, 32), ("weibel", 16, 32),
+                                          ("dgh", 64, 128)])
 def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
     """vpfv_field_1d (moments-from-partials + charge + Poisson + every
     species' tables in one CTA) reproduces the separate launches bitwise over
@@ -732,6 +733,8 @@ def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
         monkeypatch.setenv("VPFV_FIELD_SPLIT", "1" if split else "0")
         sim = R.Simulation(P.make_problem(P.ProblemSpec(problem), N, Nv), dt=1e-3)
         assert sim.fuse_field is (not split)
+        if problem == "dgh" and N == 64:
+            assert not sim._finish_in_field  # large partials keep the grid-wide finish
         for _ in range(3):
             sim.advance(1e-3)
         return sim
