@@ -219,7 +219,8 @@ int vpfv_scale(double *x, double a, long long n, void *stream);
  * packed[s] rows (vpfv_tables_1d_packed) when packed[s] != NULL, with c1 = 0
  * when corrections[s] == 0.  Bitwise the separate charge / Poisson / tables
  * calls (shared block-level code); replaces three launches per stage of
- * Simulation._stage (runner.py:183-191) for d = 1. */
+ * Simulation._stage (runner.py:183-191) for d = 1.  Nx <= vpfv_field_1d_max_cells(). */
+int vpfv_field_1d_max_cells(void);
 int vpfv_field_1d(const double *const *partials, const int *rows, const int *chunks, const double *vols,
                   double *n, const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
                   const double *tw, const double *k2, const double *kd, double *const *e,

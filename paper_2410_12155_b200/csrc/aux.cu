@@ -101,8 +101,8 @@ __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const doub
 
 __global__ void charge_kernel(const double *__restrict__ n, Charges q, int ns, int nphys,
                               double *__restrict__ rho) {
-    __shared__ double part[1024];
-    charge_block(n, q, ns, nphys, rho, part);
+    __shared__ double red[32];
+    charge_block(n, q, ns, nphys, rho, red);
 }
 
 // ---------------------------------------------------------------------------

@@ -27,6 +27,44 @@ __device__ __forceinline__ double fold_small(double *x, int n) {  // single thre
     return x[0];
 }
 
+// fold_small of C = 2^k contiguous values in registers (128-bit loads):
+// the same adjacent-pair tree
+template <int C>
+__device__ __forceinline__ double fold_pow2(const double *__restrict__ src) {
+    double x[C];
+    if (C == 1) {
+        x[0] = src[0];
+    } else {
+#pragma unroll
+        for (int t = 0; t < C; t += 2) {
+            const double2 d = *reinterpret_cast<const double2 *>(src + t);
+            x[t] = d.x;
+            x[t + 1] = d.y;
+        }
+    }
+#pragma unroll
+    for (int w = 1; w < C; w <<= 1)
+#pragma unroll
+        for (int t = 0; t < C; t += 2 * w) x[t] = __dadd_rn(x[t], x[t + w]);
+    return x[0];
+}
+
+// fold_small of one row of c (<= 16) chunks; src 16-byte aligned when c is even
+__device__ __forceinline__ double fold_row(const double *__restrict__ src, int c) {
+    switch (c) {
+        case 1: return fold_pow2<1>(src);
+        case 2: return fold_pow2<2>(src);
+        case 4: return fold_pow2<4>(src);
+        case 8: return fold_pow2<8>(src);
+        case 16: return fold_pow2<16>(src);
+        default: {
+            double tmp[16];
+            for (int t = 0; t < c; ++t) tmp[t] = src[t];
+            return fold_small(tmp, c);
+        }
+    }
+}
+
 // one warp folds one physical cell's partials [nvx][nlt] (nlt <= 16) through
 // two smem buffers of nvx doubles; the sum is valid in every lane
 __device__ __forceinline__ double moment_cell_warp(const double *__restrict__ src, int nvx, int nlt, double *bufA,
@@ -55,11 +93,40 @@ __device__ __forceinline__ double moment_cell_warp(const double *__restrict__ sr
     return r;
 }
 
+// Sum of one value per thread over the CTA by the adjacent-pair tree over
+// thread indices (level w adds thread t+w into t for t % 2w == 0, t+w < nt):
+// levels 1..16 by shuffles inside each warp, the rest over the warp sums by
+// warp 0 -- bitwise the smem tree.  blockDim.x a multiple of 32; red: 32
+// doubles of smem.  The result is valid in every thread.
+__device__ __forceinline__ double block_tree_sum(double x, double *red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int w = 1; w < 32; w <<= 1) {
+        const double y = __shfl_down_sync(0xffffffffu, x, w);
+        if ((lane & (2 * w - 1)) == 0) x = __dadd_rn(x, y);
+    }
+    if (lane == 0) red[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        x = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+        for (int w = 1; w < 32; w <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, x, w);
+            if ((lane & (2 * w - 1)) == 0 && lane + w < nw) x = __dadd_rn(x, y);
+        }
+        if (lane == 0) red[0] = x;
+    }
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();  // red may be reused
+    return r;
+}
+
 // rho = sum_s q_s n_s - mean(rho) over nphys cells by one CTA: fixed-order
-// per-thread partials, then an adjacent-pair tree over the threads
-// (charge_density, fields.py:164-169).  part: blockDim.x doubles of smem.
+// per-thread partials, then the adjacent-pair tree over the threads
+// (charge_density, fields.py:164-169).  red: 32 doubles of smem.
 __device__ __forceinline__ void charge_block(const double *__restrict__ n, const Charges &q, int ns, int nphys,
-                                             double *__restrict__ rho, double *part) {
+                                             double *__restrict__ rho, double *red) {
     const int tid = threadIdx.x, nt = blockDim.x;
     double acc = 0.0;
     for (int p = tid; p < nphys; p += nt) {
@@ -68,13 +135,7 @@ __device__ __forceinline__ void charge_block(const double *__restrict__ n, const
         rho[p] = r;
         acc = __dadd_rn(acc, r);
     }
-    part[tid] = acc;
-    __syncthreads();
-    for (int w = 1; w < nt; w <<= 1) {
-        if ((tid % (2 * w)) == 0 && tid + w < nt) part[tid] = __dadd_rn(part[tid], part[tid + w]);
-        __syncthreads();
-    }
-    const double mean = __ddiv_rn(part[0], (double)nphys);
+    const double mean = __ddiv_rn(block_tree_sum(acc, red), (double)nphys);
     for (int p = tid; p < nphys; p += nt) rho[p] = __dsub_rn(rho[p], mean);
 }
 

@@ -15,6 +15,22 @@
 
 namespace vpfv {
 
+#ifdef VPFV_FIELD_PROBE
+__device__ unsigned long long g_field_probe[16];
+#define FIELD_STAMP(k)                                                                  \
+    do {                                                                                \
+        if (threadIdx.x == 0) {                                                         \
+            unsigned long long t_;                                                      \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+            g_field_probe[k] = t_;                                                      \
+        }                                                                               \
+    } while (0)
+#else
+#define FIELD_STAMP(k) \
+    do {               \
+    } while (0)
+#endif
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -26,12 +42,44 @@ __device__ void line_transform(double2 *a, double2 *tmp, int n, const double2 *_
                                bool inverse, bool pow2) {
     const int tid = threadIdx.x, nt = blockDim.x;
     if (pow2) {
-        for (int len = 2; len <= n; len <<= 1) {
-            const int half = len >> 1, step = n / len;
+        // two radix-2 stages (len, 2 len) per pass: one thread carries the 4
+        // points they couple through both -- the same butterflies and
+        // twiddles as stage-by-stage, with half the barriers
+        const int logn = 31 - __clz(n);
+        int lg = 1;  // log2 of the current stage length
+        for (; lg + 1 <= logn; lg += 2) {
+            const int lh = lg - 1, half = 1 << lh;  // stage len = 2 half; next stage len = 4 half
+            for (int j = tid; j < (n >> 2); j += nt) {
+                const int grp = j >> lh, pos = j & (half - 1);
+                const int i0 = (grp << (lh + 2)) + pos;
+                double2 w1 = tw[pos << (logn - lg)];               // w_len^pos
+                double2 w2 = tw[pos << (logn - lg - 1)];           // w_{2len}^pos
+                double2 w3 = tw[(pos + half) << (logn - lg - 1)];  // w_{2len}^{pos+half}
+                if (inverse) {
+                    w1.y = -w1.y;
+                    w2.y = -w2.y;
+                    w3.y = -w3.y;
+                }
+                double2 x0 = a[i0], x1 = a[i0 + half], x2 = a[i0 + 2 * half], x3 = a[i0 + 3 * half];
+                double2 t = cmul(w1, x1);
+                double2 y0 = make_double2(x0.x + t.x, x0.y + t.y), y1 = make_double2(x0.x - t.x, x0.y - t.y);
+                t = cmul(w1, x3);
+                double2 y2 = make_double2(x2.x + t.x, x2.y + t.y), y3 = make_double2(x2.x - t.x, x2.y - t.y);
+                t = cmul(w2, y2);
+                a[i0] = make_double2(y0.x + t.x, y0.y + t.y);
+                a[i0 + 2 * half] = make_double2(y0.x - t.x, y0.y - t.y);
+                t = cmul(w3, y3);
+                a[i0 + half] = make_double2(y1.x + t.x, y1.y + t.y);
+                a[i0 + 3 * half] = make_double2(y1.x - t.x, y1.y - t.y);
+            }
+            __syncthreads();
+        }
+        if (lg == logn) {  // odd log2 n: the last radix-2 stage
+            const int lh = lg - 1, half = 1 << lh;
             for (int j = tid; j < (n >> 1); j += nt) {
-                const int grp = j / half, pos = j - grp * half;
-                const int i1 = grp * len + pos, i2 = i1 + half;
-                double2 w = tw[pos * step];
+                const int grp = j >> lh, pos = j & (half - 1);
+                const int i1 = (grp << lg) + pos, i2 = i1 + half;
+                double2 w = tw[pos << (logn - lg)];
                 if (inverse) w.y = -w.y;
                 double2 t = cmul(w, a[i2]);
                 double2 x = a[i1];
@@ -70,33 +118,66 @@ __device__ __forceinline__ void put(double2 *a, double2 *tmp, int m, double2 v, 
 // ---------------------------------------------------------------------------
 // 1D: single CTA
 
-// the 1D solve by one CTA; sm2 holds 3 n double2
-__device__ void poisson1d_block(const double *__restrict__ rho, double *__restrict__ Ex, double *__restrict__ phi,
-                                int n, const double2 *__restrict__ tw, const double *__restrict__ k2,
-                                const double *__restrict__ kd, int pow2, int logn, double2 *sm2) {
+// Shared-memory layout of the 1D solve (double2 units): a[n], tmp[n], ph[n],
+// then the staged spectral tables tw[n] (double2) and k2[n], kd[n] (double).
+// Staging them once replaces an L1/L2 round trip per butterfly stage.
+__host__ __device__ inline size_t poisson1d_smem(int n, bool staged) {
+    return sizeof(double2) * 3 * (size_t)n + (staged ? (sizeof(double2) + 2 * sizeof(double)) * (size_t)n : 0);
+}
+
+struct Spectral1D {
+    const double2 *tw;
+    const double *k2, *kd;
+};
+
+__device__ __forceinline__ Spectral1D stage_spectral(const double2 *__restrict__ tw, const double *__restrict__ k2,
+                                                     const double *__restrict__ kd, int n, double2 *sm2) {
+    double2 *tws = sm2 + 3 * n;
+    double *k2s = reinterpret_cast<double *>(tws + n), *kds = k2s + n;
+    for (int m = threadIdx.x; m < n; m += blockDim.x) {
+        tws[m] = tw[m];
+        k2s[m] = k2[m];
+        kds[m] = kd[m];
+    }
+    return Spectral1D{tws, k2s, kds};  // visible after the caller's next __syncthreads
+}
+
+// the 1D solve by one CTA on a[] already holding the (bit-reversed for pow2)
+// transform input: Ex (and phi) to global, and Ex also to Es (smem) if given
+__device__ void poisson1d_body(double *__restrict__ Ex, double *Es, double *__restrict__ phi, int n,
+                               Spectral1D sp, int pow2, double2 *sm2, int logn) {
     double2 *a = sm2, *tmp = sm2 + n, *ph = sm2 + 2 * n;
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int m = tid; m < n; m += nt) put(a, tmp, m, make_double2(rho[m], 0.0), pow2, logn);
-    __syncthreads();
-    line_transform(a, tmp, n, tw, false, pow2);
+    FIELD_STAMP(3);
+    line_transform(a, tmp, n, sp.tw, false, pow2);
+    FIELD_STAMP(4);
     // phi_hat and E_hat (E_hat = -i kd phi_hat = (kd*ph.y, -kd*ph.x))
     for (int k = tid; k < n; k += nt) {
         double2 p = make_double2(0.0, 0.0);
-        if (k > 0) p = make_double2(a[k].x / k2[k], a[k].y / k2[k]);
+        if (k > 0) p = make_double2(a[k].x / sp.k2[k], a[k].y / sp.k2[k]);
         ph[k] = p;
     }
     __syncthreads();
     for (int pass = (phi ? 0 : 1); pass < 2; ++pass) {
         for (int k = tid; k < n; k += nt) {
             double2 v = ph[k];
-            if (pass == 1) v = make_double2(kd[k] * v.y, -(kd[k] * v.x));
+            if (pass == 1) v = make_double2(sp.kd[k] * v.y, -(sp.kd[k] * v.x));
             put(a, tmp, k, v, pow2, logn);
         }
         __syncthreads();
-        line_transform(a, tmp, n, tw, true, pow2);
+        FIELD_STAMP(5);
+        line_transform(a, tmp, n, sp.tw, true, pow2);
+        FIELD_STAMP(6);
         const double inv = 1.0 / (double)n;
-        double *out = pass == 0 ? phi : Ex;
-        for (int m = tid; m < n; m += nt) out[m] = a[m].x * inv;
+        for (int m = tid; m < n; m += nt) {
+            const double v = a[m].x * inv;
+            if (pass == 0) {
+                phi[m] = v;
+            } else {
+                Ex[m] = v;
+                if (Es) Es[m] = v;
+            }
+        }
         __syncthreads();
     }
 }
@@ -104,17 +185,24 @@ __device__ void poisson1d_block(const double *__restrict__ rho, double *__restri
 __global__ void poisson1d_kernel(const double *__restrict__ rho, double *__restrict__ Ex,
                                  double *__restrict__ phi, int n, const double2 *__restrict__ tw,
                                  const double *__restrict__ k2, const double *__restrict__ kd,
-                                 int pow2, int logn) {
+                                 int pow2, int logn, int staged) {
     extern __shared__ double2 sm2[];
-    poisson1d_block(rho, Ex, phi, n, tw, k2, kd, pow2, logn, sm2);
+    const Spectral1D sp = staged ? stage_spectral(tw, k2, kd, n, sm2) : Spectral1D{tw, k2, kd};
+    for (int m = threadIdx.x; m < n; m += blockDim.x) put(sm2, sm2 + n, m, make_double2(rho[m], 0.0), pow2, logn);
+    __syncthreads();
+    poisson1d_body(Ex, nullptr, phi, n, sp, pow2, sm2, logn);
 }
 
 // The whole 1D field chain of a stage in one CTA (the per-stage
 // "moments -> charge -> Poisson -> tables" of Simulation._stage,
-// runner.py:183-191): rho from the species densities, the spectral solve,
-// then every species' line tables (plain e/c1 or the packed rows of the
-// tiled 1D-2V kernel) -- bitwise the separate charge / Poisson / tables
-// kernels, whose block-level code it shares (field.cuh).
+// runner.py:183-191): n_s from the fused moment partials, rho, the spectral
+// solve, then every species' line tables (plain e/c1 or the packed rows of
+// the tiled 1D-2V kernel) -- bitwise the separate moment-finish / charge /
+// Poisson / tables kernels (same per-cell arithmetic and reduction trees,
+// field.cuh), with n and rho kept in registers and Ex in shared memory
+// between the phases.  Nx <= FIELD1D_MAX_CELLS_PER_THREAD * 1024.
+constexpr int FIELD1D_CPT = 2;
+
 struct Tables1D {
     int ns;
     const double *part[8];  // moment partials [Nx][rows][chunks] of each species, or none (n given)
@@ -125,55 +213,90 @@ struct Tables1D {
     int corrections[8];
 };
 
-__global__ void field1d_kernel(double *__restrict__ n, Charges q, int ns, int nx, double *__restrict__ rho,
-                               double *__restrict__ Ex, const double2 *__restrict__ tw,
-                               const double *__restrict__ k2, const double *__restrict__ kd, int pow2, int logn,
-                               Tables1D T) {
+__global__ void __launch_bounds__(1024) field1d_kernel(double *__restrict__ n, Charges q, int ns, int nx,
+                                                       double *__restrict__ rho, double *__restrict__ Ex,
+                                                       const double2 *__restrict__ tw, const double *__restrict__ k2,
+                                                       const double *__restrict__ kd, int pow2, int logn,
+                                                       Tables1D T) {
     extern __shared__ double2 sm2[];
-    if (T.part[0]) {  // n_s from the last stage's fused moment partials (vpfv_moment_partials)
-        const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    FIELD_STAMP(0);
+    double rl[FIELD1D_CPT];  // rho of this thread's cells p = tid + j*nt
+    bool own_n = T.part[0] != nullptr;
+    for (int s = 0; own_n && s < T.ns; ++s) own_n = T.rows[s] == 1;
+    if (T.part[0] && !own_n) {  // 1D-2V partials: a warp per cell (vpfv_moment_partials), n via global
+        const int warp = tid >> 5, nw = nt >> 5;
+        double *buf = reinterpret_cast<double *>(sm2);  // a/tmp/ph are free until the transform
         for (int s = 0; s < T.ns; ++s) {
-            if (T.rows[s] == 1) {  // 1D-1V: one thread per cell folds its chunks
-                for (int p = threadIdx.x; p < nx; p += blockDim.x) {
-                    double tmp[16];
-                    for (int t = 0; t < T.chunks[s]; ++t) tmp[t] = T.part[s][(size_t)p * T.chunks[s] + t];
-                    n[(size_t)s * nx + p] = __dmul_rn(fold_small(tmp, T.chunks[s]), T.vol[s]);
-                }
-                continue;
-            }
-            double *bufA = reinterpret_cast<double *>(sm2) + (size_t)warp * 2 * T.rows[s];
+            double *bufA = buf + (size_t)warp * 2 * T.rows[s];
             for (int p = warp; p < nx; p += nw) {
                 const double x = moment_cell_warp(T.part[s] + (size_t)p * T.rows[s] * T.chunks[s], T.rows[s],
                                                   T.chunks[s], bufA, bufA + T.rows[s]);
-                if ((threadIdx.x & 31) == 0) n[(size_t)s * nx + p] = __dmul_rn(x, T.vol[s]);
+                if ((tid & 31) == 0) n[(size_t)s * nx + p] = __dmul_rn(x, T.vol[s]);
             }
         }
         __syncthreads();
     }
-    double *part = reinterpret_cast<double *>(sm2 + 3 * nx);
-    charge_block(n, q, ns, nx, rho, part);
+    const Spectral1D sp = stage_spectral(tw, k2, kd, nx, sm2);  // after the finish: its buffers overlap
+    // rho = sum_s q_s n_s per cell and its fixed-order per-thread sum (charge_block)
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < FIELD1D_CPT; ++j) {
+        const int p = tid + j * nt;
+        rl[j] = 0.0;
+        if (p >= nx) continue;
+        double r = 0.0;
+        for (int s = 0; s < T.ns; ++s) {
+            double ns_p;
+            if (own_n) {  // 1D-1V partials: this thread folds its cell's chunks
+                ns_p = __dmul_rn(fold_row(T.part[s] + (size_t)p * T.chunks[s], T.chunks[s]), T.vol[s]);
+                n[(size_t)s * nx + p] = ns_p;
+            } else {
+                ns_p = n[(size_t)s * nx + p];
+            }
+            r = s == 0 ? __dmul_rn(q.q[0], ns_p) : __dadd_rn(r, __dmul_rn(q.q[s], ns_p));
+        }
+        rl[j] = r;
+        acc = __dadd_rn(acc, r);
+    }
+    FIELD_STAMP(1);
+    const double mean = __ddiv_rn(block_tree_sum(acc, red), (double)nx);
+    FIELD_STAMP(2);
+#pragma unroll
+    for (int j = 0; j < FIELD1D_CPT; ++j) {
+        const int p = tid + j * nt;
+        if (p >= nx) continue;
+        const double r = __dsub_rn(rl[j], mean);
+        rho[p] = r;
+        put(sm2, sm2 + nx, p, make_double2(r, 0.0), pow2, logn);
+    }
     __syncthreads();
-    poisson1d_block(rho, Ex, nullptr, nx, tw, k2, kd, pow2, logn, sm2);
+    // E staged for the tables in ph's region (free once the last put is done)
+    double *Eb = reinterpret_cast<double *>(sm2 + 2 * nx);
+    poisson1d_body(Ex, Eb, nullptr, nx, sp, pow2, sm2, logn);
+    FIELD_STAMP(7);
     for (int s = 0; s < T.ns; ++s) {
         if (T.packed[s]) {
-            for (int r = threadIdx.x; r < nx + 2; r += blockDim.x) {  // rows shifted by one, periodic ghosts
+            for (int r = tid; r < nx + 2; r += nt) {  // rows shifted by one, periodic ghosts
                 const int i = r == 0 ? nx - 1 : (r == nx + 1 ? 0 : r - 1);
-                double *o = T.packed[s] + (size_t)r * 8;
+                double2 *o = reinterpret_cast<double2 *>(T.packed[s] + (size_t)r * 8);
                 double e, c1;
-                table1d_row(Ex, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
-                o[0] = e;
-                o[1] = T.corrections[s] ? c1 : 0.0;
-                for (int k = 2; k < 8; ++k) o[k] = 0.0;
+                table1d_row(Eb, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
+                o[0] = make_double2(e, T.corrections[s] ? c1 : 0.0);
+                o[1] = o[2] = o[3] = make_double2(0.0, 0.0);
             }
         } else {
-            for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            for (int i = tid; i < nx; i += nt) {
                 double e, c1;
-                table1d_row(Ex, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
+                table1d_row(Eb, i, nx, T.qmk2[s], T.g[s], T.t1[s], T.den1[s], e, c1);
                 T.e[s][i] = e;
                 T.c1[s][i] = T.corrections[s] ? c1 : 0.0;
             }
         }
     }
+    __syncthreads();
+    FIELD_STAMP(8);
 }
 
 // ---------------------------------------------------------------------------
@@ -269,7 +392,8 @@ extern "C" int vpfv_poisson_1d(const double *rho, double *Ex, double *phi, int N
                                const double *k2, const double *kd, void *stream) {
     if (N < 2) return set_error(VPFV_EARG, "poisson_1d: N < 2");
     const int logn = ilog2_if_pow2(N);
-    size_t smem = sizeof(double2) * 3 * (size_t)N;
+    const bool staged = poisson1d_smem(N, true) <= 200 * 1024;
+    const size_t smem = poisson1d_smem(N, staged);
     if (smem > 200 * 1024) return set_error(VPFV_EARG, "poisson_1d: N too large for one CTA");
     static bool once = false;
     if (!once) {
@@ -277,9 +401,17 @@ extern "C" int vpfv_poisson_1d(const double *rho, double *Ex, double *phi, int N
         once = true;
     }
     poisson1d_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(
-        rho, Ex, phi, N, (const double2 *)tw, k2, kd, logn >= 0, logn < 0 ? 0 : logn);
+        rho, Ex, phi, N, (const double2 *)tw, k2, kd, logn >= 0, logn < 0 ? 0 : logn, staged ? 1 : 0);
     return check_launch("poisson_1d");
 }
+
+#ifdef VPFV_FIELD_PROBE
+extern "C" int vpfv_field_probe(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_field_probe, sizeof(g_field_probe)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
+extern "C" int vpfv_field_1d_max_cells(void) { return FIELD1D_CPT * 1024; }
 
 extern "C" int vpfv_field_1d(const double *const *partials, const int *rows, const int *chunks, const double *vols,
                              double *n, const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
@@ -287,14 +419,13 @@ extern "C" int vpfv_field_1d(const double *const *partials, const int *rows, con
                              double *const *c1, double *const *packed, const double *qmk2, const double *g,
                              const double *t1, const double *den1, const int *corrections, void *stream) {
     if (nspecies < 1 || nspecies > 8) return set_error(VPFV_EARG, "field_1d: 1..8 species");
-    if (Nx < 2) return set_error(VPFV_EARG, "field_1d: Nx < 2");
+    if (Nx < 2 || Nx > FIELD1D_CPT * 1024) return set_error(VPFV_EARG, "field_1d: Nx outside [2, 2048]");
     const int logn = ilog2_if_pow2(Nx);
-    size_t smem = sizeof(double2) * 3 * (size_t)Nx + sizeof(double) * 1024;
+    size_t smem = poisson1d_smem(Nx, true);
     for (int s = 0; partials && s < nspecies; ++s) {
         if (!partials[s] || rows[s] < 1 || chunks[s] < 1 || chunks[s] > 16)
             return set_error(VPFV_EARG, "field_1d: bad moment partials");
-        const size_t fin = sizeof(double) * 32 * 2 * (size_t)rows[s];
-        if (fin > smem) smem = fin;
+        if (sizeof(double) * 32 * 2 * (size_t)rows[s] > smem) smem = sizeof(double) * 32 * 2 * (size_t)rows[s];
     }
     if (smem > 200 * 1024) return set_error(VPFV_EARG, "field_1d: Nx too large for one CTA");
     static bool once = false;

@@ -87,7 +87,7 @@ class FieldSolver:
     # ------------------------------------------------------------------
     def field_1d_ok(self):
         """The fused 1D chain fits one CTA (poisson.cu vpfv_field_1d)."""
-        return self.d == 1 and len(self.species) <= 8 and 48 * self.phys_shape[0] + 8 * 1024 <= 200 * 1024
+        return self.d == 1 and len(self.species) <= 8 and self.phys_shape[0] <= 2048
 
     def finish_in_field_1d(self, partial_shapes):
         """Fold the moment partials inside vpfv_field_1d too?  Only when they

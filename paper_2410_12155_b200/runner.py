@@ -31,6 +31,8 @@ from .fields import FieldSolver
 from .fvm import max_speed_per_dim
 from .grid import DistField, FrozenGhosts, fill_local_ghosts
 from .kernels import StageTables, stream_handle, wrap_flags
+
+_FINITE = np.uint64(_lib.VPFV_FINITE)
 from .timestepping import DEFAULT_SIGMA, RK4_STAGES, StepContext, max_stable_dt
 
 
@@ -98,6 +100,8 @@ class Simulation:
         S = len(self.species)
         self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
         self._flags_host = torch.empty((4, S), dtype=torch.int64, pin_memory=True)
+        self._flags_np = self._flags_host.numpy().view(np.uint64)  # the divergence check reads this view
+        self._dt_set = None  # the dt value dt_dev holds (refilled only when it changes)
         self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._graphs = {}
         self._launches = {}
@@ -192,6 +196,9 @@ class Simulation:
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, None,
                         dt_dev=self.dt_dev, cL_div=div, slot=slot, cached=cached, emit_last=emit_last)
         self._launches["step"] = _lib.launch_counter[0] - start
+        # the divergence flags reach pinned host memory as part of the step (a
+        # captured D2H node), so advance() needs only the stream sync
+        self._flags_host.copy_(self.nonfinite, non_blocking=True)
 
     # -- in-step timing of the fused stage kernel (bench roofline) -----------
     def enable_stage_timing(self, on=True):
@@ -241,7 +248,9 @@ class Simulation:
 
     def launch_step(self, dt):
         """Enqueue one RK4 step (no host sync, no rotate)."""
-        self.dt_dev.fill_(float(dt))
+        if dt != self._dt_set:
+            self.dt_dev.fill_(float(dt))
+            self._dt_set = dt
         bufs = (self.ctx.f0, self.ctx.f1, self.ctx.fout)
         # the partials left by the previous step's stage 4 describe f0 when f0
         # is that step's output and nothing wrote it since
@@ -271,14 +280,15 @@ class Simulation:
     # -- stepping ---------------------------------------------------------------
     def advance(self, dt):
         self.launch_step(dt)
-        self._flags_host.copy_(self.nonfinite, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
         self._accumulate_timing()
         self.ctx.t = self.ctx.t + dt
         self.ctx.rotate()
-        bad = self._flags_host[3].numpy().astype(np.uint64)
-        for s in range(len(self.species)):
-            if bad[s] != np.uint64(_lib.VPFV_FINITE):
+        bad = self._flags_np[3]
+        if (bad != _FINITE).any():
+            for s in range(len(self.species)):
+                if bad[s] == _FINITE:
+                    continue
                 self.ctx.f0, self.ctx.fout = self.ctx.fout, self.ctx.f0
                 self.ctx.t -= dt
                 self.ctx.step -= 1
