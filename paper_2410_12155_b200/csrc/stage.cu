@@ -300,6 +300,11 @@ static Update make_update(double *dest, const double *A, const double *B, const 
 
 struct Stage22;
 bool tma_2d2v_eligible(int Nx, int Ny, int Nvx, int Nvy, unsigned flags);
+bool march_1d1v_eligible(int Nx, int Nv, unsigned flags);
+int launch_1d1v_march(double *dest, const double *A, const double *B, const double *src, double ca, double cb,
+                      double cd, double cL, const double *ax, const double *avx, const double *c1, double hx,
+                      double hv, int Nx, int Nv, unsigned flags, const double *dt_dev, double cL_div,
+                      unsigned long long *nonfinite, double *partials, cudaStream_t stream);
 
 }  // namespace vpfv
 
@@ -312,6 +317,9 @@ extern "C" int vpfv_stage_1d1v(double *dest, const double *A, const double *B, c
                                unsigned long long *nonfinite, void *stream) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
     if (Nx < 1 || Nv < 1) return set_error(VPFV_EARG, "bad extents");
+    if (march_1d1v_eligible(Nx, Nv, flags))
+        return launch_1d1v_march(dest, A, B, src, ca, cb, cd, cL, ax, avx, c1, hx, hv, Nx, Nv, flags, dt_dev, cL_div,
+                                 nonfinite, nullptr, (cudaStream_t)stream);
     Update u = make_update(dest, A, B, src, ca, cb, cd, cL, dt_dev, cL_div, nonfinite);
     T11 t{ax, avx, c1, hx, hv, -1.0 / (60.0 * hx), -1.0 / (60.0 * hv)};
     dim3 block(128), grid((Nv + 127) / 128, Nx);
@@ -334,6 +342,9 @@ extern "C" int vpfv_stage_1d1v_fused(double *dest, const double *A, const double
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
     if ((flags & VPFV_EXACT) || Nv % 128 || Nx < 1)
         return set_error(VPFV_EARG, "1D-1V moment partials need the fast path and Nv % 128 == 0");
+    if (march_1d1v_eligible(Nx, Nv, flags))
+        return launch_1d1v_march(dest, A, B, src, ca, cb, cd, cL, ax, avx, c1, hx, hv, Nx, Nv, flags, dt_dev, cL_div,
+                                 nonfinite, moment_partials, (cudaStream_t)stream);
     Update u = make_update(dest, A, B, src, ca, cb, cd, cL, dt_dev, cL_div, nonfinite);
     T11 t{ax, avx, c1, hx, hv, -1.0 / (60.0 * hx), -1.0 / (60.0 * hv)};
     dim3 block(128), grid(Nv / 128, Nx);

@@ -760,3 +760,53 @@ def test_fused_field_1d_corrections_off(monkeypatch):
     assert torch.equal(out[0].tables[0].packed, out[1].tables[0].packed)
     assert float(out[0].tables[0].packed[:, 1].abs().max()) == 0.0
     assert np.array_equal(out[0].interiors()[0], out[1].interiors()[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,periodic_x", [((64, 256), True), ((37, 128), True), ((48, 384), False),
+                                          ((1024, 1024), True)])
+def test_1d1v_march_equals_generic(N, periodic_x, monkeypatch):
+    """The x-marching 1D-1V kernel (bulk-copied rows, stage1d1v_march.cu) is
+    bitwise the generic fast kernel for every RK4 stage's operand pattern,
+    with the moment partials and the non-finite flag."""
+    g = O.Grid(1, 1, N, (0.0, -6.0), (2 * np.pi, 6.0), (periodic_x, False))
+    rng = np.random.default_rng(N[0] + N[1])
+    mk = lambda: 1.0 + 0.3 * rng.random(g.padded_shape)  # noqa: E731
+    f0, f1, fo = mk(), mk(), mk()
+    E = {"Ex": 0.2 * np.sin(g.centers(0)) + 0.05 * rng.standard_normal(N[0])}
+    sp = O.Species("e", -1.0, 1.0, 1.0, 0.0, 0.0, (0.0, 0.0))
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({"Ex": dev(E["Ex"])}, stream)
+    flags = K.wrap_flags(pg)
+    d = {"f0": dev(f0), "f1": dev(f1), "fout": dev(fo)}
+    for (dn, an, bn, sn, ca, cb, cd, div) in R.RK4_STAGES:
+        outs = []
+        for mode in ("0", "1"):
+            monkeypatch.setenv("VPFV_1D1V_MARCH", mode)
+            dest = d[dn].clone()
+            A = dest if an == dn else d[an]
+            B = dest if bn == dn else d[bn]
+            part = torch.full(tab.partials_shape(), np.nan, dtype=torch.float64, device="cuda")
+            nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            tab.launch(dest, A, B, d[sn], ca, cb, cd, 0.0, flags, stream, dt_dev=torch.full(
+                (1,), 0.01, dtype=torch.float64, device="cuda"), cL_div=div, nonfinite=nf, partials=part)
+            torch.cuda.synchronize()
+            outs.append((dest, part, int(nf.item())))
+        (a, pa, na), (b, pb, nb) = outs
+        assert torch.equal(a, b), (dn, an, bn, sn)
+        assert torch.equal(pa, pb) and na == nb == -1
+    # a non-finite input cell: both kernels report the same first bad index
+    bad = d["f0"].clone()
+    bad[3 + N[0] // 2, 3 + N[1] // 3] = np.inf
+    flagged = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("VPFV_1D1V_MARCH", mode)
+        dest = torch.zeros_like(bad)
+        nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        tab.launch(dest, bad, bad, bad, 1.0, 0.0, 0.0, 0.01, flags, stream, nonfinite=nf)
+        torch.cuda.synchronize()
+        flagged.append(int(nf.item()))
+    assert flagged[0] == flagged[1] != -1
