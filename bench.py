@@ -224,7 +224,20 @@ def run_b200(args, rank, world, device):
     if world > 1:
         from paper_2410_12155_b200.parallel import DistributedSimulation
 
-        sim = DistributedSimulation(setup, dt=None, device=device, velocity_parts=args.velocity_parts)
+        halo = args.halo
+        if halo == "auto":  # the fused NVLink push where it applies, else NCCL send/recv
+            ok = (args.velocity_parts == 1 and all(f.grid.d == 2 for f in setup.dists)
+                  and setup.dists[0].grid.N[0] % world == 0)
+            halo = "peer" if ok else "nccl"
+        try:
+            sim = DistributedSimulation(setup, dt=None, device=device, velocity_parts=args.velocity_parts, halo=halo)
+        except Exception as e:  # noqa: BLE001 -- e.g. no peer access between these GPUs
+            if halo != "peer" or args.halo == "peer":
+                raise
+            print(f"[bench] halo='peer' unavailable ({e}); using NCCL send/recv", file=sys.stderr)
+            halo = "nccl"
+            sim = DistributedSimulation(setup, dt=None, device=device, velocity_parts=args.velocity_parts, halo=halo)
+        args.halo_used = halo
         dt = 0.9 * sim.max_dt()
         sim.fixed_dt = dt
     else:
@@ -326,6 +339,7 @@ def run_b200(args, rank, world, device):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                    "cells": cells_global, "dt": dt, "l2": l2_note(setup),
+                   "halo": getattr(args, "halo_used", None),
                    "parallelism": (f"x-slab x{world // args.velocity_parts}, vx x{args.velocity_parts}"
                                    if world > 1 else "single GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -460,6 +474,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"],
+                    help="multi-GPU x-halo: fused NVLink push from the stage kernel (peer) or NCCL send/recv")
     ap.add_argument("--velocity-parts", type=int, default=1,
                     help="multi-GPU: partitions of the first velocity dim (ranks = x-slabs x this)")
     args = ap.parse_args()

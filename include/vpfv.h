@@ -133,6 +133,35 @@ int vpfv_stage_1d2v_tiled_ok(int Nx, int Nvx, int Nvy, unsigned flags);
  * [Nx][Nvx][Nvy/chunk] fold-tree subtree sums. */
 int vpfv_stage_1d2v_partials_chunk(void);
 
+/* vpfv_stage_2d2v_fused (full x range) that also pushes its x halo to the
+ * slab neighbours over peer memory: planes 0..2 of dest are stored into
+ * peer_lo (the low x neighbour's dest, same padded shape) at its ghost planes
+ * Nx..Nx+2, planes Nx-3..Nx-1 into peer_hi at ghost planes 0..2; the last CTA
+ * then adds 1 to *sig_lo (the low neighbour's "from high" word) and *sig_hi
+ * (the high neighbour's "from low" word).  done: a zeroed device counter per
+ * concurrently running launch.  Replaces the per-stage halo exchange of the
+ * reference cluster (runner.py:394-437, partition.py:679-724). */
+int vpfv_stage_2d2v_fused_peer(double *dest, const double *A, const double *B, const double *src,
+                               double ca, double cb, double cd, double cL, const double *vxc,
+                               const double *vyc, const double *evx, const double *evy, double cB,
+                               const double *c1, double c2, const double *c3, const double *c4,
+                               const double *c5, double hx, double hy, double hvx, double hvy, int Nx,
+                               int Ny, int Nvx, int Nvy, unsigned flags, const double *dt_dev,
+                               double cL_div, unsigned long long *nonfinite,
+                               const double *packed_tables, double *moment_partials, double *peer_lo,
+                               double *peer_hi, unsigned long long *sig_lo, unsigned long long *sig_hi,
+                               unsigned *done, void *stream);
+
+/* Signal both neighbours once (after an initial halo exchange by other means). */
+int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream);
+
+/* Wait (one device thread, system-scope acquire) until sig[0] / sig[1] (this
+ * rank's words, written by its low / high neighbour) exceed consumed[k] by
+ * need_lo / need_hi, then advance consumed.  After timeout_s seconds it sets
+ * *timed_out = 1 and returns instead of hanging the device. */
+int vpfv_peer_wait(const unsigned long long *sig, unsigned long long *consumed, int need_lo, int need_hi,
+                   double timeout_s, int *timed_out, void *stream);
+
 /* vpfv_stage_2d2v_fused restricted to the interior x cells [x_begin, x_end)
  * (tiled path only; VPFV_EARG otherwise).  Planes x_begin-3 .. x_end+2 are
  * read, so a slab whose x ghosts are still in flight can update its x

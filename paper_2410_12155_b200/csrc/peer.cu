@@ -1,0 +1,74 @@
+// Signalling for the x-slab halo push over NVLink peer memory.
+//
+// In the peer mode of DistributedSimulation (parallel.py) each rank's stage
+// kernel stores its 3 boundary x planes straight into the x neighbours'
+// dest buffers (their ghost planes) as it computes them -- the halo exchange
+// of the reference cluster (runner.py:394-437, Exchanger partition.py:679-724)
+// fused into the producing kernel, no separate copy or NCCL call.  The last
+// CTA of that kernel bumps a 64-bit signal word on each neighbour
+// (vpfv_stage_2d2v_fused_peer); before its next stage reads those ghost
+// planes a rank runs vpfv_peer_wait, one thread spinning on its own signal
+// words with system-scope acquire loads.  The words only grow; each rank
+// keeps how many signals it has consumed in device memory, so the same wait
+// is valid in every replay of a captured step.  Ordering argument (DESIGN.md
+// "Multi-GPU"): a rank starts stage k only after both neighbours finished
+// stage k-1, so a push never lands in a buffer a neighbour is still reading.
+#include "common.cuh"
+
+namespace vpfv {
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void peer_signal_kernel(unsigned long long *sig_lo, unsigned long long *sig_hi) {
+    __threadfence_system();
+    if (sig_lo) atomicAdd_system(sig_lo, 1ull);
+    if (sig_hi) atomicAdd_system(sig_hi, 1ull);
+}
+
+// sig[0]: signals from the low x neighbour, sig[1]: from the high one
+__global__ void peer_wait_kernel(const unsigned long long *sig, unsigned long long *consumed, unsigned need_lo,
+                                 unsigned need_hi, unsigned long long timeout_ns, int *timed_out) {
+    const unsigned need[2] = {need_lo, need_hi};
+    const unsigned long long t0 = now_ns();
+    for (int k = 0; k < 2; ++k) {
+        if (!need[k]) continue;
+        const unsigned long long target = consumed[k] + need[k];
+        while (ld_acquire_sys(sig + k) < target) {
+            if (now_ns() - t0 > timeout_ns) {  // a lost neighbour must not hang the device
+                atomicExch(timed_out, 1);
+                return;
+            }
+            __nanosleep(200);
+        }
+        consumed[k] = target;
+    }
+    __threadfence();
+}
+
+}  // namespace vpfv
+
+using namespace vpfv;
+
+extern "C" int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream) {
+    peer_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sig_lo, sig_hi);
+    return check_launch("peer_signal");
+}
+
+extern "C" int vpfv_peer_wait(const unsigned long long *sig, unsigned long long *consumed, int need_lo, int need_hi,
+                              double timeout_s, int *timed_out, void *stream) {
+    if (!sig || !consumed || !timed_out || need_lo < 0 || need_hi < 0)
+        return set_error(VPFV_EARG, "peer_wait: bad arguments");
+    peer_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sig, consumed, (unsigned)need_lo, (unsigned)need_hi,
+                                                       (unsigned long long)(timeout_s * 1e9), timed_out);
+    return check_launch("peer_wait");
+}

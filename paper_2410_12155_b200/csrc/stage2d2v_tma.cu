@@ -69,7 +69,31 @@ struct Stage22 {
     int nseg, seglen;  // x segments per column block
     int sj, sk;        // super-tile of column blocks (block order)
     double *partials;  // moment partials [Nx][Ny][Nvx][Nvy/16] or nullptr
+    // peer halo push (x-slab ranks over NVLink, vpfv_stage_2d2v_fused_peer):
+    // planes 0..2 also go to the low x neighbour's dest (its high ghost
+    // planes), planes Nx-3..Nx-1 to the high neighbour's low ghost planes;
+    // the last CTA to finish bumps the neighbours' signal words
+    double *peer_lo, *peer_hi;
+    unsigned long long *sig_lo, *sig_hi;
+    unsigned *done;
 };
+
+// After every thread of the CTA has made its stores (peer ones included)
+// visible system-wide, count the CTA; the last one signals both neighbours.
+__device__ __forceinline__ void peer_done_signal(const Stage22 &P) {
+    if (!P.done) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(P.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *P.done = 0u;  // ready for the next launch (ordered by the kernel boundary)
+            __threadfence_system();
+            if (P.sig_lo) atomicAdd_system(P.sig_lo, 1ull);
+            if (P.sig_hi) atomicAdd_system(P.sig_hi, 1ull);
+        }
+    }
+}
 
 namespace rb {
 constexpr int BJ = 8, BL = 16, OPS_MAX = 2;
@@ -246,7 +270,10 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int j0 = jt * BJ, k0 = kt * BK, l0 = lt * BL;
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
-    if (i0 >= i1) return;
+    if (i0 >= i1) {
+        peer_done_signal(P);
+        return;
+    }
 
     // thread -> cells (y0 + a, vx0 + b, vy), a < 2, b < BB
     const int lane = tid & 31, warp = tid >> 5;
@@ -527,6 +554,16 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             }
 #pragma unroll
             for (int i = 0; i < NC; ++i) __stcs(dq + (i / BB) * P2 + (i % BB) * P3, out[i]);
+            if (P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
+                double *pq = P.peer_lo + gq + (long long)P.Nx * P1;
+#pragma unroll
+                for (int i = 0; i < NC; ++i) pq[(i / BB) * P2 + (i % BB) * P3] = out[i];
+            }
+            if (P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
+                double *pq = P.peer_hi + gq - (long long)P.Nx * P1;
+#pragma unroll
+                for (int i = 0; i < NC; ++i) pq[(i / BB) * P2 + (i % BB) * P3] = out[i];
+            }
             bool bad = false;
             if (P.partials) {
                 // reference fold tree over each aligned 16-wide vy chunk
@@ -593,6 +630,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         ppart += pstep;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
+    peer_done_signal(P);
 }
 
 // ---------------------------------------------------------------------------
@@ -817,7 +855,7 @@ static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B,
                                  double hvx, double hvy, int Nx, int Ny, int Nvx, int Nvy, int x_begin, int x_end,
                                  unsigned flags, const double *dt_dev, double cL_div, unsigned long long *nonfinite,
                                  const double *packed_tables, double *moment_partials, int xsegments,
-                                 void *stream) {
+                                 void *stream, const Stage22 *peer = nullptr) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
     if (x_begin < 0 || x_end > Nx || x_begin > x_end) return set_error(VPFV_EARG, "bad x range");
     if (x_begin == x_end) return VPFV_OK;
@@ -828,6 +866,7 @@ static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B,
     ops.add(dest, cd, src);
     if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags) || ops.n > rb::OPS_MAX) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 2D-2V path");
+        if (peer) return set_error(VPFV_EARG, "peer halo push needs the tiled 2D-2V path");
         if (!full) return set_error(VPFV_EARG, "x sub-ranges need the tiled 2D-2V path");
         return vpfv_stage_2d2v_generic(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2,
                                        c3, c4, c5, hx, hy, hvx, hvy, Nx, Ny, Nvx, Nvy, flags, dt_dev,
@@ -859,6 +898,13 @@ static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B,
     P.i0 = x_begin;
     P.i1 = x_end;
     P.partials = moment_partials;
+    if (peer) {
+        P.peer_lo = peer->peer_lo;
+        P.peer_hi = peer->peer_hi;
+        P.sig_lo = peer->sig_lo;
+        P.sig_hi = peer->sig_hi;
+        P.done = peer->done;
+    }
     int nseg = xsegments;
     static int env_seg = -1;
     if (env_seg < 0) {
@@ -903,6 +949,30 @@ extern "C" int vpfv_stage_2d2v_fused_range(double *dest, const double *A, const 
     return stage_2d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3, c4, c5, hx,
                                  hy, hvx, hvy, Nx, Ny, Nvx, Nvy, x_begin, x_end, flags, dt_dev, cL_div, nonfinite,
                                  packed_tables, moment_partials, 0, stream);
+}
+
+extern "C" int vpfv_stage_2d2v_fused_peer(double *dest, const double *A, const double *B, const double *src,
+                                          double ca, double cb, double cd, double cL, const double *vxc,
+                                          const double *vyc, const double *evx, const double *evy, double cB,
+                                          const double *c1, double c2, const double *c3, const double *c4,
+                                          const double *c5, double hx, double hy, double hvx, double hvy, int Nx,
+                                          int Ny, int Nvx, int Nvy, unsigned flags, const double *dt_dev,
+                                          double cL_div, unsigned long long *nonfinite,
+                                          const double *packed_tables, double *moment_partials, double *peer_lo,
+                                          double *peer_hi, unsigned long long *sig_lo, unsigned long long *sig_hi,
+                                          unsigned *done, void *stream) {
+    if (!packed_tables || !tma_2d2v_eligible(Nx, Ny, Nvx, Nvy, flags))
+        return set_error(VPFV_EARG, "peer halo push needs the tiled 2D-2V path");
+    if (Nx < NG || !done) return set_error(VPFV_EARG, "peer halo push: Nx >= 3 and a done counter");
+    Stage22 peer{};
+    peer.peer_lo = peer_lo;
+    peer.peer_hi = peer_hi;
+    peer.sig_lo = sig_lo;
+    peer.sig_hi = sig_hi;
+    peer.done = done;
+    return stage_2d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3, c4, c5, hx,
+                                 hy, hvx, hvy, Nx, Ny, Nvx, Nvy, 0, Nx, flags, dt_dev, cL_div, nonfinite,
+                                 packed_tables, moment_partials, 0, stream, &peer);
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,

@@ -22,6 +22,13 @@ phase space (all of y and velocity space), so
 ``SlabExchange`` holds the communication logic and is backend agnostic
 (NCCL on CUDA tensors, gloo on CPU tensors), so tests/test_parallel.py runs
 it with world size 2 on the CPU against the single-rank oracle.
+
+``halo="peer"`` (tiled 2D-2V x-slabs) fuses the x-halo exchange into the
+stage kernel instead: every rank maps its x neighbours' state buffers (CUDA
+IPC, peer access over NVLink), its stage kernel stores the boundary planes
+straight into the neighbours' ghost planes as it computes them, and a
+signal word per neighbour (``PeerHalo``, csrc/peer.cu) replaces the
+send/recv.
 """
 
 from __future__ import annotations
@@ -282,6 +289,110 @@ class SlabExchange:
         return bool(t.item())
 
 
+class PeerHalo:
+    """Pointers and signal words of the fused x-halo push for one rank.
+
+    ``peer_of`` maps each local state buffer (data_ptr) to its counterparts
+    on the low / high x neighbours (same padded shape, same role: all ranks
+    allocate and rotate their buffers alike); ``sig`` is this rank's pair of
+    signal words (written by the low / high neighbour), ``sig_lo_ptr`` /
+    ``sig_hi_ptr`` the addresses of the neighbours' words this rank bumps.
+    Built from CUDA IPC mappings across processes (``ipc``), or across
+    buffers of one process (``linked``: the single-GPU test harness, where the
+    "peers" are other slabs on the same device)."""
+
+    def __init__(self, peer_of, sig, sig_lo_ptr, sig_hi_ptr, nspecies, device, timeout_s=30.0):
+        self.peer_of = dict(peer_of)
+        self.sig = sig
+        self.sig_lo_ptr, self.sig_hi_ptr = int(sig_lo_ptr), int(sig_hi_ptr)
+        self.nspecies = nspecies
+        self.consumed = torch.zeros(2, dtype=torch.int64, device=device)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        self.done = torch.zeros(max(1, nspecies), dtype=torch.int32, device=device)
+        self.timeout_s = timeout_s
+
+    @staticmethod
+    def linked(states, sigs, nspecies, device):
+        """PeerHalo of each of len(states) slabs in one process: states[r] is
+        slab r's list of state buffers, sigs[r] its int64[2] signal words;
+        slabs are periodic neighbours in x."""
+        R = len(states)
+        out = []
+        for r in range(R):
+            lo, hi = (r - 1) % R, (r + 1) % R
+            peer_of = {a.data_ptr(): (b.data_ptr(), c.data_ptr())
+                       for a, b, c in zip(states[r], states[lo], states[hi])}
+            out.append(PeerHalo(peer_of, sigs[r], sigs[lo].data_ptr() + 8, sigs[hi].data_ptr(), nspecies, device))
+        return out
+
+    @staticmethod
+    def ipc(buffers, comm, group, nspecies, device):
+        """Map the x neighbours' counterparts of ``buffers`` and their signal
+        words into this process: CUDA IPC handles of every rank's buffers are
+        all-gathered (``torch.multiprocessing`` tensor sharing; the mapping
+        enables peer access, so a kernel on this GPU stores over NVLink into
+        the neighbour's memory).  Collective over ``group``."""
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        sig = torch.zeros(2, dtype=torch.int64, device=device)
+        mine = [reduce_tensor(b) for b in list(buffers) + [sig]]
+        allh = [None] * comm.world
+        dist.all_gather_object(allh, mine, group=group)
+        keep = []  # the mapped neighbour tensors must outlive the run
+
+        def mapped(r, k):
+            fn, args = allh[r][k]
+            t = fn(*args)
+            keep.append(t)
+            return t.data_ptr()
+
+        peer_of = {}
+        for k, b in enumerate(buffers):
+            peer_of[b.data_ptr()] = (mapped(comm.left, k), mapped(comm.right, k))
+        nb = len(buffers)
+        out = PeerHalo(peer_of, sig, mapped(comm.left, nb) + 8, mapped(comm.right, nb), nspecies, device)
+        out._keep = keep
+        torch.cuda.synchronize(device)
+        dist.barrier(group)  # every rank's words are zero before anyone signals
+        return out
+
+    def signal(self, stream):
+        """Tell both neighbours this rank's ghost-feeding planes are in place
+        (once, after the initial exchange)."""
+        for _ in range(self.nspecies):
+            _lib.call("vpfv_peer_signal", self.sig_lo_ptr, self.sig_hi_ptr, stream)
+
+    def wait(self, stream):
+        """Stream-ordered wait for both neighbours' pushes of the previous stage."""
+        _lib.call("vpfv_peer_wait", self.sig.data_ptr(), self.consumed.data_ptr(), self.nspecies, self.nspecies,
+                  float(self.timeout_s), self.timed_out.data_ptr(), stream)
+
+    def push_args(self, dest, s):
+        lo, hi = self.peer_of[dest.data_ptr()]
+        return lo, hi, self.sig_lo_ptr, self.sig_hi_ptr, self.done[s:s + 1].data_ptr()
+
+    def check(self):
+        if int(self.timed_out.item()):
+            raise RuntimeError("peer halo: a neighbour's signal did not arrive (timed out)")
+
+
+def launch_stage_peer(lt, dest, A, B, src, ca, cb, cd, cL, flags, stream, push, dt_dev=None, cL_div=1.0,
+                      nonfinite=None, partials=None):
+    """The tiled 2D-2V stage of slab table view ``lt`` (_LocalTables) with the
+    fused halo push ``push`` = PeerHalo.push_args(dest, s)."""
+    t, g = lt.t, lt.lgrid
+    h, N = g.h, g.N
+    Ny = t.grid.N[1]
+    off = lt.x0 * Ny * 8
+    ptr = lambda a: a.data_ptr() + off  # noqa: E731
+    _lib.call("vpfv_stage_2d2v_fused_peer", dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
+              float(ca), float(cb), float(cd), float(cL), t.vxc.data_ptr() + lt.v0 * 8, t.vyc.data_ptr(),
+              ptr(t.evx), ptr(t.evy), t.cB, ptr(t.c1), t.c2, ptr(t.c3), ptr(t.c4), ptr(t.c5), h[0], h[1], h[2],
+              h[3], N[0], N[1], N[2], N[3], flags, None if dt_dev is None else dt_dev.data_ptr(), float(cL_div),
+              None if nonfinite is None else nonfinite.data_ptr(), t.packed.data_ptr() + lt.x0 * Ny * 8 * 8,
+              None if partials is None else partials.data_ptr(), *push, stream)
+
+
 class _GridView:
     """Minimal stand-in carrying a slab grid, for StageTables' shape queries."""
 
@@ -361,7 +472,9 @@ class DistributedSimulation:
     each): x-slab decomposition, NCCL halo exchange, replicated Poisson."""
 
     def __init__(self, setup, cfl_fraction=0.9, dt=None, corrections=True, sigma=DEFAULT_SIGMA, *,
-                 device=None, exact=False, group=None, velocity_parts=1):
+                 device=None, exact=False, group=None, velocity_parts=1, halo="nccl"):
+        if halo not in ("nccl", "peer"):
+            raise ValueError(f"halo must be 'nccl' or 'peer', not {halo!r}")
         self.device = require_cuda(device)
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -383,6 +496,12 @@ class DistributedSimulation:
             idx[0] = slice(self.x0, self.x0 + self.nloc + 2 * NGHOST)
             idx[self.vdim] = slice(v0, v0 + nv + 2 * NGHOST)
             f0.append(torch.from_numpy(np.ascontiguousarray(data[tuple(idx)])).to(self.device))
+        self.halo = halo
+        if halo == "peer":
+            if velocity_parts != 1 or self.world < 2 or any(g.d != 2 for g in self.grids):
+                raise ValueError("halo='peer' needs 2D-2V x-slabs over >= 2 ranks (velocity_parts=1)")
+            if self.grids[0].N[0] % self.world:
+                raise ValueError("halo='peer' needs equal slabs (Nx divisible by the rank count)")
         self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
         # tables and the field solve on the GLOBAL grid (replicated), launches on the slab
         self.gtables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
@@ -409,6 +528,18 @@ class DistributedSimulation:
         self.overlap = (all(self.tiled) and all(lg.d == 2 for lg in self.lgrids) and self.nloc >= 2 * NGHOST + 1
                         and os.environ.get("VPFV_NO_OVERLAP") is None)
         self._N_arrays = [_lib.int_array(lg.N) for lg in self.lgrids]
+        self.peer = None
+        if halo == "peer":
+            if not all(self.tiled) or self.nloc < NGHOST:
+                raise ValueError("halo='peer' needs the tiled 2D-2V path and slabs of >= 3 planes")
+            bufs = [a for trio in zip(self.ctx.f0, self.ctx.f1, self.ctx.fout) for a in trio]
+            self.peer = PeerHalo.ipc(bufs, self.comm, group, S, self.device)
+            # the t = 0 ghosts by one ordinary exchange, then the first signal
+            for trio in (self.ctx.f0, self.ctx.f1, self.ctx.fout):
+                self.comm.exchange_x(trio)
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group)
+            self.peer.signal(stream_handle(self.device))
 
     # ------------------------------------------------------------------
     def traffic_report(self):
@@ -464,11 +595,35 @@ class DistributedSimulation:
         self.fields.charge(stream)
         return self.fields.poisson(self.fields.rho, False, stream)
 
+    def _stage_peer(self, dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=None, cL_div=1.0):
+        """One stage with the x halo pushed by the stage kernels themselves:
+        the field solve (densities all-gathered), then a wait for both
+        neighbours' pushes of the previous stage (src's ghost planes), then
+        the stage launches, which push dest's boundary planes onward."""
+        stream = stream_handle(self.device)
+        E = self._solve(src, from_partials=self.fuse_moment and slot is not None and slot > 0)
+        for s, gt in enumerate(self.gtables):
+            gt.update(E, stream, packed=True)
+        self.peer.wait(stream)
+        emit = self.fuse_moment and slot is not None and slot < 3
+        timed = self._timing and slot is not None
+        for s, lt in enumerate(self.tables):
+            nf = None if slot is None else self.nonfinite[slot, s:s + 1]
+            if timed:
+                self._events[slot][s][0].record()
+            launch_stage_peer(lt, dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
+                              self.peer.push_args(dest[s], s), dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
+                              partials=self.partials[s] if emit else None)
+            if timed:
+                self._events[slot][s][1].record()
+
     def _stage(self, dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=None, cL_div=1.0):
         """One stage on the slab.  On the tiled 2D-2V path the x-halo exchange
         overlaps the field solve and the x-interior planes [3, n-3), which read
         no ghost plane; the two 3-plane boundary ranges run once the ghosts
         have arrived.  Otherwise the exchange completes first."""
+        if self.peer is not None:
+            return self._stage_peer(dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=dt_dev, cL_div=cL_div)
         stream = stream_handle(self.device)
         overlap = self.overlap and self.comm.px > 1
         self.comm.exchange_v(src, self.vdim)  # velocity faces first: the x planes sent next carry them
@@ -539,6 +694,8 @@ class DistributedSimulation:
             for slot in range(4):
                 for a, b in self._events[slot]:
                     self._stage_ms[slot] += a.elapsed_time(b)
+        if self.peer is not None:
+            self.peer.check()
         self.ctx.t = self.ctx.t + dt
         self.ctx.rotate()
         flags = self.nonfinite[3].cpu().numpy().astype(np.uint64)

@@ -71,7 +71,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, names, dts, steps, q, vparts=1):
+def _worker(rank, world, port, names, dts, steps, q, vparts=1, halo="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -81,7 +81,7 @@ def _worker(rank, world, port, names, dts, steps, q, vparts=1):
         torch.cuda.set_device(0)
         out = {}
         for name, dt in zip(names, dts):
-            sim = PL.DistributedSimulation(_setup(name), dt=dt, device="cuda:0", velocity_parts=vparts)
+            sim = PL.DistributedSimulation(_setup(name), dt=dt, device="cuda:0", velocity_parts=vparts, halo=halo)
             for _ in range(steps):
                 sim.advance(dt)
             out[name] = [sim.gather(s) for s in range(len(sim.species))]
@@ -144,3 +144,101 @@ def test_velocity_partitions_same_gpu_equal_simulation(world, vparts):
     for n in names:
         for a, b in zip(got[n], refs[n][1]):
             assert np.array_equal(a, b), n
+
+
+# ---------------------------------------------------------------------------
+# fused x-halo push over peer memory (csrc/peer.cu, vpfv_stage_2d2v_fused_peer)
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+def test_peer_halo_push_linked_slabs_equal_simulation(nslabs):
+    """nslabs x-slabs of a 2D-2V Landau run on one GPU, each on its own
+    stream: every slab's stage kernel stores its 3 boundary planes into its
+    neighbours' ghost planes and signals them; each slab waits on its own
+    signal words before its next stage.  The slabs step bitwise like the
+    single-GPU Simulation, and every wait consumed exactly its signals."""
+    from paper_2410_12155_b200 import _lib, parallel as PL, runner as R
+    from paper_2410_12155_b200.fields import FieldSolver
+    from paper_2410_12155_b200.grid import NGHOST
+    from paper_2410_12155_b200.kernels import StageTables, stream_handle
+    from paper_2410_12155_b200.timestepping import RK4_STAGES
+
+    steps = 3
+    dt, want = _reference("landau2d", steps)
+    setup = _setup("landau2d")
+    dev = torch.device("cuda:0")
+    g, sp = setup.dists[0].grid, setup.species[0]
+    data, _ = R._host_filled(setup.dists[0])
+    nloc = g.N[0] // nslabs
+    lgrid = PL.local_grid(g, 0, nloc)
+    states, sigs, views = [], [], []
+    gt = StageTables(g, sp, dev)
+    for r in range(nslabs):
+        x0 = r * nloc
+        f0 = torch.from_numpy(np.ascontiguousarray(data[x0:x0 + nloc + 2 * NGHOST])).to(dev)
+        states.append([f0, f0.clone(), f0.clone()])  # (f0, f1, fout)
+        sigs.append(torch.zeros(2, dtype=torch.int64, device=dev))
+        views.append(PL._LocalTables(gt, lgrid, x0))
+    peers = PL.PeerHalo.linked(states, sigs, 1, dev)
+    fields = FieldSolver([g], [sp], dev)
+    flags = sum(_lib.VPFV_WRAP(k) for k in range(1, 4) if lgrid.periodic[k])
+    assert _lib.load().vpfv_stage_2d2v_tiled_ok(nloc, g.N[1], g.N[2], g.N[3], flags)
+    nloc_arr = _lib.int_array(lgrid.N)
+    dt_dev = torch.full((1,), dt, dtype=torch.float64, device=dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(nslabs)]
+    main = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    for r in range(nslabs):
+        peers[r].signal(stream_handle(dev))  # the t = 0 ghosts came with the global array
+    Ny = g.N[1]
+    for _ in range(steps):
+        for (dn, an, bn, sn, ca, cb, cd, div) in RK4_STAGES:
+            names = {"f0": 0, "f1": 1, "fout": 2}
+            for st in streams:
+                main.wait_stream(st)
+            for r in range(nslabs):  # this slab's rows of the global density
+                _lib.call("vpfv_moment", states[r][names[sn]].data_ptr(),
+                          fields.n.data_ptr() + r * nloc * Ny * 8, 2, 2, nloc_arr, fields.vols[0], stream_handle(dev))
+            fields.charge()
+            E = fields.poisson(fields.rho)
+            gt.update(E, stream_handle(dev), packed=True)
+            for r in range(nslabs):
+                streams[r].wait_stream(main)
+                with torch.cuda.stream(streams[r]):
+                    h = stream_handle(dev)
+                    st_ = states[r]
+                    dest = st_[names[dn]]
+                    peers[r].wait(h)
+                    PL.launch_stage_peer(views[r], dest, st_[names[an]], st_[names[bn]], st_[names[sn]], ca, cb, cd,
+                                         0.0, flags, h, peers[r].push_args(dest, 0), dt_dev=dt_dev, cL_div=div)
+        for r in range(nslabs):  # rotate f0 <-> fout
+            states[r][0], states[r][2] = states[r][2], states[r][0]
+    torch.cuda.synchronize()
+    for r in range(nslabs):
+        peers[r].check()
+        assert peers[r].consumed.tolist() == [4 * steps] * 2
+        assert sigs[r].tolist() == [4 * steps + 1] * 2  # the last stage's signal awaits the next stage
+    got = np.concatenate([s[0][lgrid.interior_slices()].cpu().numpy() for s in states], axis=0)
+    assert np.array_equal(got, want[0])
+
+
+def test_peer_halo_two_processes_same_gpu():
+    """DistributedSimulation(halo="peer") with two processes sharing the GPU:
+    each maps the other's state buffers and signal words by CUDA IPC, the
+    stage kernels push the x halo across the processes, and the gathered
+    state is bitwise the single-GPU Simulation."""
+    names = ["landau2d"]
+    refs = {n: _reference(n, 2) for n in names}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, names, [refs[n][0] for n in names], 2, q, 1, "peer"))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = _collect(q, procs, 300)
+    for p in procs:
+        p.join(60)
+    for n in names:
+        for a, b in zip(out[n], refs[n][1]):
+            assert np.array_equal(a.cpu().numpy() if hasattr(a, "cpu") else a, b)

@@ -303,3 +303,32 @@ def test_traffic_report_counts_halo_bytes():
     assert t["x_halo_bytes"] == 2 * 3 * plane * 8
     assert t["v_face_bytes"] == 1 * 8 * 3 * 14 * 14 * 8
     assert t["density_bytes"] == 3 * 64 * 8
+
+
+def test_peer_halo_linked_pointer_tables():
+    """PeerHalo.linked: each slab's buffers map to the same-role buffers of its
+    periodic x neighbours, and it bumps the low neighbour's "from high" word
+    (offset 8) and the high neighbour's "from low" word (offset 0)."""
+    from paper_2410_12155_b200.parallel import PeerHalo
+
+    R = 3
+    states = [[torch.zeros(4, dtype=torch.float64) for _ in range(3)] for _ in range(R)]
+    sigs = [torch.zeros(2, dtype=torch.int64) for _ in range(R)]
+    peers = PeerHalo.linked(states, sigs, 2, "cpu")
+    for r, p in enumerate(peers):
+        lo, hi = (r - 1) % R, (r + 1) % R
+        for k in range(3):
+            assert p.peer_of[states[r][k].data_ptr()] == (states[lo][k].data_ptr(), states[hi][k].data_ptr())
+        assert p.sig_lo_ptr == sigs[lo].data_ptr() + 8 and p.sig_hi_ptr == sigs[hi].data_ptr()
+        assert p.push_args(states[r][1], 1)[:4] == (states[lo][1].data_ptr(), states[hi][1].data_ptr(),
+                                                    sigs[lo].data_ptr() + 8, sigs[hi].data_ptr())
+        assert p.done.numel() == 2
+
+
+def test_peer_halo_mode_validation():
+    """halo='peer' is refused where the fused push does not apply."""
+    from paper_2410_12155_b200 import problems as P
+    from paper_2410_12155_b200.parallel import DistributedSimulation
+
+    with pytest.raises(ValueError):
+        DistributedSimulation(P.make_problem(P.landau_spec(), 8, 8), halo="bogus", device="cpu")
