@@ -162,6 +162,14 @@ int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, voi
 int vpfv_peer_wait(const unsigned long long *sig, unsigned long long *consumed, int need_lo, int need_hi,
                    double timeout_s, int *timed_out, void *stream);
 
+/* CUDA IPC of a device buffer between rank processes: export writes the
+ * handle of the allocation holding ptr (vpfv_ipc_handle_size() bytes) and
+ * ptr's offset in it; open maps it into the calling device's context with
+ * peer access (once per allocation and process) and returns the buffer. */
+int vpfv_ipc_handle_size(void);
+int vpfv_ipc_export(const void *ptr, unsigned char *handle_out, long long *offset_out);
+int vpfv_ipc_open(const unsigned char *handle, long long offset, void **ptr_out);
+
 /* vpfv_stage_2d2v_fused restricted to the interior x cells [x_begin, x_end)
  * (tiled path only; VPFV_EARG otherwise).  Planes x_begin-3 .. x_end+2 are
  * read, so a slab whose x ghosts are still in flight can update its x

@@ -13,6 +13,13 @@
 // is valid in every replay of a captured step.  Ordering argument (DESIGN.md
 // "Multi-GPU"): a rank starts stage k only after both neighbours finished
 // stage k-1, so a push never lands in a buffer a neighbour is still reading.
+#include <cuda.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+
 #include "common.cuh"
 
 namespace vpfv {
@@ -72,3 +79,69 @@ extern "C" int vpfv_peer_wait(const unsigned long long *sig, unsigned long long 
                                                        (unsigned long long)(timeout_s * 1e9), timed_out);
     return check_launch("peer_wait");
 }
+
+// ---------------------------------------------------------------------------
+// CUDA IPC of state buffers between the rank processes.  A handle names a
+// whole allocation (a torch caching-allocator block), so the export also
+// returns the buffer's offset in it; the open maps the allocation into the
+// calling device's context with peer access enabled (stores and system
+// atomics then travel over NVLink), once per allocation and process.
+
+typedef CUresult (*AddressRangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+static AddressRangeFn address_range() {
+    static AddressRangeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddressRangeFn>(p);
+    }
+    return fn;
+}
+
+extern "C" int vpfv_ipc_export(const void *ptr, unsigned char *handle_out, long long *offset_out) {
+    AddressRangeFn fn = address_range();
+    if (!fn) return set_error(VPFV_ECUDA, "ipc_export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return set_error(VPFV_ECUDA, "ipc_export: not device memory");
+    static std::mutex mu;
+    static std::map<CUdeviceptr, cudaIpcMemHandle_t> handles;  // one handle per allocation
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = handles.find(base);
+    if (it == handles.end()) {
+        cudaIpcMemHandle_t h;
+        cudaError_t e = cudaIpcGetMemHandle(&h, (void *)base);
+        if (e != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(e));
+        it = handles.emplace(base, h).first;
+    }
+    memcpy(handle_out, &it->second, sizeof(cudaIpcMemHandle_t));
+    *offset_out = (long long)((CUdeviceptr)ptr - base);
+    return VPFV_OK;
+}
+
+extern "C" int vpfv_ipc_open(const unsigned char *handle, long long offset, void **ptr_out) {
+    static std::mutex mu;
+    static std::map<std::string, void *> opened;
+    std::lock_guard<std::mutex> lock(mu);
+    const std::string key(reinterpret_cast<const char *>(handle), sizeof(cudaIpcMemHandle_t));
+    auto it = opened.find(key);
+    void *base = nullptr;
+    if (it != opened.end()) {
+        base = it->second;
+    } else {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handle, sizeof(h));
+        cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(e));
+        opened[key] = base;
+    }
+    *ptr_out = static_cast<char *>(base) + offset;
+    return VPFV_OK;
+}
+
+extern "C" int vpfv_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }

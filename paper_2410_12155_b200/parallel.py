@@ -328,30 +328,35 @@ class PeerHalo:
     @staticmethod
     def ipc(buffers, comm, group, nspecies, device):
         """Map the x neighbours' counterparts of ``buffers`` and their signal
-        words into this process: CUDA IPC handles of every rank's buffers are
-        all-gathered (``torch.multiprocessing`` tensor sharing; the mapping
-        enables peer access, so a kernel on this GPU stores over NVLink into
-        the neighbour's memory).  Collective over ``group``."""
-        from torch.multiprocessing.reductions import reduce_tensor
+        words into this process: the CUDA IPC handles of every rank's buffers
+        are all-gathered and each rank opens its neighbours' in its own
+        device's context with peer access (``vpfv_ipc_export`` /
+        ``vpfv_ipc_open``), so the stage kernel's stores and the signal
+        atomics go over NVLink.  Collective over ``group``."""
+        import ctypes
 
+        nh = _lib.load().vpfv_ipc_handle_size()
         sig = torch.zeros(2, dtype=torch.int64, device=device)
-        mine = [reduce_tensor(b) for b in list(buffers) + [sig]]
+
+        def export(t):
+            h = (ctypes.c_ubyte * nh)()
+            off = ctypes.c_longlong()
+            _lib.call("vpfv_ipc_export", t.data_ptr(), h, ctypes.byref(off))
+            return bytes(h), off.value
+
+        mine = [export(b) for b in list(buffers) + [sig]]
         allh = [None] * comm.world
         dist.all_gather_object(allh, mine, group=group)
-        keep = []  # the mapped neighbour tensors must outlive the run
 
         def mapped(r, k):
-            fn, args = allh[r][k]
-            t = fn(*args)
-            keep.append(t)
-            return t.data_ptr()
+            h, off = allh[r][k]
+            out = ctypes.c_void_p()
+            _lib.call("vpfv_ipc_open", (ctypes.c_ubyte * nh).from_buffer_copy(h), off, ctypes.byref(out))
+            return int(out.value)
 
-        peer_of = {}
-        for k, b in enumerate(buffers):
-            peer_of[b.data_ptr()] = (mapped(comm.left, k), mapped(comm.right, k))
+        peer_of = {b.data_ptr(): (mapped(comm.left, k), mapped(comm.right, k)) for k, b in enumerate(buffers)}
         nb = len(buffers)
         out = PeerHalo(peer_of, sig, mapped(comm.left, nb) + 8, mapped(comm.right, nb), nspecies, device)
-        out._keep = keep
         torch.cuda.synchronize(device)
         dist.barrier(group)  # every rank's words are zero before anyone signals
         return out
