@@ -258,6 +258,17 @@ int vpfv_scale(double *x, double a, long long n, void *stream);
  * calls (shared block-level code); replaces three launches per stage of
  * Simulation._stage (runner.py:183-191) for d = 1.  Nx <= vpfv_field_1d_max_cells(). */
 int vpfv_field_1d_max_cells(void);
+
+/* The same chain over ~148 CTAs: Ex = K (*) rho with green2 = the solve's
+ * Green's function K = IFFT(-i kd / k^2) stored twice (2 Nx doubles), each
+ * CTA rebuilding rho and computing E and the tables on its own cells.
+ * partials (1D-1V: one row of chunks[s] <= 16 per cell) or n given.  Agrees
+ * with the FFT path to O(eps sqrt(Nx)); Nx <= 16384. */
+int vpfv_field_1d_conv(const double *const *partials, const int *chunks, const double *vols, double *n,
+                       const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
+                       const double *green2, double *const *e, double *const *c1, double *const *packed,
+                       const double *qmk2, const double *g, const double *t1, const double *den1,
+                       const int *corrections, void *stream);
 int vpfv_field_1d(const double *const *partials, const int *rows, const int *chunks, const double *vols,
                   double *n, const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
                   const double *tw, const double *k2, const double *kd, double *const *e,

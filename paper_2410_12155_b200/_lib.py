@@ -68,6 +68,7 @@ SIGNATURES = {
     "vpfv_richardson_partials": (_i, [_p, _p, _i, _p, _p, _i, _p]),
     "vpfv_scale": (_i, [_p, _d, ctypes.c_longlong, _p]),
     "vpfv_field_1d_max_cells": (_i, []),
+    "vpfv_field_1d_conv": (_i, [_p, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_field_1d": (_i, [_p, _p, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_charge_density": (_i, [_p, _p, _i, _i, _p, _p]),
     "vpfv_poisson_1d": (_i, [_p, _p, _p, _i, _p, _p, _p, _p]),

@@ -299,6 +299,82 @@ __global__ void __launch_bounds__(1024) field1d_kernel(double *__restrict__ n, C
     FIELD_STAMP(8);
 }
 
+// The same field chain spread over the GPU: the 1D solve is the real
+// circulant map E = K (*) rho with K = IFFT(-i kd / k^2) (the spectral
+// solve's Green's function, built once on the host with numpy), so instead
+// of one CTA walking an FFT while the other SMs idle, each of ~148 CTAs
+// rebuilds rho (all Nx cells: from the 1D-1V partials or from n), takes its
+// mean, and computes E on its own few cells plus one neighbour each side
+// (a warp per cell, lanes striding the sum, shuffle reduction), then those
+// cells' table rows.  K2 = K repeated twice, so K2[m - j + Nx] needs no
+// modular index.  Rounding differs from the FFT path by O(eps sqrt(Nx)).
+__global__ void __launch_bounds__(256) field1d_conv_kernel(double *__restrict__ n, Charges q, int ns, int nx,
+                                                           double *__restrict__ rho, double *__restrict__ Ex,
+                                                           const double *__restrict__ K2, int per_cta, Tables1D T) {
+    extern __shared__ double sm1[];
+    __shared__ double red[32];
+    double *rs = sm1, *Es = sm1 + nx;  // rho (all cells), E on this CTA's cells c0-1 .. c0+M
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const bool lead = blockIdx.x == 0;
+    double acc = 0.0;
+    for (int p = tid; p < nx; p += nt) {
+        double r = 0.0;
+        for (int s = 0; s < T.ns; ++s) {
+            double ns_p;
+            if (T.part[0]) {
+                ns_p = __dmul_rn(fold_row(T.part[s] + (size_t)p * T.chunks[s], T.chunks[s]), T.vol[s]);
+                if (lead) n[(size_t)s * nx + p] = ns_p;
+            } else {
+                ns_p = n[(size_t)s * nx + p];
+            }
+            r = s == 0 ? __dmul_rn(q.q[0], ns_p) : __dadd_rn(r, __dmul_rn(q.q[s], ns_p));
+        }
+        rs[p] = r;
+        acc = __dadd_rn(acc, r);
+    }
+    const double mean = __ddiv_rn(block_tree_sum(acc, red), (double)nx);  // its barriers publish rs
+    for (int p = tid; p < nx; p += nt) {
+        const double r = __dsub_rn(rs[p], mean);
+        rs[p] = r;
+        if (lead) rho[p] = r;
+    }
+    __syncthreads();
+    const int c0 = blockIdx.x * per_cta, M = min(per_cta, nx - c0);
+    for (int o = warp; o < M + 2; o += nw) {
+        int m = c0 - 1 + o;
+        m += m < 0 ? nx : 0;
+        m -= m >= nx ? nx : 0;
+        const double *k = K2 + m + nx;  // k[-j] = K[(m - j) mod nx]
+        double e = 0.0;
+        for (int j = lane; j < nx; j += 32) e = fma(k[-j], rs[j], e);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+        if (lane == 0) Es[o] = e;
+    }
+    __syncthreads();
+    for (int o = tid; o < M; o += nt) Ex[c0 + o] = Es[o + 1];
+    for (int s = 0; s < T.ns; ++s) {
+        for (int o = tid; o < M; o += nt) {  // table1d_row's arithmetic on the staged E
+            const int i = c0 + o;
+            const double e = __dadd_rn(__dmul_rn(T.qmk2[s], Es[o + 1]), T.g[s]);
+            double c1 = __dadd_rn(T.t1[s], __ddiv_rn(__dmul_rn(T.qmk2[s], __dsub_rn(Es[o + 2], Es[o])), T.den1[s]));
+            c1 = T.corrections[s] ? c1 : 0.0;
+            if (T.packed[s]) {  // rows shifted by one; the periodic ghost rows 0 and nx+1
+                const double2 row = make_double2(e, c1), z = make_double2(0.0, 0.0);
+                for (int r : {i + 1, i == nx - 1 ? 0 : -1, i == 0 ? nx + 1 : -1}) {
+                    if (r < 0) continue;
+                    double2 *out = reinterpret_cast<double2 *>(T.packed[s] + (size_t)r * 8);
+                    out[0] = row;
+                    out[1] = out[2] = out[3] = z;
+                }
+            } else {
+                T.e[s][i] = e;
+                T.c1[s][i] = c1;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 2D: three passes over lines
 
@@ -455,6 +531,46 @@ extern "C" int vpfv_field_1d(const double *const *partials, const int *rows, con
     field1d_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, (const double2 *)tw, k2,
                                                            kd, logn >= 0, logn < 0 ? 0 : logn, T);
     return check_launch("field_1d");
+}
+
+extern "C" int vpfv_field_1d_conv(const double *const *partials, const int *chunks, const double *vols, double *n,
+                                  const double *q_host, int nspecies, int Nx, double *rho, double *Ex,
+                                  const double *green2, double *const *e, double *const *c1, double *const *packed,
+                                  const double *qmk2, const double *g, const double *t1, const double *den1,
+                                  const int *corrections, void *stream) {
+    if (nspecies < 1 || nspecies > 8) return set_error(VPFV_EARG, "field_1d_conv: 1..8 species");
+    if (Nx < 2 || Nx > 16384) return set_error(VPFV_EARG, "field_1d_conv: Nx outside [2, 16384]");
+    Charges q;
+    Tables1D T{};
+    T.ns = nspecies;
+    for (int s = 0; s < 8; ++s) q.q[s] = s < nspecies ? q_host[s] : 0.0;
+    for (int s = 0; s < nspecies; ++s) {
+        if (partials && (!partials[s] || chunks[s] < 1 || chunks[s] > 16))
+            return set_error(VPFV_EARG, "field_1d_conv: bad moment partials (one row, <= 16 chunks)");
+        T.part[s] = partials ? partials[s] : nullptr;
+        T.rows[s] = 1;
+        T.chunks[s] = partials ? chunks[s] : 0;
+        T.vol[s] = partials ? vols[s] : 0.0;
+        T.e[s] = e ? e[s] : nullptr;
+        T.c1[s] = c1 ? c1[s] : nullptr;
+        T.packed[s] = packed ? packed[s] : nullptr;
+        T.qmk2[s] = qmk2[s];
+        T.g[s] = g[s];
+        T.t1[s] = t1[s];
+        T.den1[s] = den1[s];
+        T.corrections[s] = corrections[s];
+        if (!T.packed[s] && !(T.e[s] && T.c1[s])) return set_error(VPFV_EARG, "field_1d_conv: no table outputs");
+    }
+    const int per = (Nx + 147) / 148;
+    const int grid = (Nx + per - 1) / per;
+    const size_t smem = sizeof(double) * ((size_t)Nx + per + 2);
+    static bool once = false;
+    if (!once) {
+        allow_smem((const void *)field1d_conv_kernel);
+        once = true;
+    }
+    field1d_conv_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, green2, per, T);
+    return check_launch("field_1d_conv");
 }
 
 extern "C" int vpfv_poisson_2d(const double *rho, double *Ex, double *Ey, double *phi, int Nx,

@@ -75,6 +75,12 @@ class FieldSolver:
             self.tw = dev(_twiddles(g0.N[0]))
             self.k2 = dev(k ** 2)
             self.kd = dev(kd)
+            # the solve's Green's function K (E = K (*) rho), stored twice for vpfv_field_1d_conv
+            ghat = np.zeros(g0.N[0], dtype=np.complex128)
+            nz = k != 0.0
+            ghat[nz] = -1j * kd[nz] / (k[nz] ** 2)
+            green = np.fft.ifft(ghat).real
+            self.green2 = dev(np.concatenate([green, green]))
         else:
             kx, kxd = _wavenumbers(g0.N[0], h[0])
             ky, kyd = _wavenumbers(g0.N[1], h[1])
@@ -101,12 +107,17 @@ class FieldSolver:
         total = sum(int(np.prod(sh)) for sh in partial_shapes)
         return total <= 32768 and max(512 * sh[-2] for sh in partial_shapes) <= 200 * 1024
 
-    def field_and_tables_1d(self, tables, packed, partials=None, stream=None):
+    def field_and_tables_1d(self, tables, packed, partials=None, stream=None, conv=False):
         """Moments-from-partials (when given) -> rho -> Ex -> every species'
-        line tables in one launch (vpfv_field_1d), bitwise the chain
-        moments_from_partials / charge / poisson / StageTables.update.
+        line tables in one launch.  ``conv=False``: one CTA with the FFT
+        (vpfv_field_1d), bitwise the chain moments_from_partials / charge /
+        poisson / StageTables.update; ``conv=True``: the Green's-function
+        convolution over the whole GPU (vpfv_field_1d_conv; multi-row 1D-2V
+        partials are finished by vpfv_moment_partials first).
         ``packed[s]``: species s gets the packed rows (1D-2V tiled kernel)."""
         stream = stream_handle(self.device) if stream is None else stream
+        if conv:
+            return self._field_conv_1d(tables, packed, partials, stream)
         key = (tuple(id(t) for t in tables), tuple(packed),
                None if partials is None else tuple(p.data_ptr() for p in partials))
         args = self._field1d_args.get(key)
@@ -130,6 +141,34 @@ class FieldSolver:
                 _lib.int_array([1 if t.corrections else 0 for t in tables]))
             self._field1d_args[key] = args
         _lib.call("vpfv_field_1d", *args, stream)
+        return self.E
+
+    def _field_conv_1d(self, tables, packed, partials, stream):
+        if partials is not None and any(p.shape[-2] != 1 for p in partials):
+            self.moments_from_partials(partials, stream)
+            partials = None
+        key = ("conv", tuple(id(t) for t in tables), tuple(packed),
+               None if partials is None else tuple(p.data_ptr() for p in partials))
+        args = self._field1d_args.get(key)
+        if args is None:
+            S = len(tables)
+            pk = [bool(packed[s]) and tables[s].grid.v == 2 for s in range(S)]
+            if partials is None:
+                part = (None, None, None)
+            else:
+                part = (_lib.ptr_array([p.data_ptr() for p in partials]),
+                        _lib.int_array([p.shape[-1] for p in partials]), _lib.dbl_array(self.vols))
+            args = part + (
+                self.n.data_ptr(), self.q_host, S, self.phys_shape[0], self.rho.data_ptr(),
+                self.E["Ex"].data_ptr(), self.green2.data_ptr(),
+                _lib.ptr_array([0 if pk[s] else t.e.data_ptr() for s, t in enumerate(tables)]),
+                _lib.ptr_array([0 if pk[s] else t.c1.data_ptr() for s, t in enumerate(tables)]),
+                _lib.ptr_array([t.packed.data_ptr() if pk[s] else 0 for s, t in enumerate(tables)]),
+                _lib.dbl_array([t.qmk2 for t in tables]), _lib.dbl_array([t.gx for t in tables]),
+                _lib.dbl_array([t.t1 for t in tables]), _lib.dbl_array([t.den1 for t in tables]),
+                _lib.int_array([1 if t.corrections else 0 for t in tables]))
+            self._field1d_args[key] = args
+        _lib.call("vpfv_field_1d_conv", *args, stream)
         return self.E
 
     def moments(self, srcs, stream=None):

@@ -533,6 +533,9 @@ class DistributedSimulation:
         self.overlap = (all(self.tiled) and all(lg.d == 2 for lg in self.lgrids) and self.nloc >= 2 * NGHOST + 1
                         and os.environ.get("VPFV_NO_OVERLAP") is None)
         self._N_arrays = [_lib.int_array(lg.N) for lg in self.lgrids]
+        # d = 1: the same field path as Simulation (runner.py), so slabs stay bitwise single-GPU
+        self.field_conv = (self.fields.field_1d_ok() and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
+                           and os.environ.get("VPFV_FIELD_CONV", "1") != "0")
         self.peer = None
         if halo == "peer":
             if not all(self.tiled) or self.nloc < NGHOST:
@@ -635,11 +638,15 @@ class DistributedSimulation:
         handle = self.comm.exchange_x_start(src) if overlap else self.comm.exchange_x(src)
         use_partials = self.fuse_moment and slot is not None and slot > 0
         emit = self.fuse_moment and slot is not None and slot < 3
-        E = self._solve(src, from_partials=use_partials)
+        if self.field_conv:  # Simulation's 1D field path (bitwise the same tables from the same n)
+            self._densities(src, use_partials, stream)
+            E = self.fields.field_and_tables_1d(self.gtables, self.tiled, None, stream=stream, conv=True)
+        else:
+            E = self._solve(src, from_partials=use_partials)
+            for s, gt in enumerate(self.gtables):
+                gt.update(E, stream, packed=self.tiled[s])
         n = self.nloc
         ranges = [(NGHOST, n - NGHOST), None, (0, NGHOST), (n - NGHOST, n)] if overlap else [None]
-        for s, gt in enumerate(self.gtables):
-            gt.update(E, stream, packed=self.tiled[s])
         timed = self._timing and slot is not None
         for k, r in enumerate(ranges):
             if r is None and overlap:  # the ghosts are needed from here on

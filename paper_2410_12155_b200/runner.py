@@ -119,8 +119,11 @@ class Simulation:
         # d = 1: moments-from-partials, rho, Ex and every species' tables in
         # one single-CTA launch per stage instead of 2 + 2S small ones
         self.fuse_field = self.fields.field_1d_ok() and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
-        self._finish_in_field = self.fuse_moment and self.fields.finish_in_field_1d(
-            [t.partials_shape() for t in self.tables])
+        # ... over the whole GPU (Green's-function convolution) unless VPFV_FIELD_CONV=0
+        self.field_conv = self.fuse_field and os.environ.get("VPFV_FIELD_CONV", "1") != "0"
+        self._finish_in_field = self.fuse_moment and (
+            all(t.partials_shape()[-2] == 1 for t in self.tables) if self.field_conv
+            else self.fields.finish_in_field_1d([t.partials_shape() for t in self.tables]))
         self._side = [torch.cuda.Stream(self.device) for _ in self.species[1:]]  # concurrent species
         self._diag = None
         self._last_E = None
@@ -155,7 +158,7 @@ class Simulation:
             else:
                 part = None
                 self.fields.moments(src, stream)
-            E = self.fields.field_and_tables_1d(self.tables, self.tiled, part, stream=stream)
+            E = self.fields.field_and_tables_1d(self.tables, self.tiled, part, stream=stream, conv=self.field_conv)
         elif use_partials:
             E = self.fields.solve_from_partials(self.partials if slot > 0 else self.partials_next, stream=stream)
         else:

@@ -729,8 +729,9 @@ def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
     """vpfv_field_1d (moments-from-partials + charge + Poisson + every
     species' tables in one CTA) reproduces the separate launches bitwise over
     a few steps, with and without the fused moment partials."""
-    def run(split):
+    def run(split, conv="0"):
         monkeypatch.setenv("VPFV_FIELD_SPLIT", "1" if split else "0")
+        monkeypatch.setenv("VPFV_FIELD_CONV", conv)
         sim = R.Simulation(P.make_problem(P.ProblemSpec(problem), N, Nv), dt=1e-3)
         assert sim.fuse_field is (not split)
         if problem == "dgh" and N == 64:
@@ -738,10 +739,13 @@ def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
         for _ in range(3):
             sim.advance(1e-3)
         return sim
-    a, b = run(False), run(True)
-    for x, y in zip(a.interiors(), b.interiors()):
+    a, b, c = run(False), run(True), run(False, "1")
+    for x, y, z in zip(a.interiors(), b.interiors(), c.interiors()):
         assert np.array_equal(x, y)
+        assert rel_l2(z, y) <= 1e-13  # the Green's-function convolution: rounding only
     assert torch.equal(a.fields.E["Ex"], b.fields.E["Ex"])
+    ec, eb = c.fields.E["Ex"].cpu().numpy(), b.fields.E["Ex"].cpu().numpy()
+    assert np.abs(ec - eb).max() <= 1e-12 * max(np.abs(eb).max(), 1e-300)
     for ta, tb, tiled in zip(a.tables, b.tables, a.tiled):
         if tiled and ta.grid.v == 2:
             assert torch.equal(ta.packed, tb.packed)
@@ -754,11 +758,17 @@ def test_fused_field_1d_corrections_off(monkeypatch):
     out = []
     for split in (False, True):
         monkeypatch.setenv("VPFV_FIELD_SPLIT", "1" if split else "0")
+        monkeypatch.setenv("VPFV_FIELD_CONV", "0")
         sim = R.Simulation(P.make_problem(P.ProblemSpec("dgh"), 16, 32), dt=1e-3, corrections=False)
         sim.advance(1e-3)
         out.append(sim)
     assert torch.equal(out[0].tables[0].packed, out[1].tables[0].packed)
     assert float(out[0].tables[0].packed[:, 1].abs().max()) == 0.0
+    monkeypatch.setenv("VPFV_FIELD_SPLIT", "0")
+    monkeypatch.setenv("VPFV_FIELD_CONV", "1")
+    conv = R.Simulation(P.make_problem(P.ProblemSpec("dgh"), 16, 32), dt=1e-3, corrections=False)
+    conv.advance(1e-3)
+    assert float(conv.tables[0].packed[:, 1].abs().max()) == 0.0
     assert np.array_equal(out[0].interiors()[0], out[1].interiors()[0])
 
 
