@@ -690,6 +690,28 @@ __global__ void __launch_bounds__(256) moment_partials_vec_kernel(const double *
     if (lane == 0) n[warp] = __dmul_rn(v, vol);
 }
 
+// One CTA per physical cell, one thread per vx row (Nvx a power of two,
+// 32..1024): the row's chunks folded in registers, rows 1-5 levels of the
+// tree by xor shuffles, the warp sums' levels by warp 0 -- the same
+// adjacent-pair tree as the kernels above, with Nvx threads' loads in flight
+// per cell instead of 32 (a 256-cell 1D-2V grid is 256 warps otherwise).
+template <int NLT>
+__global__ void __launch_bounds__(1024) moment_partials_row_kernel(const double *__restrict__ part,
+                                                                   double *__restrict__ n, double vol) {
+    __shared__ double wsum[32];
+    const int p = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    double v = fold_pow2<NLT>(part + ((size_t)p * blockDim.x + t) * NLT);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < nw ? wsum[lane] : 0.0;
+        for (int off = 1; off < nw; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) n[p] = __dmul_rn(v, vol);
+    }
+}
+
 template <int R>
 static bool launch_vec_r(const double *part, double *n, int nphys, int nlt, double vol, cudaStream_t s) {
     const int grid = (nphys + 7) / 8;
@@ -790,6 +812,16 @@ static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], co
 int launch_moment_from_partials(const double *part, double *n, int nphys, int nvx, int nlt, double vol,
                                 cudaStream_t s) {
     if (nlt > 16) return set_error(VPFV_EARG, "moment partials: at most 16 vy chunks");
+    if (nvx >= 32 && nvx <= 1024 && (nvx & (nvx - 1)) == 0 && (nlt & (nlt - 1)) == 0) {
+        switch (nlt) {
+            case 1: moment_partials_row_kernel<1><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+            case 2: moment_partials_row_kernel<2><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+            case 4: moment_partials_row_kernel<4><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+            case 8: moment_partials_row_kernel<8><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+            default: moment_partials_row_kernel<16><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+        }
+        return check_launch("moment_from_partials");
+    }
     bool done = false;
     switch (nvx) {
         case 32: done = launch_vec_r<1>(part, n, nphys, nlt, vol, s); break;
