@@ -152,6 +152,16 @@ int vpfv_stage_2d2v_fused_peer(double *dest, const double *A, const double *B, c
                                double *peer_hi, unsigned long long *sig_lo, unsigned long long *sig_hi,
                                unsigned *done, void *stream);
 
+/* vpfv_moment_partials (vol applied) whose results also go to every rank's
+ * density buffer: dst[k] = this slab's first cell in rank k's n (peer-mapped,
+ * own included); the last CTA then adds 1 to each sig[k] (the other ranks'
+ * density words).  The all-gather of the x-slab densities of the reference
+ * cluster's _global_density (runner.py:341-384) fused into the finish.
+ * Nvx a power of two in [32, 1024]; <= 8 ranks. */
+int vpfv_moment_partials_push(const double *partials, int nphys, int Nvx, int nchunks, double vol,
+                              double *const *dst, int ndst, unsigned long long *const *sig, int nsig,
+                              unsigned *done, void *stream);
+
 /* Signal both neighbours once (after an initial halo exchange by other means). */
 int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream);
 

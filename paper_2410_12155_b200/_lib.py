@@ -49,6 +49,7 @@ SIGNATURES = {
     "vpfv_stage_2d2v_fused_peer": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d] + [_p] + [_d] + [_p] * 3 + [_d] * 4
                                    + [_i] * 4 + [_u, _p, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_peer_signal": (_i, [_p, _p, _p]),
+    "vpfv_moment_partials_push": (_i, [_p, _i, _i, _i, _d, _p, _i, _p, _i, _p, _p]),
     "vpfv_peer_wait": (_i, [_p, _p, _i, _i, _d, _p, _p]),
     "vpfv_ipc_handle_size": (_i, []),
     "vpfv_ipc_export": (_i, [_p, _p, _p]),

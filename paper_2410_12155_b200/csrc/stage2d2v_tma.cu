@@ -712,6 +712,45 @@ __global__ void __launch_bounds__(1024) moment_partials_row_kernel(const double 
     }
 }
 
+// moment_partials_row_kernel that also stores n into every rank's density
+// buffer (peer-mapped) and, from its last CTA, bumps every other rank's
+// density signal word: the all-gather of the x-slab densities fused into
+// the finish (DistributedSimulation halo="peer").
+struct DensityPush {
+    double *dst[8];               // this slab's rows in each rank's n (own included)
+    unsigned long long *sig[8];   // the other ranks' density words
+    int ndst, nsig;
+    unsigned *done;
+};
+
+template <int NLT>
+__global__ void __launch_bounds__(1024) moment_partials_push_kernel(const double *__restrict__ part, double vol,
+                                                                    const DensityPush D) {
+    __shared__ double wsum[32];
+    const int p = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    double v = fold_pow2<NLT>(part + ((size_t)p * blockDim.x + t) * NLT);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < nw ? wsum[lane] : 0.0;
+        for (int off = 1; off < nw; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+        v = __dmul_rn(__shfl_sync(0xffffffffu, v, 0), vol);  // lanes >= nw summed zeros
+        if (lane < D.ndst) D.dst[lane][p] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (t == 0) {
+        const unsigned prev = atomicAdd(D.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *D.done = 0u;
+            __threadfence_system();
+            for (int k = 0; k < D.nsig; ++k) atomicAdd_system(D.sig[k], 1ull);
+        }
+    }
+}
+
 template <int R>
 static bool launch_vec_r(const double *part, double *n, int nphys, int nlt, double vol, cudaStream_t s) {
     const int grid = (nphys + 7) / 8;
@@ -1005,6 +1044,30 @@ extern "C" int vpfv_stage_2d2v_fused_peer(double *dest, const double *A, const d
     return stage_2d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, evy, cB, c1, c2, c3, c4, c5, hx,
                                  hy, hvx, hvy, Nx, Ny, Nvx, Nvy, 0, Nx, flags, dt_dev, cL_div, nonfinite,
                                  packed_tables, moment_partials, 0, stream, &peer);
+}
+
+extern "C" int vpfv_moment_partials_push(const double *partials, int nphys, int Nvx, int nchunks, double vol,
+                                         double *const *dst, int ndst, unsigned long long *const *sig, int nsig,
+                                         unsigned *done, void *stream) {
+    if (ndst < 1 || ndst > 8 || nsig < 0 || nsig > 8 || !done)
+        return set_error(VPFV_EARG, "moment_partials_push: 1..8 destinations, 0..8 signals, a done counter");
+    if (Nvx < 32 || Nvx > 1024 || (Nvx & (Nvx - 1)) || nchunks < 1 || nchunks > 16 || (nchunks & (nchunks - 1)))
+        return set_error(VPFV_EARG, "moment_partials_push: Nvx a power of two in [32, 1024], chunks in {1..16}");
+    DensityPush D{};
+    for (int k = 0; k < ndst; ++k) D.dst[k] = dst[k];
+    for (int k = 0; k < nsig; ++k) D.sig[k] = sig[k];
+    D.ndst = ndst;
+    D.nsig = nsig;
+    D.done = done;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (nchunks) {
+        case 1: moment_partials_push_kernel<1><<<nphys, Nvx, 0, s>>>(partials, vol, D); break;
+        case 2: moment_partials_push_kernel<2><<<nphys, Nvx, 0, s>>>(partials, vol, D); break;
+        case 4: moment_partials_push_kernel<4><<<nphys, Nvx, 0, s>>>(partials, vol, D); break;
+        case 8: moment_partials_push_kernel<8><<<nphys, Nvx, 0, s>>>(partials, vol, D); break;
+        default: moment_partials_push_kernel<16><<<nphys, Nvx, 0, s>>>(partials, vol, D); break;
+    }
+    return check_launch("moment_partials_push");
 }
 
 extern "C" int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, int nchunks,

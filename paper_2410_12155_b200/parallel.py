@@ -289,6 +289,34 @@ class SlabExchange:
         return bool(t.item())
 
 
+def _ipc_export(t):
+    """(handle bytes, offset) of a device tensor's allocation (vpfv_ipc_export)."""
+    import ctypes
+
+    nh = _lib.load().vpfv_ipc_handle_size()
+    h = (ctypes.c_ubyte * nh)()
+    off = ctypes.c_longlong()
+    _lib.call("vpfv_ipc_export", t.data_ptr(), h, ctypes.byref(off))
+    return bytes(h), off.value
+
+
+def _ipc_open(handle, offset):
+    """Device pointer of another process's buffer, mapped with peer access (vpfv_ipc_open)."""
+    import ctypes
+
+    out = ctypes.c_void_p()
+    _lib.call("vpfv_ipc_open", (ctypes.c_ubyte * len(handle)).from_buffer_copy(handle), offset, ctypes.byref(out))
+    return int(out.value)
+
+
+def _ipc_all_gather(tensors, group, world):
+    """Every rank's exported handles of ``tensors`` (collective): [rank][k]."""
+    mine = [_ipc_export(t) for t in tensors]
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    return allh
+
+
 class PeerHalo:
     """Pointers and signal words of the fused x-halo push for one rank.
 
@@ -333,27 +361,9 @@ class PeerHalo:
         device's context with peer access (``vpfv_ipc_export`` /
         ``vpfv_ipc_open``), so the stage kernel's stores and the signal
         atomics go over NVLink.  Collective over ``group``."""
-        import ctypes
-
-        nh = _lib.load().vpfv_ipc_handle_size()
         sig = torch.zeros(2, dtype=torch.int64, device=device)
-
-        def export(t):
-            h = (ctypes.c_ubyte * nh)()
-            off = ctypes.c_longlong()
-            _lib.call("vpfv_ipc_export", t.data_ptr(), h, ctypes.byref(off))
-            return bytes(h), off.value
-
-        mine = [export(b) for b in list(buffers) + [sig]]
-        allh = [None] * comm.world
-        dist.all_gather_object(allh, mine, group=group)
-
-        def mapped(r, k):
-            h, off = allh[r][k]
-            out = ctypes.c_void_p()
-            _lib.call("vpfv_ipc_open", (ctypes.c_ubyte * nh).from_buffer_copy(h), off, ctypes.byref(out))
-            return int(out.value)
-
+        allh = _ipc_all_gather(list(buffers) + [sig], group, comm.world)
+        mapped = lambda r, k: _ipc_open(*allh[r][k])  # noqa: E731
         peer_of = {b.data_ptr(): (mapped(comm.left, k), mapped(comm.right, k)) for k, b in enumerate(buffers)}
         nb = len(buffers)
         out = PeerHalo(peer_of, sig, mapped(comm.left, nb) + 8, mapped(comm.right, nb), nspecies, device)
@@ -521,8 +531,15 @@ class DistributedSimulation:
         phys_loc = (self.nloc,) + tuple(g0.N[1:g0.d])
         self.n_local = torch.empty((S,) + phys_loc, dtype=torch.float64, device=self.device)  # unit-volume folds
         self.fuse_moment = all(self.tiled)
-        self.partials = ([torch.empty(_GridView(t, lg).partials_shape(), dtype=torch.float64, device=self.device)
-                          for t, lg in zip(self.gtables, self.lgrids)] if self.fuse_moment else None)
+        mk = lambda: ([torch.empty(_GridView(t, lg).partials_shape(), dtype=torch.float64, device=self.device)  # noqa: E731
+                       for t, lg in zip(self.gtables, self.lgrids)] if self.fuse_moment else None)
+        # as in Simulation: stages 1-3 emit the moment partials of their dest
+        # (the next stage's src); stage 4's, of the new f0, serve the next
+        # step's stage 1 unless f0 was modified in place since
+        self.partials = mk()
+        self.partials_next = mk()
+        self._moment_of = None
+        self._cached = False
         self.nonfinite = torch.full((4, S), -1, dtype=torch.int64, device=self.device)
         self.dt_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._timing = False
@@ -542,6 +559,7 @@ class DistributedSimulation:
                 raise ValueError("halo='peer' needs the tiled 2D-2V path and slabs of >= 3 planes")
             bufs = [a for trio in zip(self.ctx.f0, self.ctx.f1, self.ctx.fout) for a in trio]
             self.peer = PeerHalo.ipc(bufs, self.comm, group, S, self.device)
+            self._setup_density_push(group)
             # the t = 0 ghosts by one ordinary exchange, then the first signal
             for trio in (self.ctx.f0, self.ctx.f1, self.ctx.fout):
                 self.comm.exchange_x(trio)
@@ -580,15 +598,67 @@ class DistributedSimulation:
     def step_count(self):
         return self.ctx.step
 
-    def _densities(self, srcs, from_partials, stream):
-        """Box fold sums (unit volume) -> gathered, combined across the
-        velocity partitions in fold-tree order, times the velocity volume:
-        the global n in self.fields.n, bitwise the single-GPU moment."""
+    def _setup_density_push(self, group):
+        """Peer mode: the slab densities go straight into every rank's
+        density buffer from the moment finish (vpfv_moment_partials_push),
+        double-buffered by push parity (a rank pushing stage k+1's n cannot
+        overwrite a buffer another rank still reads: it first needs that
+        rank's stage-k push, which follows its stage-k reads in stream order),
+        plus one density signal word per rank."""
+        self._dpush = None
+        if not self.fuse_moment or self.world > 8:
+            return
+        shapes = [p.shape for p in self.partials]
+        if not all(sh[-2] >= 32 and sh[-2] <= 1024 and sh[-2] & (sh[-2] - 1) == 0 and sh[-1] & (sh[-1] - 1) == 0
+                   and sh[-1] <= 16 for sh in shapes):
+            return
+        S, P, me = len(self.species), self.world, self.rank
+        g0 = self.grids[0]
+        Nx, Ny = g0.N[0], g0.N[1]
+        nbufs = torch.zeros((2, S, Nx, Ny), dtype=torch.float64, device=self.device)
+        dsig = torch.zeros(2, dtype=torch.int64, device=self.device)
+        allh = _ipc_all_gather([nbufs, dsig], group, P)
+        nptr = [nbufs.data_ptr() if q == me else _ipc_open(*allh[q][0]) for q in range(P)]
+        sptr = [_ipc_open(*allh[q][1]) for q in range(P) if q != me]
+        dests = [[_lib.ptr_array([nptr[q] + ((par * S + s) * Nx * Ny + self.x0 * Ny) * 8 for q in range(P)])
+                  for s in range(S)] for par in range(2)]
+        self._dpush = dict(nbufs=nbufs, dsig=dsig, dests=dests, sigs=_lib.ptr_array(sptr),
+                           consumed=torch.zeros(2, dtype=torch.int64, device=self.device),
+                           timed_out=torch.zeros(1, dtype=torch.int32, device=self.device),
+                           done=torch.zeros(S, dtype=torch.int32, device=self.device), count=0)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group)
+
+    def _densities_push(self, part, stream):
+        """Global n from every rank's pushes of this stage (see _setup_density_push)."""
+        d, S, P = self._dpush, len(self.species), self.world
+        par = d["count"] & 1
+        nphys = self.nloc * self.grids[0].N[1]
+        for s in range(S):
+            _lib.call("vpfv_moment_partials_push", part[s].data_ptr(), nphys, part[s].shape[-2], part[s].shape[-1],
+                      self.fields.vols[s], d["dests"][par][s], P, d["sigs"], P - 1, d["done"][s:s + 1].data_ptr(),
+                      stream)
+        _lib.call("vpfv_peer_wait", d["dsig"].data_ptr(), d["consumed"].data_ptr(), S * (P - 1), 0,
+                  float(self.peer.timeout_s), d["timed_out"].data_ptr(), stream)
+        self.fields.n.copy_(d["nbufs"][par])
+        d["count"] += 1
+
+    def _partials_for(self, slot):
+        """(partials this stage's density reads or None, partials its stage kernels emit or None)."""
+        if not self.fuse_moment or slot is None:
+            return None, None
+        use = self.partials if slot > 0 else (self.partials_next if self._cached else None)
+        return use, (self.partials if slot < 3 else self.partials_next)
+
+    def _densities(self, srcs, part, stream):
+        """Box fold sums (unit volume; from the fused partials ``part`` or a
+        moment pass) -> gathered, combined across the velocity partitions in
+        fold-tree order, times the velocity volume: the global n in
+        self.fields.n, bitwise the single-GPU moment."""
         for s, (lg, f) in enumerate(zip(self.lgrids, srcs)):
-            if from_partials:
-                _lib.call("vpfv_moment_partials", self.partials[s].data_ptr(), self.n_local[s].data_ptr(),
-                          int(np.prod(lg.N[:lg.d])), self.partials[s].shape[-2], self.partials[s].shape[-1], 1.0,
-                          stream)
+            if part is not None:
+                _lib.call("vpfv_moment_partials", part[s].data_ptr(), self.n_local[s].data_ptr(),
+                          int(np.prod(lg.N[:lg.d])), part[s].shape[-2], part[s].shape[-1], 1.0, stream)
             else:
                 _lib.call("vpfv_moment", f.data_ptr(), self.n_local[s].data_ptr(), lg.d, lg.v,
                           self._N_arrays[s], 1.0, stream)
@@ -597,9 +667,9 @@ class DistributedSimulation:
         for s in range(len(self.species)):
             _lib.call("vpfv_scale", self.fields.n[s].data_ptr(), self.fields.vols[s], per, stream)
 
-    def _solve(self, srcs, from_partials=False):
+    def _solve(self, srcs, part=None):
         stream = stream_handle(self.device)
-        self._densities(srcs, from_partials, stream)
+        self._densities(srcs, part, stream)
         self.fields.charge(stream)
         return self.fields.poisson(self.fields.rho, False, stream)
 
@@ -609,11 +679,16 @@ class DistributedSimulation:
         neighbours' pushes of the previous stage (src's ghost planes), then
         the stage launches, which push dest's boundary planes onward."""
         stream = stream_handle(self.device)
-        E = self._solve(src, from_partials=self.fuse_moment and slot is not None and slot > 0)
+        use, emit = self._partials_for(slot)
+        if use is not None and self._dpush is not None:
+            self._densities_push(use, stream)
+            self.fields.charge(stream)
+            E = self.fields.poisson(self.fields.rho, False, stream)
+        else:
+            E = self._solve(src, use)
         for s, gt in enumerate(self.gtables):
             gt.update(E, stream, packed=True)
         self.peer.wait(stream)
-        emit = self.fuse_moment and slot is not None and slot < 3
         timed = self._timing and slot is not None
         for s, lt in enumerate(self.tables):
             nf = None if slot is None else self.nonfinite[slot, s:s + 1]
@@ -621,7 +696,7 @@ class DistributedSimulation:
                 self._events[slot][s][0].record()
             launch_stage_peer(lt, dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream,
                               self.peer.push_args(dest[s], s), dt_dev=dt_dev, cL_div=cL_div, nonfinite=nf,
-                              partials=self.partials[s] if emit else None)
+                              partials=emit[s] if emit else None)
             if timed:
                 self._events[slot][s][1].record()
 
@@ -636,13 +711,12 @@ class DistributedSimulation:
         overlap = self.overlap and self.comm.px > 1
         self.comm.exchange_v(src, self.vdim)  # velocity faces first: the x planes sent next carry them
         handle = self.comm.exchange_x_start(src) if overlap else self.comm.exchange_x(src)
-        use_partials = self.fuse_moment and slot is not None and slot > 0
-        emit = self.fuse_moment and slot is not None and slot < 3
+        use, emit = self._partials_for(slot)
         if self.field_conv:  # Simulation's 1D field path (bitwise the same tables from the same n)
-            self._densities(src, use_partials, stream)
+            self._densities(src, use, stream)
             E = self.fields.field_and_tables_1d(self.gtables, self.tiled, None, stream=stream, conv=True)
         else:
-            E = self._solve(src, from_partials=use_partials)
+            E = self._solve(src, use)
             for s, gt in enumerate(self.gtables):
                 gt.update(E, stream, packed=self.tiled[s])
         n = self.nloc
@@ -657,7 +731,7 @@ class DistributedSimulation:
                 if timed and k == 0:  # (with overlap: first interior launch .. last boundary launch)
                     self._events[slot][s][0].record()
                 lt.launch(dest[s], A[s], B[s], src[s], ca, cb, cd, cL, self.flags[s], stream, dt_dev=dt_dev,
-                          cL_div=cL_div, nonfinite=nf, partials=self.partials[s] if emit else None,
+                          cL_div=cL_div, nonfinite=nf, partials=emit[s] if emit else None,
                           packed=self.tiled[s], x_range=r)
                 if timed and k == len(ranges) - 1:
                     self._events[slot][s][1].record()
@@ -667,9 +741,12 @@ class DistributedSimulation:
         start = _lib.launch_counter[0]
         bufs = {"f0": self.ctx.f0, "f1": self.ctx.f1, "fout": self.ctx.fout}
         self.nonfinite.fill_(-1)
+        sig = lambda arrays: tuple((a.data_ptr(), a._version) for a in arrays)  # noqa: E731
+        self._cached = self.fuse_moment and self._moment_of == sig(self.ctx.f0)
         for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, slot,
                         dt_dev=self.dt_dev, cL_div=div)
+        self._moment_of = sig(self.ctx.fout) if self.fuse_moment else None  # the next f0
         self._launches = _lib.launch_counter[0] - start
 
     def launches_per_step(self):
@@ -708,6 +785,8 @@ class DistributedSimulation:
                     self._stage_ms[slot] += a.elapsed_time(b)
         if self.peer is not None:
             self.peer.check()
+            if self._dpush is not None and int(self._dpush["timed_out"].item()):
+                raise RuntimeError("peer densities: another rank's push did not arrive (timed out)")
         self.ctx.t = self.ctx.t + dt
         self.ctx.rotate()
         flags = self.nonfinite[3].cpu().numpy().astype(np.uint64)
