@@ -79,7 +79,7 @@ def make_setup(name, world=1):
     raise ValueError(name)
 
 
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_rb_final_summary.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_end_rb_summary.json")
 
 
 def load_traffic():

@@ -35,21 +35,24 @@ SCALE = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3,
 
 
 def raw(report):
-    """Metric values of the first profiled launch, bytes in GB and times in ms."""
+    """Metric values of every profiled launch in a report (one dict each),
+    bytes in GB and times in ms."""
     out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = csv.reader(io.StringIO(out))
     h = next(r)
     units = next(r)
-    vals = next(r)
-    d = {}
-    for k, u, v in zip(h, units, vals):
-        if u in SCALE and v not in ("", "n/a"):
-            try:
-                v = str(float(v.replace(",", "")) * SCALE[u])
-            except ValueError:
-                pass
-        d[k] = v
-    return d
+    launches_ = []
+    for vals in r:
+        d = {}
+        for k, u, v in zip(h, units, vals):
+            if u in SCALE and v not in ("", "n/a"):
+                try:
+                    v = str(float(v.replace(",", "")) * SCALE[u])
+                except ValueError:
+                    pass
+            d[k] = v
+        launches_.append(d)
+    return launches_
 
 
 def stalls(d, n=6):
@@ -89,11 +92,11 @@ def main():
     ap.add_argument("--title", default="ncu summary")
     ap.add_argument("--cells", type=float, default=128 ** 4)
     args = ap.parse_args()
-    labels = args.labels or [f"capture {i}" for i in range(len(args.reports))]
+    caps = [d for rep in args.reports for d in raw(rep)]  # every launch of every report, in order
+    labels = args.labels or [f"capture {i}" for i in range(len(caps))]
     summary = {"captures": [], "launch_list": launches(args.launches) if args.launches else None}
     lines = [f"# {args.title}", ""]
-    for lab, rep in zip(labels, args.reports):
-        d = raw(rep)
+    for lab, d in zip(labels, caps):
         row = {k: (float(d[v]) if v in d and d[v] not in ("", "n/a") else None) for k, v in KEYS.items()}
         row["label"] = lab
         row["kernel"] = d.get("Kernel Name", "")[:90]
