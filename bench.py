@@ -51,7 +51,7 @@ KERNEL_OF = {  # the dominant (stage) kernel of each workload
     "landau2d-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "ep2d2v-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "weibel-256": "stage1d2v_rb_kernel (fused 1D-2V RHS + RK4 update, TMA-tiled)",
-    "twostream-1024": "stage_1d1v_kernel (fused 1D-1V RHS + RK4 update)",
+    "twostream-1024": "stage_1d1v_march_kernel (fused 1D-1V RHS + RK4 update, x-marching, bulk-copied rows)",
     "landau1d-128": "stage_1d1v_kernel (fused 1D-1V RHS + RK4 update)",
 }
 
