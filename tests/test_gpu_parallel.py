@@ -226,8 +226,9 @@ def test_peer_halo_two_processes_same_gpu():
     """DistributedSimulation(halo="peer") with two processes sharing the GPU:
     each maps the other's state buffers and signal words by CUDA IPC, the
     stage kernels push the x halo across the processes, and the gathered
-    state is bitwise the single-GPU Simulation."""
-    names = ["landau2d"]
+    state is bitwise the single-GPU Simulation (one and two species: the
+    waits count one signal per species and neighbour)."""
+    names = ["landau2d", "ep"]
     refs = {n: _reference(n, 2) for n in names}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
