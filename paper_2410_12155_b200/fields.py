@@ -123,7 +123,6 @@ class FieldSolver:
         args = self._field1d_args.get(key)
         if args is None:
             S = len(tables)
-            pk = [bool(packed[s]) and tables[s].grid.v == 2 for s in range(S)]
             if partials is None:
                 part = (None, None, None, None)
             else:
@@ -133,15 +132,22 @@ class FieldSolver:
             args = part + (
                 self.n.data_ptr(), self.q_host, S, self.phys_shape[0], self.rho.data_ptr(),
                 self.E["Ex"].data_ptr(), self.tw.data_ptr(), self.k2.data_ptr(), self.kd.data_ptr(),
-                _lib.ptr_array([0 if pk[s] else t.e.data_ptr() for s, t in enumerate(tables)]),
+                *self._table_args(tables, packed))
+            self._field1d_args[key] = args
+        _lib.call("vpfv_field_1d", *args, stream)
+        return self.E
+
+    @staticmethod
+    def _table_args(tables, packed):
+        """Per-species table outputs and constants of vpfv_field_1d[_conv]:
+        packed rows for the tiled 1D-2V species, plain e/c1 otherwise."""
+        pk = [bool(packed[s]) and t.grid.v == 2 for s, t in enumerate(tables)]
+        return (_lib.ptr_array([0 if pk[s] else t.e.data_ptr() for s, t in enumerate(tables)]),
                 _lib.ptr_array([0 if pk[s] else t.c1.data_ptr() for s, t in enumerate(tables)]),
                 _lib.ptr_array([t.packed.data_ptr() if pk[s] else 0 for s, t in enumerate(tables)]),
                 _lib.dbl_array([t.qmk2 for t in tables]), _lib.dbl_array([t.gx for t in tables]),
                 _lib.dbl_array([t.t1 for t in tables]), _lib.dbl_array([t.den1 for t in tables]),
                 _lib.int_array([1 if t.corrections else 0 for t in tables]))
-            self._field1d_args[key] = args
-        _lib.call("vpfv_field_1d", *args, stream)
-        return self.E
 
     def _field_conv_1d(self, tables, packed, partials, stream):
         if partials is not None and any(p.shape[-2] != 1 for p in partials):
@@ -152,7 +158,6 @@ class FieldSolver:
         args = self._field1d_args.get(key)
         if args is None:
             S = len(tables)
-            pk = [bool(packed[s]) and tables[s].grid.v == 2 for s in range(S)]
             if partials is None:
                 part = (None, None, None)
             else:
@@ -160,13 +165,7 @@ class FieldSolver:
                         _lib.int_array([p.shape[-1] for p in partials]), _lib.dbl_array(self.vols))
             args = part + (
                 self.n.data_ptr(), self.q_host, S, self.phys_shape[0], self.rho.data_ptr(),
-                self.E["Ex"].data_ptr(), self.green2.data_ptr(),
-                _lib.ptr_array([0 if pk[s] else t.e.data_ptr() for s, t in enumerate(tables)]),
-                _lib.ptr_array([0 if pk[s] else t.c1.data_ptr() for s, t in enumerate(tables)]),
-                _lib.ptr_array([t.packed.data_ptr() if pk[s] else 0 for s, t in enumerate(tables)]),
-                _lib.dbl_array([t.qmk2 for t in tables]), _lib.dbl_array([t.gx for t in tables]),
-                _lib.dbl_array([t.t1 for t in tables]), _lib.dbl_array([t.den1 for t in tables]),
-                _lib.int_array([1 if t.corrections else 0 for t in tables]))
+                self.E["Ex"].data_ptr(), self.green2.data_ptr(), *self._table_args(tables, packed))
             self._field1d_args[key] = args
         _lib.call("vpfv_field_1d_conv", *args, stream)
         return self.E
