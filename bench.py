@@ -256,33 +256,16 @@ def run_b200(args, rank, world, device):
             torch.distributed.barrier()
         torch.cuda.synchronize(device)
 
-    # Stage-kernel launch durations come from CUDA events captured around
-    # every stage launch into the step graph.  On steps of a millisecond or
-    # more (the 2D-2V and 1D-2V workloads) those event nodes cost nothing
-    # measurable and ride in the timed region itself; on the short 1D steps
-    # they cost ~8 us each (+60% on a 128^2 step), so there the timed region
-    # runs the plain graph and the durations come from a second pass of the
-    # same K steps with the events.
+    # The timed region replays the plain step graph.  The stage kernels'
+    # launch durations come from CUDA events captured around every stage
+    # launch into the graph, in a second pass of the same K steps: those event
+    # nodes cost ~8 us each on a 1D step (+60% at 128^2) and break up the
+    # concurrent species branches of a two-species step (+13% on ep2d2v-64).
     sim.enable_stage_timing(False)
     for _ in range(args.warmup):
         sim.advance(dt)
     barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    sim.advance(dt)
-    stop.record(stream)
-    barrier()
-    one = start.elapsed_time(stop)
-    if world > 1:  # every rank takes the same branch (graph variants, barriers)
-        t1 = torch.tensor([one], dtype=torch.float64, device=device)
-        torch.distributed.all_reduce(t1, op=torch.distributed.ReduceOp.MAX)
-        one = float(t1.item())
-    short = one < 1.0
-    sim.enable_stage_timing(not short)
-    sim.advance(dt)  # captures the graph variant the timed region replays
-    sim.enable_stage_timing(not short)  # reset the accumulators
-    barrier()
-    ms_roofline_pass = None
     with ClockSampler(device.index) as clocks:
         start.record(stream)
         for _ in range(args.steps):
@@ -290,17 +273,16 @@ def run_b200(args, rank, world, device):
         stop.record(stream)
         barrier()
         ms_local = start.elapsed_time(stop)
-        if short:
-            sim.enable_stage_timing(True)
+        sim.enable_stage_timing(True)
+        sim.advance(dt)  # captures the evented graph variant
+        sim.enable_stage_timing(True)  # reset the accumulators
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
             sim.advance(dt)
-            sim.enable_stage_timing(True)
-            barrier()
-            start.record(stream)
-            for _ in range(args.steps):
-                sim.advance(dt)
-            stop.record(stream)
-            barrier()
-            ms_roofline_pass = start.elapsed_time(stop)
+        stop.record(stream)
+        barrier()
+        ms_roofline_pass = start.elapsed_time(stop)
     stage_ms = sim.stage_kernel_ms()  # per RK stage slot, summed over the pass's steps and species
     sim.enable_stage_timing(False)
     ms = ms_local
@@ -354,10 +336,9 @@ def run_b200(args, rank, world, device):
                      "algorithmic_bytes_per_cell_per_step": sum(STAGE_BYTES),
                      "stage_ms_per_step": [m / args.steps for m in stage_ms],
                      "share_of_step": share, "peak_kind": peak_kind,
-                     "timing": ("stage-kernel launch durations from CUDA events captured around every "
-                                "stage launch inside the timed region" if ms_roofline_pass is None else
-                                f"stage-kernel launch durations from CUDA events captured around every "
-                                f"stage launch in a second pass of the same {args.steps} steps "
+                     "timing": (f"stage-kernel launch durations from CUDA events captured around every "
+                                f"stage launch in a second pass of the same {args.steps} steps, right after "
+                                f"the timed region, under the same clock sampling "
                                 f"({ms_roofline_pass / args.steps:.3f} ms/step with the event nodes; the "
                                 f"timed region replays the plain graph)")},
         "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
