@@ -273,10 +273,11 @@ def run_b200(args, rank, world, device):
         stop.record(stream)
         barrier()
         ms_local = start.elapsed_time(stop)
-        sim.enable_stage_timing(True)
-        sim.advance(dt)  # captures the evented graph variant
-        sim.enable_stage_timing(True)  # reset the accumulators
-        barrier()
+    sim.enable_stage_timing(True)
+    sim.advance(dt)  # captures the evented graph variant
+    sim.enable_stage_timing(True)  # reset the accumulators
+    barrier()
+    with ClockSampler(device.index) as clocks_rp:
         start.record(stream)
         for _ in range(args.steps):
             sim.advance(dt)
@@ -340,7 +341,8 @@ def run_b200(args, rank, world, device):
                                 f"stage launch in a second pass of the same {args.steps} steps, right after "
                                 f"the timed region, under the same clock sampling "
                                 f"({ms_roofline_pass / args.steps:.3f} ms/step with the event nodes; the "
-                                f"timed region replays the plain graph)")},
+                                f"timed region replays the plain graph)"),
+                     "clocks_roofline_pass": clocks_rp.summary()},
         "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
                           "frac": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9 / peak},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
