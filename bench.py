@@ -277,6 +277,8 @@ def run_b200(args, rank, world, device):
     sim.advance(dt)  # captures the evented graph variant
     sim.enable_stage_timing(True)  # reset the accumulators
     barrier()
+    time.sleep(1.0)  # let the power limiter recover (sw_power_cap) so both passes start alike
+    barrier()
     with ClockSampler(device.index) as clocks_rp:
         start.record(stream)
         for _ in range(args.steps):
