@@ -724,7 +724,7 @@ def test_1d1v_fused_moment_partials_fold_tree(N):
 
 @pytest.mark.parametrize("problem,N,Nv", [("two-stream", 16, 16), ("two-stream", 32, 128), ("lhdi", 8, 8),
                                           ("lhdi", 16, 32), ("dgh", 16, 32), ("weibel", 16, 32),
-                                          ("dgh", 64, 128)])
+                                          ("dgh", 64, 128), ("two-stream", 24, 128)])
 def test_fused_field_1d_equals_split_chain(problem, N, Nv, monkeypatch):
     """vpfv_field_1d (moments-from-partials + charge + Poisson + every
     species' tables in one CTA) reproduces the separate launches bitwise over
@@ -820,3 +820,36 @@ def test_1d1v_march_equals_generic(N, periodic_x, monkeypatch):
         torch.cuda.synchronize()
         flagged.append(int(nf.item()))
     assert flagged[0] == flagged[1] != -1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nphys,nvx,nlt", [(5, 32, 1), (3, 64, 16), (4, 1024, 2), (2, 256, 8), (3, 48, 4)])
+def test_moment_partials_finish_is_the_fold_tree(nphys, nvx, nlt):
+    """vpfv_moment_partials on random chunk sums equals the reference fold
+    tree over (vx rows, chunk columns) -- the row-parallel kernel for
+    power-of-two Nvx, the warp-per-cell kernel otherwise -- times vol."""
+    rng = np.random.default_rng(nphys * nvx + nlt)
+    part = rng.standard_normal((nphys, nvx, nlt))
+    want = np.array([O.fold_tree_sum(part[p], (0, 1)) * 0.37 for p in range(nphys)])
+    d = torch.from_numpy(part).cuda()
+    n = torch.empty(nphys, dtype=torch.float64, device="cuda")
+    _lib.call("vpfv_moment_partials", d.data_ptr(), n.data_ptr(), nphys, nvx, nlt, 0.37, K.stream_handle())
+    torch.cuda.synchronize()
+    assert np.array_equal(n.cpu().numpy(), want)
+
+
+@pytest.mark.gpu
+def test_peer_wait_times_out_instead_of_hanging():
+    """A neighbour that never signals: vpfv_peer_wait gives up after its
+    timeout and raises the flag (the device is not left spinning)."""
+    sig = torch.zeros(2, dtype=torch.int64, device="cuda")
+    consumed = torch.zeros(2, dtype=torch.int64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("vpfv_peer_wait", sig.data_ptr(), consumed.data_ptr(), 1, 1, 0.05, flag.data_ptr(), K.stream_handle())
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 1
+    sig.fill_(1)  # the signals arrive: the next wait passes and consumes them
+    flag.zero_()
+    _lib.call("vpfv_peer_wait", sig.data_ptr(), consumed.data_ptr(), 1, 1, 5.0, flag.data_ptr(), K.stream_handle())
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0 and consumed.tolist() == [1, 1]
