@@ -266,7 +266,13 @@ class Simulation:
 
     # -- timestep control -----------------------------------------------------
     def _E_host(self, arrays):
-        E = self.fields.solve(arrays)
+        if arrays is self.ctx.f0 and self.fuse_moment and self._moment_of == self._signature(self.ctx.f0):
+            # stage 4 left the fused moment partials of this f0: the CFL mode's
+            # extra field solve per step (runner.py:199-205) and the
+            # diagnostics rows cost a moment finish, not a pass over f
+            E = self.fields.solve_from_partials(self.partials_next)
+        else:
+            E = self.fields.solve(arrays)
         return {k: v.cpu().numpy() for k, v in E.items()}
 
     def max_dt(self):

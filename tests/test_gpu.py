@@ -853,3 +853,24 @@ def test_peer_wait_times_out_instead_of_hanging():
     _lib.call("vpfv_peer_wait", sig.data_ptr(), consumed.data_ptr(), 1, 1, 5.0, flag.data_ptr(), K.stream_handle())
     torch.cuda.synchronize()
     assert int(flag.item()) == 0 and consumed.tolist() == [1, 1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem,N,Nv", [("landau", 16, 16), ("two-stream", 32, 128), ("dgh", 16, 32)])
+def test_cfl_solve_from_cached_partials(problem, N, Nv):
+    """After a step, max_dt (the CFL mode's per-step solve) takes the density
+    from stage 4's fused partials instead of a moment pass over f0: the same
+    E bit for bit, hence the same dt; an in-place edit of f0 falls back."""
+    sim = R.Simulation(P.make_problem(P.ProblemSpec(problem), N, Nv))
+    dt = sim.max_dt()
+    sim.advance(0.5 * dt)
+    assert sim.fuse_moment and sim._moment_of == sim._signature(sim.ctx.f0)
+    a = sim._E_host(sim.ctx.f0)
+    b = {k: v.cpu().numpy() for k, v in sim.fields.solve(sim.ctx.f0).items()}
+    for k in b:
+        assert np.array_equal(a[k], b[k])
+    sim.ctx.f0[0].mul_(1.0)  # bumps the tensor version: the partials no longer describe f0
+    assert sim._moment_of != sim._signature(sim.ctx.f0)
+    c = sim._E_host(sim.ctx.f0)
+    for k in b:
+        assert np.array_equal(c[k], b[k])
