@@ -765,7 +765,9 @@ class DistributedSimulation:
 
     # ------------------------------------------------------------------
     def max_dt(self):
-        E = self._solve(self.ctx.f0)
+        sig = tuple((a.data_ptr(), a._version) for a in self.ctx.f0)
+        cached = self.fuse_moment and self._moment_of == sig  # stage 4's partials describe f0
+        E = self._solve(self.ctx.f0, self.partials_next if cached else None)
         return stable_dt(self.grids, self.species, {k: v.cpu().numpy() for k, v in E.items()}, self.sigma)
 
     def current_dt(self):
