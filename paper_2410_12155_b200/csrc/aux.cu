@@ -1,5 +1,6 @@
 // Per-stage line tables, charge density, ghost wraps, box copies, errors.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -12,6 +13,11 @@ static thread_local char g_err[256] = "";
 int set_error(int code, const char *msg) {
     snprintf(g_err, sizeof g_err, "%s", msg);
     return code;
+}
+
+bool pdl_enabled() {
+    const char *e = getenv("VPFV_PDL");
+    return !(e && e[0] == '0');
 }
 
 int check_launch(const char *what) {

@@ -18,4 +18,32 @@ __device__ __forceinline__ double ldg(const double *p) { return __ldg(p); }
 int set_error(int code, const char *msg);
 int check_launch(const char *what);
 
+// Programmatic dependent launch (the short 1D chains): a kernel launched with
+// launch_pdl may start while its predecessor in the stream drains; it runs
+// its independent prologue, then pdl_wait() before touching anything the
+// predecessor wrote.  pdl_trigger() lets the successor start launching --
+// only in kernels whose successor is always PDL-aware (the 1D field kernel,
+// followed by the stage kernels): measured, a stage kernel that triggered
+// let the ordinary moment launch after it read a half-written f.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // VPFV_PDL != 0
+
+template <typename... Args>
+cudaError_t launch_pdl(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 }  // namespace vpfv

@@ -316,6 +316,8 @@ __global__ void __launch_bounds__(256) field1d_conv_kernel(double *__restrict__ 
     double *rs = sm1, *Es = sm1 + nx;  // rho (all cells), E on this CTA's cells c0-1 .. c0+M
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const bool lead = blockIdx.x == 0;
+    pdl_trigger();  // the stage kernel after this may start launching
+    pdl_wait();     // the partials / n of the previous stage
     double acc = 0.0;
     for (int p = tid; p < nx; p += nt) {
         double r = 0.0;
@@ -569,7 +571,13 @@ extern "C" int vpfv_field_1d_conv(const double *const *partials, const int *chun
         allow_smem((const void *)field1d_conv_kernel);
         once = true;
     }
-    field1d_conv_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, green2, per, T);
+    if (partials) {  // after a (triggering) stage kernel: programmatic launch
+        const cudaError_t rc = launch_pdl(field1d_conv_kernel, dim3(grid), dim3(256), smem, (cudaStream_t)stream, n,
+                                          q, nspecies, Nx, rho, Ex, green2, per, T);
+        if (rc != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(rc));
+    } else {  // after the separate moment kernel: an ordinary launch
+        field1d_conv_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, green2, per, T);
+    }
     return check_launch("field_1d_conv");
 }
 

@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(256) stage_1d1v_kernel(Update u, const double 
     const long long P1 = Nv + 2 * NG;
     const long long c = (long long)(i + NG) * P1 + (j + NG);
     Axis X{P1, i, Nx, (wrap & 2u) != 0}, V{1, j, Nv, (wrap & 4u) != 0};
-    double a_x = ldg(t.ax + j), a_v = ldg(t.avx + i), c1 = ldg(t.c1 + i);
+    double a_x = ldg(t.ax + j);  // velocity centres: not written by the predecessor
+    pdl_wait();                  // tables and src of the preceding launches
+    double a_v = ldg(t.avx + i), c1 = ldg(t.c1 + i);
     double rhs = flux_first<EXACT>(src, c, X, a_x, t.hx, t.mhx);
     rhs = flux_next<EXACT>(rhs, src, c, V, a_v, t.hv, t.mhv);
     rhs = corr_add<EXACT>(rhs, c1, diag<EXACT>(src, c, X, V));
@@ -324,10 +326,11 @@ extern "C" int vpfv_stage_1d1v(double *dest, const double *A, const double *B, c
     T11 t{ax, avx, c1, hx, hv, -1.0 / (60.0 * hx), -1.0 / (60.0 * hv)};
     dim3 block(128), grid((Nv + 127) / 128, Nx);
     cudaStream_t s = (cudaStream_t)stream;
-    if (flags & VPFV_EXACT)
-        stage_1d1v_kernel<true><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags, nullptr);
-    else
-        stage_1d1v_kernel<false><<<grid, block, 0, s>>>(u, src, t, Nx, Nv, flags, nullptr);
+    double *none = nullptr;
+    cudaError_t e = (flags & VPFV_EXACT)
+                        ? launch_pdl(stage_1d1v_kernel<true>, grid, block, 0, s, u, src, t, Nx, Nv, flags, none)
+                        : launch_pdl(stage_1d1v_kernel<false>, grid, block, 0, s, u, src, t, Nx, Nv, flags, none);
+    if (e != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(e));
     return check_launch("stage_1d1v");
 }
 
@@ -348,7 +351,9 @@ extern "C" int vpfv_stage_1d1v_fused(double *dest, const double *A, const double
     Update u = make_update(dest, A, B, src, ca, cb, cd, cL, dt_dev, cL_div, nonfinite);
     T11 t{ax, avx, c1, hx, hv, -1.0 / (60.0 * hx), -1.0 / (60.0 * hv)};
     dim3 block(128), grid(Nv / 128, Nx);
-    stage_1d1v_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(u, src, t, Nx, Nv, flags, moment_partials);
+    cudaError_t e = launch_pdl(stage_1d1v_kernel<false>, grid, block, 0, (cudaStream_t)stream, u, src, t, Nx, Nv, flags,
+                               moment_partials);
+    if (e != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(e));
     return check_launch("stage_1d1v_fused");
 }
 

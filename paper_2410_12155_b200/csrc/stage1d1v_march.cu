@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(160, 1) stage_1d1v_march_kernel(const March11 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    pdl_wait();  // the tables (field kernel) and src / operands of the preceding launches
     for (int k = tid; k < i1 - i0; k += blockDim.x) {
         tabs[0][k] = __ldg(P.avx + i0 + k);
         tabs[1][k] = __ldg(P.c1 + i0 + k);
@@ -312,8 +313,19 @@ int launch_1d1v_march(double *dest, const double *A, const double *B, const doub
         attr = true;
     }
     dim3 grid(nvb, (Nx + bx - 1) / bx);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(160);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
     void *args[] = {(void *)&P};
-    cudaLaunchKernel(fns[ops], grid, dim3(160), args, smem, stream);
+    const cudaError_t rc = cudaLaunchKernelExC(&cfg, fns[ops], args);
+    if (rc != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(rc));
     return check_launch("stage_1d1v_march");
 }
 
