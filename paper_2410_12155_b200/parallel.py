@@ -487,7 +487,7 @@ class DistributedSimulation:
     each): x-slab decomposition, NCCL halo exchange, replicated Poisson."""
 
     def __init__(self, setup, cfl_fraction=0.9, dt=None, corrections=True, sigma=DEFAULT_SIGMA, *,
-                 device=None, exact=False, group=None, velocity_parts=1, halo="nccl"):
+                 device=None, exact=False, group=None, velocity_parts=1, halo="nccl", use_graphs=True):
         if halo not in ("nccl", "peer"):
             raise ValueError(f"halo must be 'nccl' or 'peer', not {halo!r}")
         self.device = require_cuda(device)
@@ -554,6 +554,8 @@ class DistributedSimulation:
         self.field_conv = (self.fields.field_1d_ok() and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
                            and os.environ.get("VPFV_FIELD_CONV", "1") != "0")
         self.peer = None
+        self.use_graphs = use_graphs
+        self._graphs = {}
         if halo == "peer":
             if not all(self.tiled) or self.nloc < NGHOST:
                 raise ValueError("halo='peer' needs the tiled 2D-2V path and slabs of >= 3 planes")
@@ -736,18 +738,42 @@ class DistributedSimulation:
                 if timed and k == len(ranges) - 1:
                     self._events[slot][s][1].record()
 
-    def launch_step(self, dt):
-        self.dt_dev.fill_(float(dt))
-        start = _lib.launch_counter[0]
+    def _step_launches(self):
         bufs = {"f0": self.ctx.f0, "f1": self.ctx.f1, "fout": self.ctx.fout}
+        start = _lib.launch_counter[0]
         self.nonfinite.fill_(-1)
-        sig = lambda arrays: tuple((a.data_ptr(), a._version) for a in arrays)  # noqa: E731
-        self._cached = self.fuse_moment and self._moment_of == sig(self.ctx.f0)
         for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, slot,
                         dt_dev=self.dt_dev, cL_div=div)
-        self._moment_of = sig(self.ctx.fout) if self.fuse_moment else None  # the next f0
         self._launches = _lib.launch_counter[0] - start
+
+    def launch_step(self, dt):
+        """Enqueue one RK4 step.  In peer mode a steady-state step (stage-4
+        partials cached) talks to the other ranks only through peer stores and
+        signal words, so it is captured once into a CUDA graph per buffer
+        rotation and density-buffer parity and replayed; otherwise the stages
+        are launched eagerly (NCCL / gloo collectives, the first step, timing)."""
+        self.dt_dev.fill_(float(dt))
+        sig = lambda arrays: tuple((a.data_ptr(), a._version) for a in arrays)  # noqa: E731
+        self._cached = self.fuse_moment and self._moment_of == sig(self.ctx.f0)
+        if self.use_graphs and self.peer is not None and self._dpush is not None and self._cached \
+                and not self._timing:
+            d = self._dpush
+            key = tuple(a.data_ptr() for a in self.ctx.f0 + self.ctx.f1 + self.ctx.fout) + (d["count"] & 1,)
+            g = self._graphs.get(key)
+            if g is None:
+                count0 = d["count"]
+                torch.cuda.synchronize(self.device)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._step_launches()
+                d["count"] = count0  # captured, not run: replay below advances it
+                self._graphs[key] = g
+            g.replay()
+            d["count"] += len(RK4_STAGES)  # every stage of a cached step pushes its densities
+        else:
+            self._step_launches()
+        self._moment_of = sig(self.ctx.fout) if self.fuse_moment else None  # the next f0
 
     def launches_per_step(self):
         return self._launches

@@ -85,6 +85,7 @@ def _worker(rank, world, port, names, dts, steps, q, vparts=1, halo="nccl"):
             for _ in range(steps):
                 sim.advance(dt)
             out[name] = [sim.gather(s) for s in range(len(sim.species))]
+            out[name + ":graphs"] = len(getattr(sim, "_graphs", {}))
         if rank == 0:
             q.put(out)
     finally:
@@ -229,11 +230,11 @@ def test_peer_halo_two_processes_same_gpu():
     state is bitwise the single-GPU Simulation (one and two species: the
     waits count one signal per species and neighbour)."""
     names = ["landau2d", "ep"]
-    refs = {n: _reference(n, 2) for n in names}
+    refs = {n: _reference(n, 5) for n in names}  # step 1 eager, then graphs for both rotations, replayed
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, names, [refs[n][0] for n in names], 2, q, 1, "peer"))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, names, [refs[n][0] for n in names], 5, q, 1, "peer"))
              for r in range(2)]
     for p in procs:
         p.start()
@@ -243,3 +244,4 @@ def test_peer_halo_two_processes_same_gpu():
     for n in names:
         for a, b in zip(out[n], refs[n][1]):
             assert np.array_equal(a.cpu().numpy() if hasattr(a, "cpu") else a, b)
+        assert out[n + ":graphs"] == 2  # steady-state steps ran as graphs (both buffer rotations)
