@@ -310,7 +310,9 @@ def run_b200(args, rank, world, device):
     # H2D of the step's input state from pinned memory, step, D2H of the result
     e2e = None
     if rank == 0 and world == 1 and args.e2e_steps > 0:
-        e2e = e2e_measure(sim, dt, args.e2e_steps, device, cells_global)
+        # at least ~50 ms of wall clock, so host jitter does not dominate a short step
+        e2e = e2e_measure(sim, dt, max(args.e2e_steps, min(2000, int(50.0 / max(ms_per_step, 1e-3)))), device,
+                          cells_global)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -395,7 +397,7 @@ def e2e_measure(sim, dt, steps, device, cells):
     el = time.perf_counter() - t0
     nbytes = pipe.bytes_per_step()
     return {"value": cells * steps / el, "unit": "cell-updates/s", "h2d_bytes_per_step": nbytes,
-            "d2h_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps,
             "how": "per step: H2D of the input state (interior; ghosts are frozen or periodic images) from "
                    "pinned host memory, the graph-replayed RK4 step, D2H of the new state; "
                    "runner.HostPipeline overlaps the upload of step k+1 and the download of step k-1 with "
