@@ -982,7 +982,7 @@ static int stage_2d2v_fused_impl(double *dest, const double *A, const double *B,
         const char *e = getenv("VPFV_XSEG");
         env_seg = e ? atoi(e) : 0;
     }
-    if (nseg <= 0 && env_seg > 0) nseg = env_seg;
+    if (env_seg > 0) nseg = env_seg;  // VPFV_XSEG overrides the caller (A/B experiments)
     if (nseg <= 0) {  // ~1.5 waves of one CTA per SM, segments >= 8 planes (each adds 6 x-halo planes)
         const int cols = tma_2d2v_columns(Ny, Nvx, Nvy);
         nseg = (3 * 148 / 2 + cols - 1) / cols;
