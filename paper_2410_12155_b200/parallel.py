@@ -361,6 +361,12 @@ class PeerHalo:
         device's context with peer access (``vpfv_ipc_export`` /
         ``vpfv_ipc_open``), so the stage kernel's stores and the signal
         atomics go over NVLink.  Collective over ``group``."""
+        devs = [None] * comm.world  # peer access must exist between the neighbours' GPUs
+        dist.all_gather_object(devs, torch.device(device).index, group=group)
+        me = torch.device(device).index
+        for r in (comm.left, comm.right):
+            if devs[r] != me and not torch.cuda.can_device_access_peer(me, devs[r]):
+                raise RuntimeError(f"no peer access from GPU {me} to GPU {devs[r]}")
         sig = torch.zeros(2, dtype=torch.int64, device=device)
         allh = _ipc_all_gather(list(buffers) + [sig], group, comm.world)
         mapped = lambda r, k: _ipc_open(*allh[r][k])  # noqa: E731
@@ -615,6 +621,10 @@ class DistributedSimulation:
                    and sh[-1] <= 16 for sh in shapes):
             return
         S, P, me = len(self.species), self.world, self.rank
+        devs = [None] * P  # every rank stores into every other rank's buffer
+        dist.all_gather_object(devs, self.device.index, group=group)
+        if any(d != self.device.index and not torch.cuda.can_device_access_peer(self.device.index, d) for d in devs):
+            return  # the NCCL all-gather of the densities stays
         g0 = self.grids[0]
         Nx, Ny = g0.N[0], g0.N[1]
         nbufs = torch.zeros((2, S, Nx, Ny), dtype=torch.float64, device=self.device)
