@@ -162,7 +162,9 @@ int vpfv_moment_partials_push(const double *partials, int nphys, int Nvx, int nc
                               double *const *dst, int ndst, unsigned long long *const *sig, int nsig,
                               unsigned *done, void *stream);
 
-/* Signal both neighbours once (after an initial halo exchange by other means). */
+/* Signal both neighbours once (after an initial halo exchange by other means).
+ * With vpfv_peer_wait: the completion half of the reference cluster's halo
+ * exchange (Exchanger, /root/reference/pkg/src/vpfv/partition.py:679-724). */
 int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream);
 
 /* Wait (one device thread, system-scope acquire) until sig[0] / sig[1] (this
@@ -172,7 +174,9 @@ int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, voi
 int vpfv_peer_wait(const unsigned long long *sig, unsigned long long *consumed, int need_lo, int need_hi,
                    double timeout_s, int *timed_out, void *stream);
 
-/* CUDA IPC of a device buffer between rank processes: export writes the
+/* CUDA IPC of a device buffer between rank processes (no reference
+ * counterpart: the reference cluster shares one address space,
+ * runner.py:259-496): export writes the
  * handle of the allocation holding ptr (vpfv_ipc_handle_size() bytes) and
  * ptr's offset in it; open maps it into the calling device's context with
  * peer access (once per allocation and process) and returns the buffer. */
@@ -269,8 +273,9 @@ int vpfv_scale(double *x, double a, long long n, void *stream);
  * Simulation._stage (runner.py:183-191) for d = 1.  Nx <= vpfv_field_1d_max_cells(). */
 int vpfv_field_1d_max_cells(void);
 
-/* The same chain over ~148 CTAs: Ex = K (*) rho with green2 = the solve's
- * Green's function K = IFFT(-i kd / k^2) stored twice (2 Nx doubles), each
+/* The same chain over ~148 CTAs: Ex = K (*) rho with green2 = the spectral
+ * solve's (fields.py:172-213) Green's function K = IFFT(-i kd / k^2) stored
+ * twice (2 Nx doubles), each
  * CTA rebuilding rho and computing E and the tables on its own cells.
  * partials (1D-1V: one row of chunks[s] <= 16 per cell) or n given.  Agrees
  * with the FFT path to O(eps sqrt(Nx)); Nx <= 16384. */
