@@ -229,7 +229,7 @@ def run_b200(args, rank, world, device):
 
         halo = args.halo
         if halo == "auto":  # the fused NVLink push where it applies, else NCCL send/recv
-            ok = (args.velocity_parts == 1 and all(f.grid.d == 2 for f in setup.dists)
+            ok = (args.velocity_parts == 1 and all(f.grid.v == 2 for f in setup.dists)
                   and setup.dists[0].grid.N[0] % world == 0)
             halo = "peer" if ok else "nccl"
         try:

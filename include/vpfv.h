@@ -162,6 +162,19 @@ int vpfv_moment_partials_push(const double *partials, int nphys, int Nvx, int nc
                               double *const *dst, int ndst, unsigned long long *const *sig, int nsig,
                               unsigned *done, void *stream);
 
+/* vpfv_stage_1d2v_fused (full x range) with the same peer halo push as
+ * vpfv_stage_2d2v_fused_peer (planes 0..2 / Nx-3..Nx-1 stored into the x
+ * neighbours' ghost planes, the last CTA signalling sig_lo / sig_hi). */
+int vpfv_stage_1d2v_fused_peer(double *dest, const double *A, const double *B, const double *src,
+                               double ca, double cb, double cd, double cL, const double *vxc,
+                               const double *vyc, const double *evx, const double *avy,
+                               const double *c1, double c2, double hx, double hvx, double hvy, int Nx,
+                               int Nvx, int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                               unsigned long long *nonfinite, const double *packed_tables,
+                               double *moment_partials, double *peer_lo, double *peer_hi,
+                               unsigned long long *sig_lo, unsigned long long *sig_hi, unsigned *done,
+                               void *stream);
+
 /* Signal both neighbours once (after an initial halo exchange by other means).
  * With vpfv_peer_wait: the completion half of the reference cluster's halo
  * exchange (Exchanger, /root/reference/pkg/src/vpfv/partition.py:679-724). */

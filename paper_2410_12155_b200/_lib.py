@@ -60,6 +60,8 @@ SIGNATURES = {
     "vpfv_stage_2d2v_tiled_ok": (_i, [_i, _i, _i, _i, _u]),
     "vpfv_stage_1d2v_fused": (_i, [_p] * 4 + [_d] * 4 + [_p] * 5 + [_d] * 4 + [_i] * 3
                               + [_u, _p, _d, _p, _p, _p, _i, _p]),
+    "vpfv_stage_1d2v_fused_peer": (_i, [_p] * 4 + [_d] * 4 + [_p] * 5 + [_d] * 4 + [_i] * 3
+                                   + [_u, _p, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_stage_1d2v_tiled_ok": (_i, [_i, _i, _i, _u]),
     "vpfv_tables_1d_packed": (_i, [_p, _p, _i, _d, _d, _d, _d, _p]),
     "vpfv_stage_2d2v_partials_chunk": (_i, []),

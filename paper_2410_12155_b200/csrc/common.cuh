@@ -30,6 +30,26 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();  // VPFV_PDL != 0
 
+// Peer halo push (x-slab ranks over NVLink): after every thread of the CTA
+// has made its stores (peer ones included) visible system-wide, count the
+// CTA; the last one bumps both neighbours' signal words (csrc/peer.cu).
+// P: a stage parameter block with done / sig_lo / sig_hi.
+template <class StageParams>
+__device__ __forceinline__ void peer_done_signal(const StageParams &P) {
+    if (!P.done) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(P.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *P.done = 0u;  // ready for the next launch (ordered by the kernel boundary)
+            __threadfence_system();
+            if (P.sig_lo) atomicAdd_system(P.sig_lo, 1ull);
+            if (P.sig_hi) atomicAdd_system(P.sig_hi, 1ull);
+        }
+    }
+}
+
 template <typename... Args>
 cudaError_t launch_pdl(void (*kernel)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args... args) {

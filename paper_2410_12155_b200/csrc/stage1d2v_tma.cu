@@ -49,6 +49,10 @@ struct Stage12 {
     int wrap_x;
     int i0, i1, nseg, seglen;
     double *partials;  // [Nx][Nvx][Nvy/16] or nullptr
+    // peer halo push (vpfv_stage_1d2v_fused_peer; as Stage22 in stage2d2v_tma.cu)
+    double *peer_lo, *peer_hi;
+    unsigned long long *sig_lo, *sig_hi;
+    unsigned *done;
 };
 
 namespace r12 {
@@ -129,7 +133,10 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int k0 = kt * BK, l0 = lt * BL;
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
-    if (i0 >= i1) return;
+    if (i0 >= i1) {
+        peer_done_signal(P);
+        return;
+    }
 
     // thread -> cells (vx0 + b, vy), b < 4; half-warps are 16-lane vy rows
     const int lane = tid & 31, warp = tid >> 5;
@@ -308,6 +315,16 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             double *dq = P.dest + gq;
 #pragma unroll
             for (int b = 0; b < BB; ++b) __stcs(dq + b * P2, out[b]);
+            if (P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
+                double *pq = P.peer_lo + gq + (long long)P.Nx * P1;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) pq[b * P2] = out[b];
+            }
+            if (P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
+                double *pq = P.peer_hi + gq - (long long)P.Nx * P1;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) pq[b * P2] = out[b];
+            }
             if (P.nonfinite) {
                 const double sum = (out[0] + out[1]) + (out[2] + out[3]);
                 if (!isfinite(sum)) {
@@ -339,6 +356,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         gq += P1;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
+    peer_done_signal(P);
 }
 
 // Geometry (VPFV_R12_CFG): 1 = (32, 16) tiles, 128 threads, <=168 registers,
@@ -439,13 +457,13 @@ struct Operands12 {  // ca A + cb B + cd dest grouped by array; the src part is 
 };
 }  // namespace
 
-extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const double *src,
-                                     double ca, double cb, double cd, double cL, const double *vxc,
-                                     const double *vyc, const double *evx, const double *avy,
-                                     const double *c1, double c2, double hx, double hvx, double hvy, int Nx,
-                                     int Nvx, int Nvy, unsigned flags, const double *dt_dev, double cL_div,
-                                     unsigned long long *nonfinite, const double *packed_tables,
-                                     double *moment_partials, int xsegments, void *stream) {
+static int stage_1d2v_fused_impl(double *dest, const double *A, const double *B, const double *src, double ca,
+                                 double cb, double cd, double cL, const double *vxc, const double *vyc,
+                                 const double *evx, const double *avy, const double *c1, double c2, double hx,
+                                 double hvx, double hvy, int Nx, int Nvx, int Nvy, unsigned flags,
+                                 const double *dt_dev, double cL_div, unsigned long long *nonfinite,
+                                 const double *packed_tables, double *moment_partials, int xsegments, void *stream,
+                                 const Stage12 *peer) {
     if (dest == src) return set_error(VPFV_EALIAS, "dest must not alias src");
     Operands12 ops;
     ops.add(A, ca, src);
@@ -453,6 +471,7 @@ extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double
     ops.add(dest, cd, src);
     if (!packed_tables || !tma_1d2v_eligible(Nx, Nvx, Nvy, flags) || ops.n > r12::OPS_MAX) {
         if (moment_partials) return set_error(VPFV_EARG, "fused moment needs the tiled 1D-2V path");
+        if (peer) return set_error(VPFV_EARG, "peer halo push needs the tiled 1D-2V path");
         return vpfv_stage_1d2v(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, avy, c1, c2, hx, hvx, hvy, Nx,
                                Nvx, Nvy, flags, dt_dev, cL_div, nonfinite, stream);
     }
@@ -481,10 +500,52 @@ extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double
     P.partials = moment_partials;
     P.i0 = 0;
     P.i1 = Nx;
+    if (peer) {
+        P.peer_lo = peer->peer_lo;
+        P.peer_hi = peer->peer_hi;
+        P.sig_lo = peer->sig_lo;
+        P.sig_hi = peer->sig_hi;
+        P.done = peer->done;
+    }
     const double *opp[r12::OPS_MAX] = {ops.n > 0 ? ops.ptr[0] : nullptr, ops.n > 1 ? ops.ptr[1] : nullptr};
     cudaStream_t st = (cudaStream_t)stream;
     const int cfg = geo12_cfg();
     if (cfg == 2 && Nvx % 64 == 0) return launch12<r12::Geo<64, 1>>(src, opp, packed_tables, P, xsegments, st);
     if (cfg == 1) return launch12<r12::Geo<32, 3>>(src, opp, packed_tables, P, xsegments, st);
     return launch12<r12::Geo<32, 2>>(src, opp, packed_tables, P, xsegments, st);
+}
+
+extern "C" int vpfv_stage_1d2v_fused(double *dest, const double *A, const double *B, const double *src,
+                                     double ca, double cb, double cd, double cL, const double *vxc,
+                                     const double *vyc, const double *evx, const double *avy,
+                                     const double *c1, double c2, double hx, double hvx, double hvy, int Nx,
+                                     int Nvx, int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                                     unsigned long long *nonfinite, const double *packed_tables,
+                                     double *moment_partials, int xsegments, void *stream) {
+    return stage_1d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, avy, c1, c2, hx, hvx, hvy, Nx, Nvx,
+                                 Nvy, flags, dt_dev, cL_div, nonfinite, packed_tables, moment_partials, xsegments,
+                                 stream, nullptr);
+}
+
+extern "C" int vpfv_stage_1d2v_fused_peer(double *dest, const double *A, const double *B, const double *src,
+                                          double ca, double cb, double cd, double cL, const double *vxc,
+                                          const double *vyc, const double *evx, const double *avy,
+                                          const double *c1, double c2, double hx, double hvx, double hvy, int Nx,
+                                          int Nvx, int Nvy, unsigned flags, const double *dt_dev, double cL_div,
+                                          unsigned long long *nonfinite, const double *packed_tables,
+                                          double *moment_partials, double *peer_lo, double *peer_hi,
+                                          unsigned long long *sig_lo, unsigned long long *sig_hi, unsigned *done,
+                                          void *stream) {
+    if (!packed_tables || !tma_1d2v_eligible(Nx, Nvx, Nvy, flags))
+        return set_error(VPFV_EARG, "peer halo push needs the tiled 1D-2V path");
+    if (Nx < NG || !done) return set_error(VPFV_EARG, "peer halo push: Nx >= 3 and a done counter");
+    Stage12 peer{};
+    peer.peer_lo = peer_lo;
+    peer.peer_hi = peer_hi;
+    peer.sig_lo = sig_lo;
+    peer.sig_hi = sig_hi;
+    peer.done = done;
+    return stage_1d2v_fused_impl(dest, A, B, src, ca, cb, cd, cL, vxc, vyc, evx, avy, c1, c2, hx, hvx, hvy, Nx, Nvx,
+                                 Nvy, flags, dt_dev, cL_div, nonfinite, packed_tables, moment_partials, 0, stream,
+                                 &peer);
 }

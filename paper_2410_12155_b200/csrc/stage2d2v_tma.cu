@@ -78,22 +78,6 @@ struct Stage22 {
     unsigned *done;
 };
 
-// After every thread of the CTA has made its stores (peer ones included)
-// visible system-wide, count the CTA; the last one signals both neighbours.
-__device__ __forceinline__ void peer_done_signal(const Stage22 &P) {
-    if (!P.done) return;
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(P.done, 1u);
-        if (prev == gridDim.x - 1) {
-            *P.done = 0u;  // ready for the next launch (ordered by the kernel boundary)
-            __threadfence_system();
-            if (P.sig_lo) atomicAdd_system(P.sig_lo, 1ull);
-            if (P.sig_hi) atomicAdd_system(P.sig_hi, 1ull);
-        }
-    }
-}
 
 namespace rb {
 constexpr int BJ = 8, BL = 16, OPS_MAX = 2;

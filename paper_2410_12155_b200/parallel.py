@@ -399,10 +399,19 @@ class PeerHalo:
 
 def launch_stage_peer(lt, dest, A, B, src, ca, cb, cd, cL, flags, stream, push, dt_dev=None, cL_div=1.0,
                       nonfinite=None, partials=None):
-    """The tiled 2D-2V stage of slab table view ``lt`` (_LocalTables) with the
-    fused halo push ``push`` = PeerHalo.push_args(dest, s)."""
+    """The tiled 2D-2V or 1D-2V stage of slab table view ``lt``
+    (_LocalTables) with the fused halo push ``push`` = PeerHalo.push_args(dest, s)."""
     t, g = lt.t, lt.lgrid
     h, N = g.h, g.N
+    if (g.d, g.v) == (1, 2):
+        vo = lt.v0 * 8
+        _lib.call("vpfv_stage_1d2v_fused_peer", dest.data_ptr(), A.data_ptr(), B.data_ptr(), src.data_ptr(),
+                  float(ca), float(cb), float(cd), float(cL), t.vxc.data_ptr() + vo, t.vyc.data_ptr(),
+                  t.e.data_ptr() + lt.x0 * 8, t.avy.data_ptr() + vo, t.c1.data_ptr() + lt.x0 * 8, t.c2, h[0], h[1],
+                  h[2], N[0], N[1], N[2], flags, None if dt_dev is None else dt_dev.data_ptr(), float(cL_div),
+                  None if nonfinite is None else nonfinite.data_ptr(), t.packed.data_ptr() + lt.x0 * 8 * 8,
+                  None if partials is None else partials.data_ptr(), *push, stream)
+        return
     Ny = t.grid.N[1]
     off = lt.x0 * Ny * 8
     ptr = lambda a: a.data_ptr() + off  # noqa: E731
@@ -519,8 +528,8 @@ class DistributedSimulation:
             f0.append(torch.from_numpy(np.ascontiguousarray(data[tuple(idx)])).to(self.device))
         self.halo = halo
         if halo == "peer":
-            if velocity_parts != 1 or self.world < 2 or any(g.d != 2 for g in self.grids):
-                raise ValueError("halo='peer' needs 2D-2V x-slabs over >= 2 ranks (velocity_parts=1)")
+            if velocity_parts != 1 or self.world < 2 or any(g.v != 2 for g in self.grids):
+                raise ValueError("halo='peer' needs 2D-2V or 1D-2V x-slabs over >= 2 ranks (velocity_parts=1)")
             if self.grids[0].N[0] % self.world:
                 raise ValueError("halo='peer' needs equal slabs (Nx divisible by the rank count)")
         self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
@@ -626,13 +635,14 @@ class DistributedSimulation:
         if any(d != self.device.index and not torch.cuda.can_device_access_peer(self.device.index, d) for d in devs):
             return  # the NCCL all-gather of the densities stays
         g0 = self.grids[0]
-        Nx, Ny = g0.N[0], g0.N[1]
-        nbufs = torch.zeros((2, S, Nx, Ny), dtype=torch.float64, device=self.device)
+        phys = tuple(g0.N[:g0.d])
+        per, row = int(np.prod(phys)), int(np.prod(phys[1:]))  # cells, cells per x row
+        nbufs = torch.zeros((2, S) + phys, dtype=torch.float64, device=self.device)
         dsig = torch.zeros(2, dtype=torch.int64, device=self.device)
         allh = _ipc_all_gather([nbufs, dsig], group, P)
         nptr = [nbufs.data_ptr() if q == me else _ipc_open(*allh[q][0]) for q in range(P)]
         sptr = [_ipc_open(*allh[q][1]) for q in range(P) if q != me]
-        dests = [[_lib.ptr_array([nptr[q] + ((par * S + s) * Nx * Ny + self.x0 * Ny) * 8 for q in range(P)])
+        dests = [[_lib.ptr_array([nptr[q] + ((par * S + s) * per + self.x0 * row) * 8 for q in range(P)])
                   for s in range(S)] for par in range(2)]
         self._dpush = dict(nbufs=nbufs, dsig=dsig, dests=dests, sigs=_lib.ptr_array(sptr),
                            consumed=torch.zeros(2, dtype=torch.int64, device=self.device),
@@ -645,7 +655,8 @@ class DistributedSimulation:
         """Global n from every rank's pushes of this stage (see _setup_density_push)."""
         d, S, P = self._dpush, len(self.species), self.world
         par = d["count"] & 1
-        nphys = self.nloc * self.grids[0].N[1]
+        g0 = self.grids[0]
+        nphys = self.nloc * int(np.prod(g0.N[1:g0.d]))
         for s in range(S):
             _lib.call("vpfv_moment_partials_push", part[s].data_ptr(), nphys, part[s].shape[-2], part[s].shape[-1],
                       self.fields.vols[s], d["dests"][par][s], P, d["sigs"], P - 1, d["done"][s:s + 1].data_ptr(),
@@ -687,19 +698,22 @@ class DistributedSimulation:
 
     def _stage_peer(self, dest, A, B, src, ca, cb, cd, cL, slot, dt_dev=None, cL_div=1.0):
         """One stage with the x halo pushed by the stage kernels themselves:
-        the field solve (densities all-gathered), then a wait for both
+        the field solve (densities pushed to / gathered from every rank), then a wait for both
         neighbours' pushes of the previous stage (src's ghost planes), then
         the stage launches, which push dest's boundary planes onward."""
         stream = stream_handle(self.device)
         use, emit = self._partials_for(slot)
         if use is not None and self._dpush is not None:
             self._densities_push(use, stream)
+        else:
+            self._densities(src, use, stream)
+        if self.field_conv:  # d = 1: Simulation's GPU-wide field chain (tables included)
+            self.fields.field_and_tables_1d(self.gtables, self.tiled, None, stream=stream, conv=True)
+        else:
             self.fields.charge(stream)
             E = self.fields.poisson(self.fields.rho, False, stream)
-        else:
-            E = self._solve(src, use)
-        for s, gt in enumerate(self.gtables):
-            gt.update(E, stream, packed=True)
+            for s, gt in enumerate(self.gtables):
+                gt.update(E, stream, packed=True)
         self.peer.wait(stream)
         timed = self._timing and slot is not None
         for s, lt in enumerate(self.tables):

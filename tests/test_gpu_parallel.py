@@ -227,9 +227,9 @@ def test_peer_halo_two_processes_same_gpu():
     """DistributedSimulation(halo="peer") with two processes sharing the GPU:
     each maps the other's state buffers and signal words by CUDA IPC, the
     stage kernels push the x halo across the processes, and the gathered
-    state is bitwise the single-GPU Simulation (one and two species: the
-    waits count one signal per species and neighbour)."""
-    names = ["landau2d", "ep"]
+    state is bitwise the single-GPU Simulation (2D-2V and 1D-2V, one and
+    two species: the waits count one signal per species and neighbour)."""
+    names = ["landau2d", "ep", "lhdi64"]  # 2D-2V one and two species, 1D-2V two species
     refs = {n: _reference(n, 5) for n in names}  # step 1 eager, then graphs for both rotations, replayed
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
