@@ -114,7 +114,9 @@ __device__ __forceinline__ void scatter12(double (&w)[6], double ti, double &fin
     }
 }
 
-template <class GEO>
+// PEER: the x-halo push of vpfv_stage_1d2v_fused_peer, compiled only into the
+// instantiation that needs it (the ordinary launches carry no extra code)
+template <class GEO, bool PEER>
 __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     stage1d2v_rb_kernel(const __grid_constant__ Maps12 maps, const Stage12 P) {
     using namespace r12;
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) {
-        peer_done_signal(P);
+        if (PEER) peer_done_signal(P);
         return;
     }
 
@@ -315,12 +317,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             double *dq = P.dest + gq;
 #pragma unroll
             for (int b = 0; b < BB; ++b) __stcs(dq + b * P2, out[b]);
-            if (P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
+            if (PEER && P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
                 double *pq = P.peer_lo + gq + (long long)P.Nx * P1;
 #pragma unroll
                 for (int b = 0; b < BB; ++b) pq[b * P2] = out[b];
             }
-            if (P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
+            if (PEER && P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
                 double *pq = P.peer_hi + gq - (long long)P.Nx * P1;
 #pragma unroll
                 for (int b = 0; b < BB; ++b) pq[b * P2] = out[b];
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         gq += P1;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
-    peer_done_signal(P);
+    if (PEER) peer_done_signal(P);
 }
 
 // Geometry (VPFV_R12_CFG): 1 = (32, 16) tiles, 128 threads, <=168 registers,
@@ -411,10 +413,14 @@ static int launch12(const double *src, const double *const ops[r12::OPS_MAX], co
     if (!tma_map(tab, 2, tdims, tstr, tbox, &maps.tab)) return set_error(VPFV_ECUDA, "table map failed");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(stage1d2v_rb_kernel<GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        cudaFuncSetAttribute(stage1d2v_rb_kernel<GEO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        cudaFuncSetAttribute(stage1d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
         attr = true;
     }
-    stage1d2v_rb_kernel<GEO><<<cols * nseg, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    if (P.done)
+        stage1d2v_rb_kernel<GEO, true><<<cols * nseg, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    else
+        stage1d2v_rb_kernel<GEO, false><<<cols * nseg, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
     return check_launch("stage_1d2v_tma");
 }
 

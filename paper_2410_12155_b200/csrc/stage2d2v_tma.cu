@@ -221,7 +221,9 @@ __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Ma
     }
 }
 
-template <class GEO>
+// PEER: the x-halo push of vpfv_stage_2d2v_fused_peer, compiled only into the
+// instantiation that needs it (the ordinary launches carry no extra code)
+template <class GEO, bool PEER>
 __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int i0 = P.i0 + seg * P.seglen;
     const int i1 = min(P.i1, i0 + P.seglen);
     if (i0 >= i1) {
-        peer_done_signal(P);
+        if (PEER) peer_done_signal(P);
         return;
     }
 
@@ -538,12 +540,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             }
 #pragma unroll
             for (int i = 0; i < NC; ++i) __stcs(dq + (i / BB) * P2 + (i % BB) * P3, out[i]);
-            if (P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
+            if (PEER && P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
                 double *pq = P.peer_lo + gq + (long long)P.Nx * P1;
 #pragma unroll
                 for (int i = 0; i < NC; ++i) pq[(i / BB) * P2 + (i % BB) * P3] = out[i];
             }
-            if (P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
+            if (PEER && P.peer_hi && q >= P.Nx - NG) {  // my plane q -> the high neighbour's ghost plane q - Nx
                 double *pq = P.peer_hi + gq - (long long)P.Nx * P1;
 #pragma unroll
                 for (int i = 0; i < NC; ++i) pq[(i / BB) * P2 + (i % BB) * P3] = out[i];
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         ppart += pstep;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
-    peer_done_signal(P);
+    if (PEER) peer_done_signal(P);
 }
 
 // ---------------------------------------------------------------------------
@@ -818,11 +820,15 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
         attr = true;
     }
     const int nblocks = (P.Ny / BJ) * (P.Nvx / GEO::BK) * (P.Nvy / BL) * P.nseg;
-    stage2d2v_rb_kernel<GEO><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    if (P.done)
+        stage2d2v_rb_kernel<GEO, true><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    else
+        stage2d2v_rb_kernel<GEO, false><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
     return check_launch("stage_2d2v_tma");
 }
 
