@@ -72,8 +72,32 @@ def advection_speeds(grid, species, E):
 
 
 def max_speed_per_dim(grid, species, E):
-    """max |A^d| per dimension (fvm.py:125-127)."""
-    return [float(np.max(np.abs(a))) for a in advection_speeds(grid, species, E)]
+    """max |A^d| per dimension (fvm.py:125-127).
+
+    Equal to the maximum over the broadcast speed arrays of
+    ``advection_speeds`` without building them (at 128^4 those are 128^3-cell
+    arrays, ~10 ms of host time per CFL step): a velocity-dim speed is
+    fl(e(x) +- c(v)) with e the field part, and for fixed c that is monotone
+    in e, so its largest magnitude sits at the smallest or largest e."""
+    if grid.v == 1 or (grid.d, grid.v) not in ((1, 2), (2, 2)):
+        return [float(np.max(np.abs(a))) for a in advection_speeds(grid, species, E)]
+    s = species
+    gx, gy = _g(s)[:2]
+    cB = magnetic_factor(s)
+    E = {k: np.asarray(v) for k, v in E.items()}
+
+    def extreme(e, c, sign):  # max over (x, v) of |fl(e(x) + sign c(v))|
+        lo, hi = np.min(e), np.max(e)
+        return float(max(np.max(np.abs(lo + sign * c)), np.max(np.abs(hi + sign * c))))
+
+    if (grid.d, grid.v) == (1, 2):
+        evx = s.qm * s.kappa2 * E["Ex"] + gx
+        return [float(np.max(np.abs(grid.centers(1)))), extreme(evx, cB * grid.centers(2), 1.0),
+                float(np.max(np.abs(-cB * grid.centers(1) + gy)))]
+    evx = s.qm * s.kappa2 * E["Ex"] + gx
+    evy = s.qm * s.kappa2 * E["Ey"] + gy
+    return [float(np.max(np.abs(grid.centers(2)))), float(np.max(np.abs(grid.centers(3)))),
+            extreme(evx, cB * grid.centers(3), 1.0), extreme(evy, cB * grid.centers(2), -1.0)]
 
 
 def correction_coeffs(grid, species, E):

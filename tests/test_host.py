@@ -186,3 +186,24 @@ def test_richardson_error_mirror():
     assert richardson_error(a + 2.0, fine) == 2.0
     with pytest.raises(ValueError):
         richardson_error(np.zeros((8, 8)), np.zeros((8, 16)))
+
+
+@pytest.mark.parametrize("which", ["landau2d", "lhdi", "ep", "weibel"])
+def test_max_speed_per_dim_equals_broadcast_max(which):
+    """The CFL speeds from the field extremes equal the maxima over the full
+    broadcast speed arrays (fvm.py:125-127), with and without magnetic field."""
+    from paper_2410_12155_b200 import problems as P
+    from paper_2410_12155_b200.fvm import advection_speeds, max_speed_per_dim
+
+    setup = {"landau2d": lambda: P.make_problem(P.landau_spec(), 16, 16),
+             "lhdi": lambda: P.make_problem(P.ProblemSpec("lhdi"), 16, 32),
+             "ep": lambda: P.make_electron_proton_2d2v(16, 32),
+             "weibel": lambda: P.make_problem(P.ProblemSpec("weibel"), 16, 32)}[which]()
+    rng = np.random.default_rng(7)
+    for f, sp in zip(setup.dists, setup.species):
+        g = f.grid
+        shape = tuple(g.N[:g.d])
+        E = {"Ex": 0.3 * rng.standard_normal(shape)}
+        if g.d == 2:
+            E["Ey"] = 0.3 * rng.standard_normal(shape)
+        assert max_speed_per_dim(g, sp, E) == [float(np.max(np.abs(a))) for a in advection_speeds(g, sp, E)]
