@@ -207,3 +207,18 @@ def test_max_speed_per_dim_equals_broadcast_max(which):
         if g.d == 2:
             E["Ey"] = 0.3 * rng.standard_normal(shape)
         assert max_speed_per_dim(g, sp, E) == [float(np.max(np.abs(a))) for a in advection_speeds(g, sp, E)]
+
+
+def test_bench_workloads_and_weak_scaling():
+    """bench.py's workloads: config 5 grows its x extent with the rank count
+    (weak scaling, 64^4 per species per GPU); the L2 note tells resident
+    buffers from streamed ones; the JSON keys the contract needs exist."""
+    import bench
+
+    s1, s4 = bench.make_setup("ep2d2v-64"), bench.make_setup("ep2d2v-64", 4)
+    assert [f.grid.N for f in s1.dists] == [(64, 64, 64, 64)] * 2
+    assert [f.grid.N for f in s4.dists] == [(256, 64, 64, 64)] * 2
+    assert "ep2d2v-64" in bench.WEAK and "landau2d-128" not in bench.WEAK
+    assert bench.l2_note(bench.make_setup("landau1d-128")).startswith("inputs smaller than L2")
+    assert bench.l2_note(bench.make_setup("ep2d2v-64")).startswith("inputs larger than L2")
+    assert set(bench.KERNEL_OF) == set(bench.WORKLOADS)
