@@ -310,14 +310,15 @@ __global__ void __launch_bounds__(1024) field1d_kernel(double *__restrict__ n, C
 // modular index.  Rounding differs from the FFT path by O(eps sqrt(Nx)).
 __global__ void __launch_bounds__(256) field1d_conv_kernel(double *__restrict__ n, Charges q, int ns, int nx,
                                                            double *__restrict__ rho, double *__restrict__ Ex,
-                                                           const double *__restrict__ K2, int per_cta, Tables1D T) {
+                                                           const double *__restrict__ K2, int per_cta, Tables1D T,
+                                                           int trigger) {
     extern __shared__ double sm1[];
     __shared__ double red[32];
     double *rs = sm1, *Es = sm1 + nx;  // rho (all cells), E on this CTA's cells c0-1 .. c0+M
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const bool lead = blockIdx.x == 0;
-    pdl_trigger();  // the stage kernel after this may start launching
-    pdl_wait();     // the partials / n of the previous stage
+    if (trigger) pdl_trigger();  // the (programmatic) stage kernel after this may start launching
+    pdl_wait();                  // the partials / n of the previous stage
     double acc = 0.0;
     for (int p = tid; p < nx; p += nt) {
         double r = 0.0;
@@ -571,12 +572,18 @@ extern "C" int vpfv_field_1d_conv(const double *const *partials, const int *chun
         allow_smem((const void *)field1d_conv_kernel);
         once = true;
     }
-    if (partials) {  // after a (triggering) stage kernel: programmatic launch
+    // From 1D-1V partials of one species the caller's next launch is that
+    // species' stage kernel, a programmatic dependent: launch programmatically
+    // and let it start early.  Otherwise (a moment kernel before, 1D-2V or
+    // several species after) an ordinary launch that does not trigger.
+    const int trigger = partials && nspecies == 1 ? 1 : 0;
+    if (partials) {
         const cudaError_t rc = launch_pdl(field1d_conv_kernel, dim3(grid), dim3(256), smem, (cudaStream_t)stream, n,
-                                          q, nspecies, Nx, rho, Ex, green2, per, T);
+                                          q, nspecies, Nx, rho, Ex, green2, per, T, trigger);
         if (rc != cudaSuccess) return set_error(VPFV_ECUDA, cudaGetErrorString(rc));
-    } else {  // after the separate moment kernel: an ordinary launch
-        field1d_conv_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, green2, per, T);
+    } else {
+        field1d_conv_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(n, q, nspecies, Nx, rho, Ex, green2, per, T,
+                                                                      0);
     }
     return check_launch("field_1d_conv");
 }

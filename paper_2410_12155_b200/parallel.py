@@ -703,6 +703,7 @@ class DistributedSimulation:
         the stage launches, which push dest's boundary planes onward."""
         stream = stream_handle(self.device)
         use, emit = self._partials_for(slot)
+        self.peer.wait(stream)  # both neighbours' pushes of the previous stage (src's ghost planes)
         if use is not None and self._dpush is not None:
             self._densities_push(use, stream)
         else:
@@ -714,7 +715,6 @@ class DistributedSimulation:
             E = self.fields.poisson(self.fields.rho, False, stream)
             for s, gt in enumerate(self.gtables):
                 gt.update(E, stream, packed=True)
-        self.peer.wait(stream)
         timed = self._timing and slot is not None
         for s, lt in enumerate(self.tables):
             nf = None if slot is None else self.nonfinite[slot, s:s + 1]
