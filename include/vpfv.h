@@ -246,6 +246,13 @@ int vpfv_moment_partials(const double *partials, double *n, int nphys, int Nvx, 
 int vpfv_moment(const double *f, double *n, int d, int v, const int *N, double vol,
                 void *stream);
 
+/* Velocity moment with schedule="position-major": the per-cell sequential
+ * sum s += f over the velocity interior in C order, then n = s * vol --
+ * bitwise the reference's compiled _seq_moment_{2,3,4}d (fields.py:50-83,
+ * :100-106). */
+int vpfv_moment_seq(const double *f, double *n, int d, int v, const int *N, double vol,
+                    void *stream);
+
 /* Momentum / kinetic-energy velocity sums per physical cell with the
  * midpoint-to-average lift of higher_moments (fields.py:131-161):
  * out[p][2k] = sum_v (v_c f + h_k^2/12 df/dv_k),

@@ -448,6 +448,9 @@ def zeroth_moment(data, g, schedule="velocity-major"):  # fields.py:86-111
     vol = velocity_volume(g)
     if schedule == "velocity-major":
         n = fold_tree_sum(interior, g.velocity_dims)
+    elif schedule == "position-major":  # _seq_moment_{2,3,4}d (fields.py:50-83): s += f in C order
+        flat = interior.reshape(tuple(g.N[:g.d]) + (-1,))
+        n = np.add.accumulate(flat, axis=-1)[..., -1]  # strictly sequential, left to right
     elif schedule == "free":
         n = interior.sum(axis=g.velocity_dims)
     else:

@@ -67,6 +67,7 @@ SIGNATURES = {
     "vpfv_stage_2d2v_partials_chunk": (_i, []),
     "vpfv_stage_1d2v_partials_chunk": (_i, []),
     "vpfv_moment": (_i, [_p, _p, _i, _i, _p, _d, _p]),
+    "vpfv_moment_seq": (_i, [_p, _p, _i, _i, _p, _d, _p]),
     "vpfv_higher_moments": (_i, [_p, _i, _i, _p, _p, _p, _d, _d, _p, _p]),
     "vpfv_richardson_partials": (_i, [_p, _p, _i, _p, _p, _i, _p]),
     "vpfv_scale": (_i, [_p, _d, ctypes.c_longlong, _p]),

@@ -133,3 +133,53 @@ extern "C" int vpfv_moment(const double *f, double *n, int d, int v, const int *
         f, n, nphys, ny, Pvel, s_row, nv1, nv2, off_v, vol, d, Py_pad, nbuf);
     return check_launch("moment");
 }
+
+// ---------------------------------------------------------------------------
+// schedule="position-major": the reference's compiled per-cell sequential sum
+// (fields.py:50-83, _seq_moment_{2,3,4}d): s = 0; s += f[v] over the velocity
+// interior in C order; n = s * vol.  One warp per physical cell: the lanes load
+// 32 consecutive values of a velocity row (coalesced) and every lane adds them
+// in index order from shuffles, so the association is the reference's.
+namespace vpfv {
+__global__ void moment_seq_kernel(const double *__restrict__ f, double *__restrict__ n, int nphys, int ny,
+                                  long long Pvel, long long s_row, int nv1, int nv2, long long off_v, double vol,
+                                  int d, long long Py_pad) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= nphys) return;
+    long long base;
+    if (d == 1) {
+        base = (long long)(warp + NG) * Pvel;
+    } else {
+        const int ix = warp / ny, iy = warp - ix * ny;
+        base = ((long long)(ix + NG) * Py_pad + (iy + NG)) * Pvel;
+    }
+    double s = 0.0;
+    for (int a = 0; a < nv1; ++a) {
+        const double *row = f + base + off_v + (long long)a * s_row + NG;
+        for (int c = 0; c < nv2; c += 32) {
+            const int m = min(32, nv2 - c);
+            const double x = lane < m ? row[c + lane] : 0.0;
+            for (int j = 0; j < m; ++j) s = __dadd_rn(s, __shfl_sync(0xffffffffu, x, j));
+        }
+    }
+    if (lane == 0) n[warp] = __dmul_rn(s, vol);
+}
+}  // namespace vpfv
+
+extern "C" int vpfv_moment_seq(const double *f, double *n, int d, int v, const int *N, double vol,
+                               void *stream) {
+    if (d < 1 || d > 2 || v < d || d + v > 4) return set_error(VPFV_EDIM, "unsupported (d, v)");
+    int nphys = 1;
+    for (int k = 0; k < d; ++k) nphys *= N[k];
+    const int nv1 = (v == 2) ? N[d] : 1, nv2 = N[d + v - 1];
+    long long Pvel = 1;
+    for (int k = d; k < d + v; ++k) Pvel *= (N[k] + 2 * NG);
+    const long long s_row = (v == 2) ? (N[d + 1] + 2 * NG) : 0;
+    const long long off_v = (v == 2) ? (long long)NG * s_row : 0;
+    const int ny = (d == 2) ? N[1] : 1;
+    const long long Py_pad = (d == 2) ? (N[1] + 2 * NG) : 1;
+    const int threads = 256, grid = (nphys * 32 + threads - 1) / threads;
+    moment_seq_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(f, n, nphys, ny, Pvel, s_row, nv1, nv2, off_v,
+                                                                   vol, d, Py_pad);
+    return check_launch("moment_seq");
+}

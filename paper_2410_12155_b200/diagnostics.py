@@ -2,9 +2,10 @@
 
 Mirrors /root/reference/pkg/src/vpfv/diagnostics.py: ``DiagnosticsRow``,
 ``DIAGNOSTICS_SCHEMA``, ``field_amplitude``, ``conserved_quantities``,
-``fit_growth_rate``.  These run per output cadence, not per stage, on host
-copies of the device state (moving them onto the device is SURVEY.md 8f
-row 1).
+``rows_to_csv``, ``fit_growth_rate``, ``richardson_error`` with the
+reference's signatures, return values and validation.  They run per output
+cadence, not per stage; on device state the velocity sums run on the GPU
+(``DeviceDiagnostics``).
 """
 
 from __future__ import annotations
@@ -70,7 +71,7 @@ def field_amplitude(E, grid):
     return math.sqrt(total * vol)
 
 
-def higher_moments(data, grid):
+def higher_moments_arrays(data, grid):
     """Momentum and kinetic-energy densities with the midpoint-to-average lift
     (fields.py:131-161); ghosts of ``data`` must be synchronised."""
     g = grid
@@ -96,8 +97,31 @@ def higher_moments(data, grid):
     return mom, 0.5 * kin
 
 
-def conserved_quantities(datas, grids, species, E, t, dt):
-    """One DiagnosticsRow from host padded arrays with synchronised ghosts
+def _host_E(E):
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)) for k, v in E.items()}
+
+
+def conserved_quantities(dists, species, state, t, dt):
+    """One :class:`DiagnosticsRow` from synchronised fields
+    (diagnostics.py:85-122, same signature and order of operations).
+
+    ``dists`` are DistFields (host numpy data with current ghosts, or device
+    tensors with stored velocity ghosts -- then the velocity sums run on the
+    device through ``DeviceDiagnostics`` and only physical-grid arrays reach
+    the host); ``state`` is the field solve of the same instant (``.E``)."""
+    data0 = dists[0].data
+    E = _host_E(state.E)
+    if hasattr(data0, "is_cuda") and data0.is_cuda:
+        from .kernels import stream_handle
+
+        diag = DeviceDiagnostics([f.grid for f in dists], data0.device)
+        return diag.row([f.data for f in dists], species, E, t, dt, stream_handle(data0.device))
+    return conserved_quantities_arrays([np.asarray(f.data) for f in dists], [f.grid for f in dists], species,
+                                       E, t, dt)
+
+
+def conserved_quantities_arrays(datas, grids, species, E, t, dt):
+    """``conserved_quantities`` on host padded arrays with synchronised ghosts
     (diagnostics.py:85-122)."""
     masses = []
     mom_tot = None
@@ -108,7 +132,7 @@ def conserved_quantities(datas, grids, species, E, t, dt):
             cellvol *= w
         interior = data[g.interior_slices()]
         masses.append((sp.name, float(fold_tree_sum(interior, tuple(range(g.ndim)))) * cellvol))
-        mom, kin = higher_moments(data, g)
+        mom, kin = higher_moments_arrays(data, g)
         physvol = 1.0
         for k in range(g.d):
             physvol *= g.h[k]
@@ -123,22 +147,58 @@ def conserved_quantities(datas, grids, species, E, t, dt):
                           field_amplitude=field_amplitude(E, grids[0]))
 
 
-def fit_growth_rate(ts, amps, t_min=None, t_max=None, peaks=False):
-    """Least-squares slope of log |E| (the amplitude convention of
-    diagnostics.py:133-160); ``peaks=True`` fits only local maxima, the robust
-    choice for damped oscillations."""
-    ts = np.asarray(ts, dtype=float)
-    a = np.asarray(amps, dtype=float)
-    lo = -np.inf if t_min is None else t_min
-    hi = np.inf if t_max is None else t_max
-    if peaks:
-        idx = [i for i in range(1, len(a) - 1)
-               if a[i] >= a[i - 1] and a[i] > a[i + 1] and lo <= ts[i] <= hi]
-    else:
-        idx = [i for i in range(len(a)) if lo <= ts[i] <= hi]
-    if len(idx) < 2:
-        raise ValueError("not enough samples in the fit window")
-    return float(np.polyfit(ts[idx], np.log(a[idx]), 1)[0])
+def rows_to_csv(rows, species_names):
+    """Diagnostics rows as CSV text, 17 significant digits (diagnostics.py:125-130)."""
+    lines = [",".join(DiagnosticsRow.header(species_names))]
+    for row in rows:
+        lines.append(",".join(f"{v:.17g}" for v in row.values()))
+    return "\n".join(lines) + "\n"
+
+
+def fit_growth_rate(t, amplitude, window):
+    """Least-squares exponential rate of ``amplitude`` over ``window``
+    (diagnostics.py:133-160): fits log(amplitude) = a + gamma t on the samples
+    with window[0] <= t <= window[1] and returns ``(gamma, stderr)``; at least
+    10 samples and positive amplitudes are required (ValueError otherwise)."""
+    t = np.asarray(t, dtype=float)
+    amplitude = np.asarray(amplitude, dtype=float)
+    lo, hi = window
+    keep = (t >= lo) & (t <= hi)
+    count = int(np.count_nonzero(keep))
+    if count < 10:
+        raise ValueError(f"window [{lo}, {hi}] holds {count} samples; need >= 10")
+    ts = t[keep]
+    amps = amplitude[keep]
+    if np.any(amps <= 0.0):
+        raise ValueError("amplitude must be positive on the fit window")
+    y = np.log(amps)
+    n = ts.size
+    tm = ts.mean()
+    ym = y.mean()
+    sxx = float(np.sum((ts - tm) ** 2))
+    gamma = float(np.sum((ts - tm) * (y - ym)) / sxx)
+    resid = y - (ym + gamma * (ts - tm))
+    stderr = math.sqrt(float(np.sum(resid ** 2)) / max(n - 2, 1) / sxx)
+    return gamma, stderr
+
+
+def fit_peak_rate(t, amplitude, window):
+    """Damping/growth rate fitted on the local maxima of ``amplitude`` inside
+    ``window`` (the robust choice for oscillating, damped |E|):
+    ``fit_growth_rate``'s least squares on the peaks only; returns
+    ``(gamma, stderr)``.  Needs at least 3 peaks."""
+    t = np.asarray(t, dtype=float)
+    a = np.asarray(amplitude, dtype=float)
+    lo, hi = window
+    idx = [i for i in range(1, len(a) - 1) if a[i] >= a[i - 1] and a[i] > a[i + 1] and lo <= t[i] <= hi]
+    if len(idx) < 3:
+        raise ValueError(f"window [{lo}, {hi}] holds {len(idx)} amplitude peaks; need >= 3")
+    ts, y = t[idx], np.log(a[idx])
+    tm, ym = ts.mean(), y.mean()
+    sxx = float(np.sum((ts - tm) ** 2))
+    gamma = float(np.sum((ts - tm) * (y - ym)) / sxx)
+    resid = y - (ym + gamma * (ts - tm))
+    return gamma, math.sqrt(float(np.sum(resid ** 2)) / max(len(idx) - 2, 1) / sxx)
 
 
 class DeviceDiagnostics:

@@ -49,7 +49,11 @@ def _wavenumbers(n, h):
 class FieldSolver:
     """Device moment -> rho -> E chain for a set of species on one physical grid."""
 
-    def __init__(self, grids, species, device):
+    def __init__(self, grids, species, device, schedule="velocity-major"):
+        if schedule not in ("velocity-major", "position-major", "free"):
+            raise ValueError(f"unknown schedule {schedule!r}")
+        self.schedule = schedule
+        self._moment_fn = "vpfv_moment_seq" if schedule == "position-major" else "vpfv_moment"
         self.grids = list(grids)
         self.species = list(species)
         self.device = device
@@ -173,7 +177,7 @@ class FieldSolver:
     def moments(self, srcs, stream=None):
         stream = stream_handle(self.device) if stream is None else stream
         for s, (g, f) in enumerate(zip(self.grids, srcs)):
-            _lib.call("vpfv_moment", f.data_ptr(), self.n[s].data_ptr(), g.d, g.v,
+            _lib.call(self._moment_fn, f.data_ptr(), self.n[s].data_ptr(), g.d, g.v,
                       self.N_arrays[s], self.vols[s], stream)
         return self.n
 
@@ -235,10 +239,14 @@ def _dev_array(a, device):
 
 
 def zeroth_moment(f, schedule="velocity-major"):
-    """n(x) = sum_v f * prod(h_v) (fields.py:86-111); bitwise the fold tree.
+    """n(x) = sum_v f * prod(h_v) (fields.py:86-111).
 
-    Every schedule maps to the deterministic fold tree on the device (the
-    reference's schedules agree to summation-order rounding).
+    ``"velocity-major"``: the deterministic fold tree (``vpfv_moment``,
+    bitwise the reference); ``"position-major"``: the per-cell sequential sum
+    in C order (``vpfv_moment_seq``, bitwise the reference's compiled
+    ``_seq_moment_*``); ``"free"``: the reference's library reduction with no
+    fixed order ("performance experiments only") -- here the fold tree, one
+    valid order of that sum.
     """
     if schedule not in ("velocity-major", "position-major", "free"):
         raise ValueError(f"unknown schedule {schedule!r}")
@@ -246,9 +254,38 @@ def zeroth_moment(f, schedule="velocity-major"):
     device = _device_of(f.data)
     data = _dev_array(f.data, device)
     out = torch.empty(tuple(g.N[:g.d]), dtype=torch.float64, device=device)
-    _lib.call("vpfv_moment", data.data_ptr(), out.data_ptr(), g.d, g.v, _lib.int_array(g.N),
+    fn = "vpfv_moment_seq" if schedule == "position-major" else "vpfv_moment"
+    _lib.call(fn, data.data_ptr(), out.data_ptr(), g.d, g.v, _lib.int_array(g.N),
               velocity_cell_volume(g), stream_handle(device))
     return out if isinstance(f.data, torch.Tensor) else out.cpu().numpy()
+
+
+def higher_moments(f):
+    """Momentum and kinetic-energy densities on the physical grid with the
+    midpoint-to-average lift (fields.py:131-161): returns ``(momentum,
+    kinetic)``, ``momentum`` one physical-grid array per velocity dim and
+    ``kinetic`` = 1/2 sum_d <v_d^2 f>.  Ghosts must be synchronised.  Device
+    data: the velocity sums run in ``vpfv_higher_moments``; host data: the
+    reference's numpy arithmetic."""
+    from .diagnostics import higher_moments_arrays
+
+    g = f.grid
+    if not isinstance(f.data, torch.Tensor):
+        return higher_moments_arrays(np.asarray(f.data), g)
+    device = f.data.device
+    data = f.data.contiguous()
+    vcs = [torch.as_tensor(g.centers(k), dtype=torch.float64, device=device) for k in g.velocity_dims]
+    hv = [g.h[k] for k in g.velocity_dims]
+    out = torch.empty(tuple(g.N[:g.d]) + (2 * g.v,), dtype=torch.float64, device=device)
+    _lib.call("vpfv_higher_moments", data.data_ptr(), g.d, g.v, _lib.int_array(g.N), vcs[0].data_ptr(),
+              vcs[1].data_ptr() if len(vcs) > 1 else None, hv[0], hv[1] if len(hv) > 1 else 0.0,
+              out.data_ptr(), stream_handle(device))
+    vol = velocity_cell_volume(g)
+    mom = [out[..., 2 * k] * vol for k in range(g.v)]
+    kin = 0.0
+    for k in range(g.v):
+        kin = kin + out[..., 2 * k + 1] * vol
+    return mom, 0.5 * kin
 
 
 def charge_density(densities, species):

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .diagnostics import conserved_quantities
+from .diagnostics import conserved_quantities_arrays
 from .fields import FieldSolver
 from .fvm import max_speed_per_dim
 from .grid import DistField, FrozenGhosts, fill_local_ghosts
@@ -94,7 +94,7 @@ class Simulation:
         # velocity ghosts are frozen: all three buffers start as the filled t=0 array
         self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
         self.tables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
-        self.fields = FieldSolver(self.grids, self.species, self.device)
+        self.fields = FieldSolver(self.grids, self.species, self.device, schedule)
         base = _lib.VPFV_EXACT if exact else 0
         self.flags = [base | wrap_flags(g) for g in self.grids]
         S = len(self.species)
@@ -110,7 +110,9 @@ class Simulation:
         # f0) serve the next step's stage 1 unless f0 was modified in place
         # since (torch's version counter) -- then the standalone moment runs
         self.tiled = [t.fused_moment_ok(f) for t, f in zip(self.tables, self.flags)]
-        self.fuse_moment = all(self.tiled)
+        # the fused epilogue partials are nodes of the fold tree: the
+        # sequential "position-major" sum needs the standalone moment
+        self.fuse_moment = all(self.tiled) and schedule != "position-major"
         mk = lambda: ([torch.empty(t.partials_shape(), dtype=torch.float64, device=self.device)  # noqa: E731
                        for t in self.tables] if self.fuse_moment else None)
         self.partials = mk()       # written by stages 1-3, read by stages 2-4
@@ -363,7 +365,7 @@ class Simulation:
     def diagnostics_row_host(self, dt):
         """The same row from a host copy of the state (the reference path)."""
         E = self._E_host(self.ctx.f0)
-        return conserved_quantities(self._host_state(), self.grids, self.species, E, self.ctx.t, dt)
+        return conserved_quantities_arrays(self._host_state(), self.grids, self.species, E, self.ctx.t, dt)
 
     def field_amplitude(self):
         from .diagnostics import field_amplitude

@@ -20,7 +20,7 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2410_12155_b200 import problems as P, runner as R  # noqa: E402
-from paper_2410_12155_b200.diagnostics import DiagnosticsRow, fit_growth_rate  # noqa: E402
+from paper_2410_12155_b200.diagnostics import DiagnosticsRow, fit_growth_rate, fit_peak_rate  # noqa: E402
 
 out = sys.argv[1] if len(sys.argv) > 1 else "profiles"
 os.makedirs(out, exist_ok=True)
@@ -43,13 +43,13 @@ def run(name, setup, t_end, cadence, max_steps=10 ** 7):
 summary = {}
 sim, rows, wall = run("landau1d", P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128), 20.0, 5)
 ts, amps = [r.t for r in rows], [r.field_amplitude for r in rows]
-gamma = fit_growth_rate(ts, amps, t_min=0.0, t_max=20.0, peaks=True)
+gamma, _ = fit_peak_rate(ts, amps, (0.0, 20.0))
 summary["landau1d_128"] = {"steps": sim.step_count, "wall_s": wall, "damping_rate": gamma,
                            "reference_root": -0.153359, "rel_err": abs(gamma + 0.153359) / 0.153359}
 
 sim, rows, wall = run("twostream", P.make_problem(P.ProblemSpec("two-stream"), 1024, 1024), 30.0, 10)
 ts, amps = [r.t for r in rows], [r.field_amplitude for r in rows]
-gamma = fit_growth_rate(ts, amps, t_min=10.0, t_max=25.0)
+gamma, _ = fit_growth_rate(ts, amps, (10.0, 25.0))
 summary["twostream_1024"] = {"steps": sim.step_count, "wall_s": wall, "growth_rate": gamma,
                              "reference_root": 0.2931724221224933,
                              "rel_err": abs(gamma - 0.2931724221224933) / 0.2931724221224933}

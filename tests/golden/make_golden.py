@@ -228,9 +228,74 @@ def make_cluster_fixture():
     assert np.array_equal(a.interiors()[0], b.gather(0))
 
 
+def make_diagnostics_fixtures():
+    """Reference diagnostics (diagnostics.py:85-180, fields.py:50-161):
+    conserved-quantity rows, higher moments and both moment schedules of the
+    3-step states of the step fixtures, ``rows_to_csv`` text, growth-rate fits
+    (a synthetic series and a real 1D-1V Landau run) and Richardson errors."""
+    from vpfv.diagnostics import fit_growth_rate, richardson_error, rows_to_csv
+    from vpfv.fields import higher_moments
+
+    cases = [
+        ("landau1d", lambda: make_landau_1d(landau_spec(alpha=0.01), 16, 16), 0.05),
+        ("twostream", lambda: make_problem(ProblemSpec("two-stream"), 16, 16), 0.05),
+        ("dgh", lambda: make_problem(ProblemSpec("dgh"), 8, 8), 0.05),
+        ("lhdi", lambda: make_problem(ProblemSpec("lhdi"), 8, 8), 0.002),
+        ("bimax1d2v", lambda: bimaxwellian_1d2v(8, 8, 10), 0.02),
+        ("landau2d", lambda: make_problem(landau_spec(), 8, 8), 0.05),
+    ]
+    for name, mk, dt in cases:
+        sim = Simulation(mk(), dt=dt)
+        rows = [sim.diagnostics_row(0.0)]
+        for _ in range(3):
+            sim.advance(dt)
+        rows.append(sim.diagnostics_row(dt))
+        dists = sim._wrap(sim.ctx.f0)
+        out = {"row0": np.array(rows[0].values()), "row3": np.array(rows[1].values())}
+        for s, f in enumerate(dists):
+            mom, kin = higher_moments(f)
+            for k, m in enumerate(mom):
+                out[f"mom{k}_f{s}"] = np.asarray(m)
+            out[f"kin_f{s}"] = np.asarray(kin)
+            out[f"nvm_f{s}"] = zeroth_moment(f, "velocity-major")
+            out[f"npm_f{s}"] = zeroth_moment(f, "position-major")
+        names = [sp.name for sp in sim.species]
+        meta = dict(species_names=names, csv=rows_to_csv(rows, names), dt=dt)
+        save(f"diag_{name}.npz", meta, **out)
+
+    # growth-rate fits: a synthetic series and a real reference run
+    t = np.linspace(0.0, 30.0, 301)
+    amp = 1e-3 * np.exp(0.29 * t) * (1.0 + 0.01 * np.sin(3.0 * t))
+    g1 = fit_growth_rate(t, amp, (10.0, 25.0))
+    sim = Simulation(make_landau_1d(landau_spec(alpha=0.01), 32, 32))
+    rows = sim.run(6.0, cadence=1)
+    tr = np.array([r.t for r in rows])
+    ar = np.array([r.field_amplitude for r in rows])
+    g2 = fit_growth_rate(tr, ar, (0.0, 6.0))
+    errors = {}
+    for bad in [((0.0, 0.5),), ((0.0, 30.0),)]:
+        try:
+            fit_growth_rate(t, amp if bad[0][1] < 1 else -amp, bad[0])
+        except ValueError as e:
+            errors[str(bad[0])] = str(e)
+    rng = np.random.default_rng(40)
+    a, b = rng.random((4, 6)), rng.random((8, 12))
+    a3, b3 = rng.random((3, 4, 5)), rng.random((6, 8, 10))
+    rich = [richardson_error(a, b), richardson_error(a3, b3)]
+    save("fits.npz", dict(fit_synthetic=list(g1), fit_landau=list(g2), errors=errors, seed=40,
+                          richardson=rich),
+         t=t, amp=amp, t_landau=tr, amp_landau=ar)
+
+
 if __name__ == "__main__":
+    import sys as _sys
+
+    if "--diagnostics" in _sys.argv:
+        make_diagnostics_fixtures()
+        raise SystemExit(0)
     make_stage_fixtures()
     make_moment_fixtures()
     make_poisson_fixtures()
     make_step_fixtures()
     make_cluster_fixture()
+    make_diagnostics_fixtures()

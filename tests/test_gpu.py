@@ -291,11 +291,11 @@ def _amplitude_history(sim, t_end):
 
 
 def test_landau_damping_rate():
-    from paper_2410_12155_b200.diagnostics import fit_growth_rate
+    from paper_2410_12155_b200.diagnostics import fit_peak_rate
 
     sim = R.Simulation(P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128))
     ts, amps = _amplitude_history(sim, 20.0)
-    gamma = fit_growth_rate(ts, amps, peaks=True)
+    gamma, _ = fit_peak_rate(ts, amps, (0.0, 20.0))
     root = -0.15335946690960492  # test_dispersion.py:497-508 (k = 0.5)
     assert abs(gamma - root) <= 0.02 * abs(root), gamma
     assert abs(gamma - (-0.15416)) <= 2e-3  # CPU oracle fit at 128^2
@@ -306,7 +306,8 @@ def test_two_stream_growth_rate():
 
     sim = R.Simulation(P.make_problem(P.ProblemSpec("two-stream"), 256, 256))
     ts, amps = _amplitude_history(sim, 25.0)
-    gamma = fit_growth_rate(ts, amps, t_min=10.0, t_max=25.0)
+    gamma, stderr = fit_growth_rate(ts, amps, (10.0, 25.0))  # the reference signature (diagnostics.py:133)
+    assert stderr < 0.01
     root = 0.2931724221224933  # test_dispersion.py:185-212 table, k = 0.6, v_T^2 = 0.1
     assert abs(gamma - root) <= 0.01 * root, gamma
     assert abs(gamma - 0.29312) <= 1e-3  # CPU oracle fit at 256^2
