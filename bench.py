@@ -266,13 +266,17 @@ def run_b200(args, rank, world, device):
         sim.advance(dt)
     barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(device.index) as clocks:
         start.record(stream)
-        for _ in range(args.steps):
+        marks[0].record(stream)
+        for k in range(args.steps):
             sim.advance(dt)
+            marks[k + 1].record(stream)
         stop.record(stream)
         barrier()
         ms_local = start.elapsed_time(stop)
+    per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps))
     sim.enable_stage_timing(True)
     sim.advance(dt)  # captures the evented graph variant
     sim.enable_stage_timing(True)  # reset the accumulators
@@ -288,6 +292,8 @@ def run_b200(args, rank, world, device):
         ms_roofline_pass = start.elapsed_time(stop)
     stage_ms = sim.stage_kernel_ms()  # per RK stage slot, summed over the pass's steps and species
     sim.enable_stage_timing(False)
+    launches_per_step = sim.launches_per_step()
+    nvlink = nvlink_line(sim, world, ms_local / args.steps)
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], dtype=torch.float64, device=device)
@@ -295,6 +301,10 @@ def run_b200(args, rank, world, device):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = cells_global * args.steps / (ms / 1e3)
+    q = lambda f: per_step[min(len(per_step) - 1, int(f * len(per_step)))]  # noqa: E731
+    step_stats = {"median_ms": statistics.median(per_step), "p10_ms": q(0.1), "p90_ms": q(0.9),
+                  "min_ms": per_step[0], "max_ms": per_step[-1], "rank": rank,
+                  "how": "CUDA events between consecutive steps of the timed region (rank 0's stream)"}
 
     # roofline of the dominant kernel (the fused stage), from in-graph events
     stage_bytes = sum(b * cells_local for b in STAGE_BYTES) * args.steps
@@ -305,6 +315,10 @@ def run_b200(args, rank, world, device):
         traffic, traffic_src = None, None
     achieved = stage_bytes / stage_s / 1e9 if stage_s > 0 else None
     share = stage_s / (ms_local / 1e3)
+    per_stage = [{"stage": k + 1, "ms": m / args.steps, "algorithmic_bytes_per_cell": STAGE_BYTES[k],
+                  "hbm_frac": (STAGE_BYTES[k] * cells_local * args.steps / (m / 1e3) / 1e9 / peak) if m > 0 else None}
+                 for k, m in enumerate(stage_ms)]
+    fp64 = fp64_roofline(args.workload, stage_ms, cells_local, args.steps)
 
     # end to end through the public API with host buffers:
     # H2D of the step's input state from pinned memory, step, D2H of the result
@@ -314,14 +328,16 @@ def run_b200(args, rank, world, device):
         e2e = e2e_measure(sim, dt, max(args.e2e_steps, min(2000, int(50.0 / max(ms_per_step, 1e-3)))), device,
                           cells_global)
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        del sim
+        parity = parity_check(args.workload, dt, device)
         v, info = cpu_reference_steps(make_setup(args.workload), dt, 2, budget_s=args.cpu_budget)
         cpu = {"value": v, "unit": "cell-updates/s", "cores": info["cores"], "kind": "port",
                "sample": f"{info['steps']} full RK4 step(s) of the same {args.workload} problem "
                          f"({info['seconds']:.1f} s), threaded C restatement of the reference kernels "
                          f"(oracle/stage_ref.c, bitwise = reference numba) + numpy FFT"}
-    launches = sim.launches_per_step() * args.steps
+    launches = launches_per_step * args.steps
     line = {
         "metric": "phase-space cell-updates/sec per RK4 step",
         "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
@@ -341,6 +357,8 @@ def run_b200(args, rank, world, device):
                      "algorithmic_bytes_per_cell_per_step": sum(STAGE_BYTES),
                      "stage_ms_per_step": [m / args.steps for m in stage_ms],
                      "share_of_step": share, "peak_kind": peak_kind,
+                     "per_stage": per_stage, "fp64": fp64,
+                     "fp64_frac": fp64["frac"] if fp64 else None,
                      "timing": (f"stage-kernel launch durations from CUDA events captured around every "
                                 f"stage launch in a second pass of the same {args.steps} steps, right after "
                                 f"the timed region, under the same clock sampling "
@@ -349,11 +367,67 @@ def run_b200(args, rank, world, device):
                      "clocks_roofline_pass": clocks_rp.summary()},
         "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
                           "frac": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9 / peak},
-        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-        "nvlink": nvlink_line(sim, world, ms / args.steps),
+        "step_stats": step_stats,
+        "e2e": e2e, "cpu_baseline": cpu, "parity": parity, "gpu_launches": launches,
+        "nvlink": nvlink,
         "clocks": clocks.summary(),
     }
     return line
+
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r2_fp64_peak.json")
+STAGE_PROFILE = os.path.join(ROOT, "profiles", "r2_stage_profile.json")
+
+
+def fp64_roofline(workload, stage_ms, cells, steps):
+    """FP64 issue roofline of the stage kernel: fp64 instructions per cell per
+    RK stage (DFMA + DMUL + DADD lane ops, counted in the committed ncu SASS
+    capture of the same kernel, profiles/r2_stage_profile.json) x cells / the
+    stage's event-timed duration, against the measured DFMA throughput of
+    this B200 (profiles/r2_fp64_peak.json, scripts/probes/fp64_peak.cu)."""
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            peak = float(json.load(f)["fp64_dfma_per_s"])
+        with open(STAGE_PROFILE) as f:
+            prof = json.load(f)
+    except (OSError, KeyError, ValueError):
+        return None
+    ops = prof.get("dp_ops_per_cell", {}).get(workload)
+    if not ops or len(ops) != 4:
+        return None
+    per = [o * cells * steps / (m / 1e3) if m > 0 else None for o, m in zip(ops, stage_ms)]
+    tot_ops = sum(o * cells * steps for o in ops)
+    tot_s = sum(stage_ms) / 1e3
+    achieved = tot_ops / tot_s if tot_s > 0 else None
+    return {"bound": "fp64", "dp_ops_per_cell_per_stage": ops, "achieved": achieved, "peak": peak,
+            "unit": "fp64 ops/s (DFMA, DMUL, DADD lane instructions)",
+            "frac": achieved / peak if achieved else None,
+            "per_stage_frac": [p / peak if p else None for p in per],
+            "source": os.path.relpath(STAGE_PROFILE, ROOT) + " + " + os.path.relpath(FP64_PEAK_FILE, ROOT)}
+
+
+def parity_check(workload, dt, device):
+    """One RK4 step of the benchmarked problem on the GPU against the threaded
+    C restatement of the reference (oracle/, the cpu_baseline leg), from the
+    same initial state with the same dt: relative L2 per species (north-star
+    bar 1e-12) and a checksum of each side."""
+    from oracle import cbackend as C
+    from paper_2410_12155_b200 import runner as R
+
+    setup = make_setup(workload)
+    sim = R.Simulation(setup, device=device)
+    sim.fixed_dt = dt
+    sim.advance(dt)
+    got = sim.interiors()
+    del sim
+    ref = C.CSimulation([f.grid for f in setup.dists], setup.species,
+                        [np.array(f.data) for f in make_setup(workload).dists], dt=dt)
+    ref.advance(dt)
+    want = ref.interiors()
+    rels = [float(np.linalg.norm(a - b) / np.linalg.norm(b)) for a, b in zip(got, want)]
+    return {"steps": 1, "rel_l2": rels, "bar": 1e-12, "ok": all(r <= 1e-12 for r in rels),
+            "checksum_gpu": [float(np.sum(a)) for a in got], "checksum_oracle": [float(np.sum(b)) for b in want],
+            "oracle": "oracle/stage_ref.c (threaded C restatement, bitwise = reference numba) + numpy FFT"}
 
 
 def l2_note(setup):
@@ -456,6 +530,27 @@ def run_reference(args):
     }
 
 
+def spawn_ranks(n):
+    """``python bench.py --gpus N`` without a launcher: re-exec through
+    torch.distributed.run with one rank per GPU on 127.0.0.1 (the driver's own
+    launch line), after checking that N GPUs are visible (VPFV_SAME_DEVICE=1
+    puts every rank on GPU 0 -- validation only).  Returns the exit code."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n and not os.environ.get("VPFV_SAME_DEVICE"):
+        print(f"[bench] --gpus {n} requested but only {have} GPU(s) are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, check=False).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -473,8 +568,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "b200" and world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)

@@ -518,6 +518,16 @@ class DistributedSimulation:
         self.vdim = g0.d  # the first velocity dim is the one split across velocity partitions
         self.x0, self.nloc = slab_bounds(g0.N[0], self.comm.px, self.comm.ix)
         self.vbox = [slab_bounds(g.N[self.vdim], self.comm.pv, self.comm.iv) for g in self.grids]
+        if self.comm.pv > 1:
+            # the per-rank folds + fold_pairs reproduce the global adjacent-pair
+            # fold tree only for power-of-two spans (the reference's own
+            # bitwise condition, test_partition.py:736-767)
+            for g in self.grids:
+                span = g.N[self.vdim] // self.comm.pv
+                if g.N[self.vdim] % self.comm.pv or span & (span - 1):
+                    raise ValueError(f"velocity_parts={self.comm.pv}: each rank's velocity span "
+                                     f"({g.N[self.vdim]}/{self.comm.pv}) must be a power of two for the "
+                                     f"densities to stay bitwise the single-GPU fold tree")
         self.lgrids = tuple(local_grid(g, self.x0, self.nloc, v0, nv) for g, (v0, nv) in zip(self.grids, self.vbox))
         f0 = []
         for f, (v0, nv) in zip(setup.dists, self.vbox):

@@ -358,7 +358,7 @@ class Simulation:
 
         t = None
         for a, g, name in zip(self.ctx.f0, self.grids, self._names):
-            _, t = load_device(os.path.join(directory, f"{tag}_{name}.vpfv"), a, g)
+            _, t = load_device(os.path.join(directory, f"{tag}_{name}.vpfv"), a, g, species=name)
         self.ctx.t = t
         return t
 
@@ -426,6 +426,13 @@ class HostPipeline:
         """Step ``host_in(k)`` (a list of pinned per-species arrays) into
         ``host_out(k)`` for k < steps; returns after the last download."""
         sim, main = self.sim, torch.cuda.current_stream(self.sim.device)
+        saved = (sim.ctx.f0, sim.ctx.fout)
+        try:
+            self._run(sim, main, host_in, host_out, dt, steps)
+        finally:  # the simulation's own state buffers, not the pipeline's double buffers
+            sim.ctx.f0, sim.ctx.fout = saved
+
+    def _run(self, sim, main, host_in, host_out, dt, steps):
         with torch.cuda.stream(self.h2d):
             for d, sl, h in zip(self.din[0], self._inner, host_in(0)):
                 d[sl].copy_(h, non_blocking=True)

@@ -114,19 +114,27 @@ def save_device(path, array, grid, name, time, planes=8):
             fh.write(bufs[pk & 1][:pn].numpy().tobytes())
 
 
-def load_device(path, array, grid, planes=8):
+def load_device(path, array, grid, planes=8, species=None):
     """Stream a snapshot's interior into the padded device ``array``
-    (ghosts untouched); returns (species name, time).  The file's grid must
-    match ``grid``."""
+    (ghosts untouched); returns (species name, time).  The file's grid
+    (extents, dimensionality, box bounds) must match ``grid`` and, when given,
+    its species tag ``species``.  The copies are ordered after the work
+    already queued on the caller's stream (e.g. a launched step still reading
+    ``array``)."""
     inner = grid.interior_slices()
     plane = tuple(grid.N[1:])
     bufs = [torch.empty((planes,) + plane, dtype=torch.float64).pin_memory() for _ in range(2)]
     copy = torch.cuda.Stream(array.device)
+    copy.wait_stream(torch.cuda.current_stream(array.device))
     done = [None, None]
     with open(path, "rb") as fh:
         name, time, g = _read_header(fh)
         if tuple(g.N) != tuple(grid.N) or (g.d, g.v) != (grid.d, grid.v):
             raise ValueError(f"snapshot grid {g.N} (d={g.d}, v={g.v}) does not match {grid.N}")
+        if tuple(g.lo) != tuple(grid.lo) or tuple(g.hi) != tuple(grid.hi):
+            raise ValueError(f"snapshot box {g.lo}..{g.hi} does not match {grid.lo}..{grid.hi}")
+        if species is not None and name != species:
+            raise ValueError(f"snapshot holds species {name!r}, expected {species!r}")
         per_plane = int(np.prod(plane)) * 8
         for k, (a, b) in enumerate(_chunks(grid, planes)):
             buf = bufs[k & 1]
