@@ -128,9 +128,13 @@ def test_device_diagnostics_and_moments_vs_reference(name):
         assert np.array_equal(n_pm, ref[f"npm_f{s}"])
         assert np.array_equal(F.zeroth_moment(f, "velocity-major").cpu().numpy(), ref[f"nvm_f{s}"])
         mom, kin = F.higher_moments(f)
+        # momentum is a cancelling sum (two-stream: +-v0 beams give 2e-5 out of
+        # terms of order n v0 ~ 1): the absolute bar is set by the summed
+        # magnitudes, bounded by sqrt(2 n kin), not by the result
+        mscale = np.sqrt(2.0 * np.abs(ref[f"kin_f{s}"]).max() * np.abs(ref[f"nvm_f{s}"]).max())
         for k, m in enumerate(mom):
             w = ref[f"mom{k}_f{s}"]
-            assert np.allclose(m.cpu().numpy(), w, rtol=1e-12, atol=1e-14 * np.abs(w).max())
+            assert np.allclose(m.cpu().numpy(), w, rtol=1e-12, atol=1e-13 * mscale)
         w = ref[f"kin_f{s}"]
         assert np.allclose(kin.cpu().numpy(), w, rtol=1e-12, atol=1e-14 * np.abs(w).max())
 
