@@ -875,3 +875,43 @@ def test_cfl_solve_from_cached_partials(problem, N, Nv):
     c = sim._E_host(sim.ctx.f0)
     for k in b:
         assert np.array_equal(c[k], b[k])
+
+
+def test_dropin_host_stepping_allocation_audit_and_parity():
+    """The drop-in ``fused_stage`` on host arrays
+    stepping the reference's 3-buffer RK4 protocol: after a warm-up step, ten
+    more allocate nothing field-sized on the host (the reference's own audit,
+    /root/reference/pkg/tests/test_timestepping.py:234-254) or on the device,
+    and the state matches the oracle's numpy restatement stepping the same
+    protocol (exact mode: bitwise the reference kernels)."""
+    import tracemalloc
+
+    from paper_2410_12155_b200.timestepping import RK4_STAGES
+
+    c = G.stage_case("stage_2d2v_frozen")
+    g, og, sp, E = pgrid(c["grid"]), c["grid"], c["species"], c["E"]
+    host = {"f0": c["src"].copy(), "f1": np.zeros(g.padded_shape), "fout": np.zeros(g.padded_shape)}
+    ref = {k: v.copy() for k, v in host.items()}
+
+    def step(bufs, fs, **kw):
+        for dn, an, bn, sn, ca, cb, cd, div in RK4_STAGES:
+            fs(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.01 / div, g if fs is K.fused_stage else og,
+               sp, E, **kw)
+        bufs["f0"], bufs["fout"] = bufs["fout"], bufs["f0"]
+
+    step(host, K.fused_stage)
+    step(ref, O.fused_stage, check=False)
+    torch.cuda.synchronize()
+    dev0 = torch.cuda.memory_allocated()
+    tracemalloc.start()
+    base, _ = tracemalloc.get_traced_memory()
+    for _ in range(10):
+        step(host, K.fused_stage)
+    _, peak = tracemalloc.get_traced_memory()
+    tracemalloc.stop()
+    assert peak - base < host["f0"].nbytes / 4, f"stepping allocated {peak - base} bytes on the host"
+    assert torch.cuda.memory_allocated() == dev0
+    for _ in range(10):
+        step(ref, O.fused_stage, check=False)
+    inner = g.interior_slices()
+    assert np.array_equal(host["f0"][inner], ref["f0"][inner])
