@@ -527,8 +527,9 @@ def combine_partials(partials, ranks=None, log=None, stage=0, cell_count=None):
         nxt, nwho = [], []
         for i in range(0, len(level) - 1, 2):
             if log is not None and who[i] is not None:
-                log.log(stage, "reduce", who[i + 1], who[i], cell_count if cell_count is not None
-                        else np.size(level[i + 1]))
+                up = level[i + 1]
+                n = cell_count if cell_count is not None else (up.numel() if hasattr(up, "numel") else np.size(up))
+                log.log(stage, "reduce", who[i + 1], who[i], n)
             nxt.append(level[i] + level[i + 1])
             nwho.append(who[i])
         if len(level) % 2:
@@ -541,3 +542,33 @@ def combine_partials(partials, ranks=None, log=None, stage=0, cell_count=None):
 def reduction_rounds(m):
     """ceil(log2 m) combine rounds for m partials."""
     return (int(m) - 1).bit_length()
+
+
+def _main(argv=None):
+    """``python -m paper_2410_12155_b200.partition plan ...``: the plan report
+    of the reference's ``vpfv plan`` (cli.py:207-222) for a uniform grid given
+    on the command line instead of an INI file (the config layer is out of
+    scope)."""
+    import argparse
+    import json
+
+    ap = argparse.ArgumentParser(prog="python -m paper_2410_12155_b200.partition")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    p = sub.add_parser("plan", help="partition plan report (JSON)")
+    p.add_argument("--d", type=int, required=True)
+    p.add_argument("--v", type=int, required=True)
+    p.add_argument("--N", type=int, nargs="+", required=True, help="cells per dim (one species)")
+    p.add_argument("--n", type=int, nargs="+", required=True, help="partitions per dim")
+    p.add_argument("--species", type=int, default=1)
+    p.add_argument("--r", type=int, default=1, help="species per rank")
+    p.add_argument("--strategy", default="vp", choices=STRATEGIES)
+    p.add_argument("--vmax", type=float, default=6.0)
+    a = ap.parse_args(argv)
+    g = make_grid(a.d, a.v, a.N, [0.0] * a.d + [-a.vmax] * a.v, [2 * math.pi] * a.d + [a.vmax] * a.v,
+                  periodic=tuple([True] * a.d + [False] * a.v))
+    plan = plan_partitions([g] * a.species, a.n, r=a.r, strategy=a.strategy)
+    print(json.dumps(plan.to_report(), indent=2))
+
+
+if __name__ == "__main__":
+    _main()
