@@ -61,21 +61,24 @@ STAGE_BYTES = (16, 24, 24, 32)  # algorithmic bytes/cell of RK stages 1..4 (SURV
 WEAK = {"ep2d2v-64"}  # per-GPU box fixed: the global x extent grows with the rank count (BASELINE config 5)
 
 
-def make_setup(name, world=1):
+def make_setup(name, world=1, device=None):
+    """The workload's set-up; ``device``: padded arrays built on the GPU
+    (problems.separable_on_device, bitwise the host builder)."""
     from paper_2410_12155_b200 import problems as P
 
+    kw = {"device": device}
     if name == "landau2d-128":
-        return P.make_problem(P.landau_spec(), 128, 128)
+        return P.make_problem(P.landau_spec(), 128, 128, **kw)
     if name == "landau1d-128":
-        return P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128)
+        return P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128, **kw)
     if name == "landau2d-64":
-        return P.make_problem(P.landau_spec(), 64, 64)
+        return P.make_problem(P.landau_spec(), 64, 64, **kw)
     if name == "twostream-1024":
-        return P.make_problem(P.ProblemSpec("two-stream"), 1024, 1024)
+        return P.make_problem(P.ProblemSpec("two-stream"), 1024, 1024, **kw)
     if name == "weibel-256":
-        return P.make_bimaxwellian_1d2v(256, 256, 256)
+        return P.make_bimaxwellian_1d2v(256, 256, 256, **kw)
     if name == "ep2d2v-64":  # 64^4 per species per GPU; N ranks hold N x-slabs of 64 planes
-        return P.make_electron_proton_2d2v((64 * world, 64), (64, 64))
+        return P.make_electron_proton_2d2v((64 * world, 64), (64, 64), **kw)
     raise ValueError(name)
 
 
@@ -223,7 +226,12 @@ def run_b200(args, rank, world, device):
     from paper_2410_12155_b200 import runner as R
     from paper_2410_12155_b200.kernels import stream_handle  # noqa: F401
 
-    setup = make_setup(args.workload, world)
+    import torch as _t
+
+    t0 = time.perf_counter()
+    setup = make_setup(args.workload, world, device=device if world == 1 else None)
+    _t.cuda.synchronize(device)
+    setup_s = time.perf_counter() - t0
     if world > 1:
         from paper_2410_12155_b200.parallel import DistributedSimulation
 
@@ -336,11 +344,15 @@ def run_b200(args, rank, world, device):
         torch.cuda.empty_cache()
         e2e_dropin = e2e_dropin_measure(setup, h0, E_host, dt, device, cells_global)
 
-    cpu, parity = None, None
+    cpu, parity, host_setup_s = None, None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sim = None
         parity = parity_check(args.workload, dt, device)
-        v, info = cpu_reference_steps(make_setup(args.workload), dt, 2, budget_s=args.cpu_budget)
+        t0 = time.perf_counter()
+        host_setup = make_setup(args.workload)
+        host_setup_s = time.perf_counter() - t0
+        v, info = cpu_reference_steps(host_setup, dt, 2, budget_s=args.cpu_budget)
+        del host_setup
         cpu = {"value": v, "unit": "cell-updates/s", "cores": info["cores"], "kind": "port",
                "sample": f"{info['steps']} full RK4 step(s) of the same {args.workload} problem "
                          f"({info['seconds']:.1f} s), threaded C restatement of the reference kernels "
@@ -376,7 +388,11 @@ def run_b200(args, rank, world, device):
         "step_roofline": {"achieved_GBs": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9,
                           "frac": 96 * cells_local * args.steps / (ms_local / 1e3) / 1e9 / peak},
         "step_stats": step_stats,
-        "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu, "parity": parity, "gpu_launches": launches,
+        "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu,
+        "setup": {"built_on": "device" if world == 1 else "host", "seconds": setup_s, "host_build_seconds": host_setup_s,
+                  "how": "make_problem factor arrays on the host, the padded product on the GPU "
+                         "(vpfv_init_separable, bitwise the host builder); host_build_seconds: the numpy "
+                         "builder of the same set-up (built for the cpu_baseline leg)"}, "parity": parity, "gpu_launches": launches,
         "nvlink": nvlink,
         "clocks": clocks.summary(),
     }

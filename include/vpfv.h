@@ -363,6 +363,19 @@ int vpfv_box_copy(double *dst, const long long *ds, const int *dorig,
                   int ndim, const int *ext, void *stream);
 
 /* ---------------------------------------------------------------------- */
+/* Separable initial condition on the padded box (nphys padded physical
+ * cells x nv1 x nv2 padded velocity cells, velocity fastest):
+ * out = sum_{t < nterms} (P_t[p] * V1_t[k]) * V2_t[l], each product and the
+ * sum rounded once in that order -- numpy's broadcast of the reference
+ * set-ups (problems.py:210-507), so bitwise the host builder.  nv2 == 1:
+ * one velocity dim, V2 unused.  Replaces the host product + upload of
+ * make_problem for production-size grids. */
+int vpfv_init_separable(double *out, long long nphys, int nv1, int nv2,
+                        const double *P0, const double *V10, const double *V20,
+                        const double *P1, const double *V11, const double *V21,
+                        int nterms, void *stream);
+
+/* ---------------------------------------------------------------------- */
 int vpfv_version(void);
 /* 0 if device `dev` is an sm_100 part this library was built for. */
 int vpfv_check_device(int dev);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "vpfv_wrap_fill": (_i, [_p, _i, _p, _u, _p]),
     "vpfv_box_copy": (_i, [_p, _p, _p, _p, _p, _p, _i, _p, _p]),
     "vpfv_version": (_i, []),
+    "vpfv_init_separable": (_i, [_p, ctypes.c_longlong, _i, _i] + [_p] * 6 + [_i, _p]),
     "vpfv_check_device": (_i, [_i]),
     "vpfv_last_error": (ctypes.c_char_p, []),
 }

@@ -143,9 +143,55 @@ static int launch_box(double *dst, const double *src, const Box &b, cudaStream_t
     return check_launch("box_copy");
 }
 
+// ---------------------------------------------------------------------------
+// separable initial conditions: out = sum_t (P_t[phys] * V1_t[vx]) * V2_t[vy]
+// over the padded box, each product rounded once in numpy's left-to-right
+// broadcast order (the reference set-ups, problems.py:210-507, are products
+// of Gauss-Legendre line / plane averages), so the result is bitwise the
+// host builder's.  One thread per padded vy row segment, vy fastest.
+
+struct SepTerm {
+    const double *P, *V1, *V2;
+};
+
+__global__ void init_separable_kernel(double *__restrict__ out, long long nphys, int nv1, int nv2, SepTerm t0,
+                                      SepTerm t1, int nterms) {
+    const long long n = nphys * nv1 * nv2;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int l = (int)(i % nv2);
+        const long long r = i / nv2;
+        const int k = (int)(r % nv1);
+        const long long p = r / nv1;
+        double v = __dmul_rn(t0.P[p], t0.V1[k]);
+        if (t0.V2) v = __dmul_rn(v, t0.V2[l]);
+        if (nterms > 1) {
+            double w = __dmul_rn(t1.P[p], t1.V1[k]);
+            if (t1.V2) w = __dmul_rn(w, t1.V2[l]);
+            v = __dadd_rn(v, w);
+        }
+        out[i] = v;
+    }
+}
+
 }  // namespace vpfv
 
 using namespace vpfv;
+
+extern "C" int vpfv_init_separable(double *out, long long nphys, int nv1, int nv2, const double *P0,
+                                   const double *V10, const double *V20, const double *P1, const double *V11,
+                                   const double *V21, int nterms, void *stream) {
+    if (nterms < 1 || nterms > 2 || nphys < 1 || nv1 < 1 || nv2 < 1 || !P0 || !V10 || (nterms > 1 && (!P1 || !V11)))
+        return set_error(VPFV_EARG, "init_separable: bad arguments");
+    if (nv2 > 1 && (!V20 || (nterms > 1 && !V21))) return set_error(VPFV_EARG, "init_separable: missing V2");
+    SepTerm t0{P0, V10, nv2 > 1 ? V20 : nullptr}, t1{P1, V11, nv2 > 1 ? V21 : nullptr};
+    const long long n = nphys * nv1 * nv2;
+    const int block = 256;
+    const long long want = (n + block - 1) / block;
+    const int grid = (int)(want < 148LL * 16 ? want : 148LL * 16);
+    init_separable_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(out, nphys, nv1, nv2, t0, t1, nterms);
+    return check_launch("init_separable");
+}
 
 extern "C" int vpfv_tables_1d(const double *Ex, double *e, double *c1, int Nx, double qmk2,
                               double g, double t1, double den1, void *stream) {

@@ -57,6 +57,20 @@ def _host_filled(f):
     return data, frozen
 
 
+def _device_filled(f, device):
+    """A device-resident set-up field with the ghosts _host_filled would
+    give it: the velocity slabs are its own t=0 values (frozen), the periodic
+    dims are wrapped whole-column in ascending order on the device
+    (vpfv_wrap_fill, grid.py:263-277)."""
+    g = f.grid
+    data = f.data.to(device=device, dtype=torch.float64).contiguous().clone()
+    mask = sum(1 << k for k in range(g.ndim) if g.periodic[k])
+    if mask:
+        _lib.call("vpfv_wrap_fill", data.data_ptr(), g.ndim, _lib.int_array(g.N), mask,
+                  torch.cuda.current_stream(device).cuda_stream)
+    return data
+
+
 def require_cuda(device=None):
     if not torch.cuda.is_available():
         raise _lib.VpfvError("no CUDA device visible: the B200 path has no CPU fallback")
@@ -88,9 +102,13 @@ class Simulation:
         self._names = [f.species for f in setup.dists]
         f0, self.frozen = [], []
         for f in setup.dists:
-            data, frozen = _host_filled(f)
-            f0.append(torch.from_numpy(data).to(self.device))
-            self.frozen.append(frozen)
+            if isinstance(f.data, torch.Tensor) and f.data.is_cuda:
+                f0.append(_device_filled(f, self.device))  # built on the device (problems.separable_on_device)
+                self.frozen.append(None)  # captured from the device buffer when a host view needs it
+            else:
+                data, frozen = _host_filled(f)
+                f0.append(torch.from_numpy(data).to(self.device))
+                self.frozen.append(frozen)
         # velocity ghosts are frozen: all three buffers start as the filled t=0 array
         self.ctx = StepContext(f0=f0, f1=[a.clone() for a in f0], fout=[a.clone() for a in f0])
         self.tables = [StageTables(g, sp, self.device, corrections) for g, sp in zip(self.grids, self.species)]
@@ -310,6 +328,9 @@ class Simulation:
 
     def _host_state(self):
         datas = []
+        for s_, (a, g) in enumerate(zip(self.ctx.f0, self.grids)):
+            if self.frozen[s_] is None:  # device-built set-up: the velocity slabs never change
+                self.frozen[s_] = FrozenGhosts.capture(DistField(g, data=a.cpu().numpy()))
         for a, g, fr in zip(self.ctx.f0, self.grids, self.frozen):
             h = a.cpu().numpy().copy()
             fill_local_ghosts(DistField(g, data=h), fr)

@@ -915,3 +915,32 @@ def test_dropin_host_stepping_allocation_audit_and_parity():
         step(ref, O.fused_stage, check=False)
     inner = g.interior_slices()
     assert np.array_equal(host["f0"][inner], ref["f0"][inner])
+
+
+@pytest.mark.parametrize("build", [
+    lambda dev: P.make_problem(P.landau_spec(), 32, 32, device=dev),
+    lambda dev: P.make_landau_1d(P.landau_spec(alpha=0.01), 64, 64, device=dev),
+    lambda dev: P.make_problem(P.ProblemSpec("two-stream"), 64, 128, device=dev),
+    lambda dev: P.make_problem(P.ProblemSpec("lhdi"), 16, 16, device=dev),
+    lambda dev: P.make_bimaxwellian_1d2v(32, 32, 32, device=dev),
+    lambda dev: P.make_electron_proton_2d2v((32, 32), (32, 32), device=dev),
+], ids=["landau2d-32", "landau1d-64", "twostream-64x128", "lhdi-16", "bimax-32", "ep2d2v-32"])
+def test_device_initial_conditions_bitwise_host(build):
+    """problems.separable_on_device (vpfv_init_separable) builds the padded
+    initial arrays on the GPU bitwise equal to the host builder (itself
+    bitwise the reference, tests/test_host.py); a Simulation started from the
+    device set-up steps bitwise like one started from the host set-up."""
+    from paper_2410_12155_b200 import runner as R
+
+    dev_setup, host_setup = build("cuda:0"), build(None)
+    for fd, fh in zip(dev_setup.dists, host_setup.dists):
+        assert isinstance(fd.data, torch.Tensor) and fd.data.is_cuda
+        assert np.array_equal(fd.data.cpu().numpy(), fh.data)
+    a, b = R.Simulation(dev_setup), R.Simulation(host_setup)
+    dt = 0.5 * b.max_dt()
+    for sim in (a, b):
+        sim.advance(dt)
+    for x, y in zip(a.interiors(), b.interiors()):
+        assert np.array_equal(x, y)
+    for x, y in zip(a._host_state(), b._host_state()):  # ghosts too (frozen slabs captured from the device)
+        assert np.array_equal(x, y)
