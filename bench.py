@@ -41,6 +41,7 @@ WORKLOADS = {
     "landau2d-128": "2D2V Landau damping 128^2 x 128^2, single electron species (BASELINE config 4)",
     "landau1d-128": "1D1V Landau damping 128 x 128, alpha = 0.01 (BASELINE config 1)",
     "landau2d-64": "2D2V Landau damping 64^2 x 64^2 (reduced, for quick runs)",
+    "landau2d-32": "2D2V Landau damping 32^2 x 32^2 (single-core numpy CPU-leg sample only)",
     "twostream-1024": "1D1V two-stream 1024 x 1024 (BASELINE config 2)",
     "weibel-256": "1D2V bi-Maxwellian 256^3 (BASELINE config 3)",
     "ep2d2v-64": "2D2V electron-proton m_r=1836, 64^4 per species (BASELINE config 5, per GPU)",
@@ -49,6 +50,7 @@ WORKLOADS = {
 KERNEL_OF = {  # the dominant (stage) kernel of each workload
     "landau2d-128": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "landau2d-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
+    "landau2d-32": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "ep2d2v-64": "stage2d2v_rb_kernel (fused 2D-2V RHS + RK4 update, TMA-tiled)",
     "weibel-256": "stage1d2v_rb_kernel (fused 1D-2V RHS + RK4 update, TMA-tiled)",
     "twostream-1024": "stage_1d1v_march_kernel (fused 1D-1V RHS + RK4 update, x-marching, bulk-copied rows)",
@@ -73,6 +75,8 @@ def make_setup(name, world=1, device=None):
         return P.make_landau_1d(P.landau_spec(alpha=0.01), 128, 128, **kw)
     if name == "landau2d-64":
         return P.make_problem(P.landau_spec(), 64, 64, **kw)
+    if name == "landau2d-32":
+        return P.make_problem(P.landau_spec(), 32, 32, **kw)
     if name == "twostream-1024":
         return P.make_problem(P.ProblemSpec("two-stream"), 1024, 1024, **kw)
     if name == "weibel-256":
@@ -353,10 +357,12 @@ def run_b200(args, rank, world, device):
         host_setup_s = time.perf_counter() - t0
         v, info = cpu_reference_steps(host_setup, dt, 2, budget_s=args.cpu_budget)
         del host_setup
+        legs = cpu_legs(args.workload)
         cpu = {"value": v, "unit": "cell-updates/s", "cores": info["cores"], "kind": "port",
                "sample": f"{info['steps']} full RK4 step(s) of the same {args.workload} problem "
                          f"({info['seconds']:.1f} s), threaded C restatement of the reference kernels "
-                         f"(oracle/stage_ref.c, bitwise = reference numba) + numpy FFT"}
+                         f"(oracle/stage_ref.c, bitwise = reference numba) + numpy FFT; built -O3 without "
+                         f"-march (portable baseline)", "single_core_legs": legs}
     launches = launches_per_step * args.steps
     line = {
         "metric": "phase-space cell-updates/sec per RK4 step",
@@ -598,6 +604,67 @@ def run_reference(args):
     }
 
 
+LEG_WORKLOAD = {"landau2d-128": "landau2d-64", "ep2d2v-64": "ep2d2v-64", "weibel-256": "weibel-256",
+                "twostream-1024": "twostream-1024", "landau1d-128": "landau1d-128", "landau2d-64": "landau2d-64"}
+
+
+def cpu_leg_child(kind, workload):
+    """One single-core CPU leg (run in a subprocess with OMP_NUM_THREADS=1):
+    ``numpy`` = the oracle's restatement of the reference's production driver
+    (OracleSimulation, rhs="numpy": runner.py:183-191's vlasov_rhs path);
+    ``c1`` = the C restatement of the numba kernels on one thread
+    (_kernels.py:320-373 driven per stage, = the numba-driven step on one
+    core).  Prints one JSON object."""
+    from oracle import cbackend as C
+    from oracle import vpfv_oracle as O
+
+    setup = make_setup(workload)
+    grids = [f.grid for f in setup.dists]
+    datas = [np.array(f.data) for f in setup.dists]
+    c0 = C.CSimulation(grids, setup.species, datas)
+    dt = 0.9 * c0.max_dt()
+    del c0
+    cells = sum(int(np.prod(g.N)) for g in grids)
+    if kind == "numpy":
+        sim = O.OracleSimulation(grids, setup.species, datas, dt=dt, rhs="numpy")
+    else:
+        sim = C.CSimulation(grids, setup.species, datas, dt=dt)
+    t0 = time.perf_counter()
+    n = 0
+    while n < 1 or time.perf_counter() - t0 < 5.0:
+        sim.advance(dt)
+        n += 1
+    el = time.perf_counter() - t0
+    print(json.dumps({"value": cells * n / el, "steps": n, "seconds": el, "cells": cells,
+                      "threads": C.num_threads() if kind == "c1" else 1}))
+
+
+def cpu_legs(workload):
+    """BASELINE.md section 3's single-core legs, each on a bounded sample
+    (per-cell costs; the numpy driver at 64^4 would take ~30 s a step)."""
+    out = []
+    for kind, what in (("numpy", "reference production driver restated in numpy (vlasov_rhs + fold-tree "
+                                 "moment + FFT Poisson), OracleSimulation rhs='numpy', 1 core"),
+                       ("c1", "numba-equivalent fused kernels (oracle/stage_ref.c, bitwise = numba) driven "
+                              "stage by stage, OMP_NUM_THREADS=1")):
+        wl = LEG_WORKLOAD.get(workload, workload)
+        if kind == "numpy" and wl in ("landau2d-64", "ep2d2v-64", "weibel-256", "twostream-1024"):
+            wl = {"landau2d-64": "landau2d-32", "ep2d2v-64": "landau2d-32", "weibel-256": "landau2d-32",
+                  "twostream-1024": "landau1d-128"}[wl]
+        env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-leg", kind, "--workload", wl],
+                               env=env, capture_output=True, text=True, timeout=300)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # noqa: BLE001 -- a leg that fails is reported, not fatal
+            out.append({"kind": kind, "error": str(e)[:200]})
+            continue
+        out.append({"kind": "port", "leg": kind, "value": d["value"], "unit": "cell-updates/s", "cores": 1,
+                    "what": what, "sample": f"{d['steps']} RK4 step(s) of {wl} ({d['cells']} cells, "
+                                            f"{d['seconds']:.1f} s)"})
+    return out
+
+
 def spawn_ranks(n):
     """``python bench.py --gpus N`` without a launcher: re-exec through
     torch.distributed.run with one rank per GPU on 127.0.0.1 (the driver's own
@@ -631,9 +698,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"],
                     help="multi-GPU x-halo: fused NVLink push from the stage kernel (peer) or NCCL send/recv")
+    ap.add_argument("--cpu-leg", choices=["numpy", "c1"], help=argparse.SUPPRESS)
     ap.add_argument("--velocity-parts", type=int, default=1,
                     help="multi-GPU: partitions of the first velocity dim (ranks = x-slabs x this)")
     args = ap.parse_args()
+    if args.cpu_leg:
+        cpu_leg_child(args.cpu_leg, args.workload)
+        return
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":

@@ -180,6 +180,19 @@ int vpfv_stage_1d2v_fused_peer(double *dest, const double *A, const double *B, c
  * exchange (Exchanger, /root/reference/pkg/src/vpfv/partition.py:679-724). */
 int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream);
 
+/* The step's divergence verdict across ranks over peer memory (the
+ * reference rolls the whole cluster back when any box is non-finite,
+ * runner.py:453-464): this rank's word (step << 1 | any nonfinite[s] != -1)
+ * is stored into *slots[r] (its slot in rank r's flag array, peer-mapped;
+ * `slots` is a device array of world such pointers) for every r; then it waits until every word of its own array `mine`
+ * (world words) carries the step's stamp and writes the OR of their bad bits
+ * to *out (device word; copy it to pinned memory to read it on the host).
+ * `stamp` is this rank's device step counter.  Timeout -> *timed_out = 1 and
+ * the rank counts as diverged.  No host synchronisation; graph-capturable. */
+int vpfv_flag_exchange(const long long *nonfinite, int nspecies, unsigned long long *const *slots,
+                       int world, const unsigned long long *mine, unsigned long long *stamp,
+                       unsigned long long *out, double timeout_s, int *timed_out, void *stream);
+
 /* Wait (one device thread, system-scope acquire) until sig[0] / sig[1] (this
  * rank's words, written by its low / high neighbour) exceed consumed[k] by
  * need_lo / need_hi, then advance consumed.  After timeout_s seconds it sets
@@ -363,6 +376,13 @@ int vpfv_box_copy(double *dst, const long long *ds, const int *dorig,
                   int ndim, const int *ext, void *stream);
 
 /* ---------------------------------------------------------------------- */
+/* The tiled stage kernels' fused-moment partials computed from f itself:
+ * part[row][c] = the first four fold-tree levels (fields.py:28-47) over the
+ * aligned 16-wide vy chunk c of every interior velocity row of the padded
+ * array f (ndim 2..4, N interior extents, N[ndim-1] % 16 == 0). */
+int vpfv_moment_chunk_partials(const double *f, double *part, int ndim, const int *N, void *stream);
+
+/* ---------------------------------------------------------------------- */
 /* Separable initial condition on the padded box (nphys padded physical
  * cells x nv1 x nv2 padded velocity cells, velocity fastest):
  * out = sum_{t < nterms} (P_t[p] * V1_t[k]) * V2_t[l], each product and the
@@ -374,6 +394,25 @@ int vpfv_init_separable(double *out, long long nphys, int nv1, int nv2,
                         const double *P0, const double *V10, const double *V20,
                         const double *P1, const double *V11, const double *V21,
                         int nterms, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* NCCL mode of the x-slab layer for non-torch hosts (csrc/comm.cu), the
+ * reference cluster's exchange (Exchanger, partition.py:679-724) and field
+ * gather (runner.py:336-392) over an NCCL communicator (opaque pointer).
+ * vpfv_comm_unique_id fills vpfv_comm_id_size() bytes on one rank; every
+ * rank passes them to vpfv_comm_init.  vpfv_halo_exchange_x: the 3 first /
+ * last interior x planes of the padded array f (extents N) to the x
+ * neighbours' high / low ghost planes, ranks forming a periodic ring.
+ * vpfv_density_allgather: count doubles per rank into n (rank order).
+ * vpfv_flag_allreduce: in-place max of one int64 (the divergence verdict).
+ * Stream-ordered, graph-capturable; VPFV_ENCCL on NCCL errors. */
+int vpfv_comm_id_size(void);
+int vpfv_comm_unique_id(unsigned char *id_out);
+int vpfv_comm_init(void **comm_out, int world, int rank, const unsigned char *id, int device);
+int vpfv_comm_destroy(void *comm);
+int vpfv_halo_exchange_x(void *comm, double *f, int ndim, const int *N, void *stream);
+int vpfv_density_allgather(void *comm, const double *n_local, double *n, long long count, void *stream);
+int vpfv_flag_allreduce(void *comm, long long *flag, void *stream);
 
 /* ---------------------------------------------------------------------- */
 int vpfv_version(void);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "vpfv_stage_2d2v_fused_peer": (_i, [_p] * 4 + [_d] * 4 + [_p] * 4 + [_d] + [_p] + [_d] + [_p] * 3 + [_d] * 4
                                    + [_i] * 4 + [_u, _p, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "vpfv_peer_signal": (_i, [_p, _p, _p]),
+    "vpfv_flag_exchange": (_i, [_p, _i, _p, _i, _p, _p, _p, _d, _p, _p]),
     "vpfv_moment_partials_push": (_i, [_p, _i, _i, _i, _d, _p, _i, _p, _i, _p, _p]),
     "vpfv_peer_wait": (_i, [_p, _p, _i, _i, _d, _p, _p]),
     "vpfv_ipc_handle_size": (_i, []),
@@ -83,6 +84,14 @@ SIGNATURES = {
     "vpfv_wrap_fill": (_i, [_p, _i, _p, _u, _p]),
     "vpfv_box_copy": (_i, [_p, _p, _p, _p, _p, _p, _i, _p, _p]),
     "vpfv_version": (_i, []),
+    "vpfv_moment_chunk_partials": (_i, [_p, _p, _i, _p, _p]),
+    "vpfv_comm_id_size": (_i, []),
+    "vpfv_comm_unique_id": (_i, [_p]),
+    "vpfv_comm_init": (_i, [_p, _i, _i, _p, _i]),
+    "vpfv_comm_destroy": (_i, [_p]),
+    "vpfv_halo_exchange_x": (_i, [_p, _p, _i, _p, _p]),
+    "vpfv_density_allgather": (_i, [_p, _p, _p, ctypes.c_longlong, _p]),
+    "vpfv_flag_allreduce": (_i, [_p, _p, _p]),
     "vpfv_init_separable": (_i, [_p, ctypes.c_longlong, _i, _i] + [_p] * 6 + [_i, _p]),
     "vpfv_check_device": (_i, [_i]),
     "vpfv_last_error": (ctypes.c_char_p, []),

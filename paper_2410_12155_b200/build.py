@@ -39,7 +39,7 @@ def build(force=False, verbose=False):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), *sources(), "-o", OUT + ".tmp"]
+    cmd = [nvcc, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), *sources(), "-ldl", "-o", OUT + ".tmp"]
     subprocess.check_call(cmd)
     os.replace(OUT + ".tmp", OUT)
     return OUT

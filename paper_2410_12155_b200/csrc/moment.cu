@@ -103,6 +103,40 @@ __global__ void moment_kernel(const double *__restrict__ f, double *__restrict__
     }
 }
 
+struct Dims4 {
+    int n[4];
+};
+
+// Fused-moment partials straight from f (the layout the tiled stage kernels'
+// epilogues write: the first four fold-tree levels over every aligned 16-wide
+// vy chunk of every interior velocity row).  Used when f was edited in place
+// on one rank of a peer-mode run, so every rank keeps the same density path.
+__global__ void chunk_partials_kernel(const double *__restrict__ f, double *__restrict__ part, int ndim, Dims4 N,
+                                      long long nrows, int nch) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= nrows * nch) return;
+    const int c = (int)(t % nch);
+    long long r = t / nch, off = 0;
+    // padded offset of interior row r (dims 0 .. ndim-2), vy handled below
+    long long st[4];
+    st[ndim - 1] = 1;
+    for (int k = ndim - 2; k >= 0; --k) st[k] = st[k + 1] * (N.n[k + 1] + 2 * NG);
+    for (int k = ndim - 2; k >= 0; --k) {
+        const long long i = r % N.n[k];
+        r /= N.n[k];
+        off += (i + NG) * st[k];
+    }
+    const double *x = f + off + NG + 16 * c;
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = x[i];
+#pragma unroll
+    for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+        for (int i = 0; i < 16; i += 2 * w) a[i] = __dadd_rn(a[i], a[i + w]);
+    part[t] = a[0];
+}
+
 }  // namespace vpfv
 
 using namespace vpfv;
@@ -182,4 +216,16 @@ extern "C" int vpfv_moment_seq(const double *f, double *n, int d, int v, const i
     moment_seq_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(f, n, nphys, ny, Pvel, s_row, nv1, nv2, off_v,
                                                                    vol, d, Py_pad);
     return check_launch("moment_seq");
+}
+
+extern "C" int vpfv_moment_chunk_partials(const double *f, double *part, int ndim, const int *N, void *stream) {
+    if (ndim < 2 || ndim > 4 || N[ndim - 1] % 16) return set_error(VPFV_EARG, "chunk_partials: vy extent must be a multiple of 16");
+    Dims4 D{};
+    long long rows = 1;
+    for (int k = 0; k < ndim; ++k) D.n[k] = N[k];
+    for (int k = 0; k < ndim - 1; ++k) rows *= N[k];
+    const int nch = N[ndim - 1] / 16;
+    const long long n = rows * nch;
+    chunk_partials_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(f, part, ndim, D, rows, nch);
+    return check_launch("moment_chunk_partials");
 }

@@ -62,9 +62,62 @@ __global__ void peer_wait_kernel(const unsigned long long *sig, unsigned long lo
     __threadfence();
 }
 
+// The per-step divergence verdict of every rank, exchanged over peer
+// memory inside the step (the reference rolls the whole cluster back when any
+// box went non-finite, runner.py:453-464).  Each rank stamps its word
+// (step << 1 | bad) into its slot of every rank's flag array, then waits
+// until all slots of its own array carry this step's stamp and ORs the bad
+// bits into *out.  The step counter lives on the device, so a captured step
+// replays correctly; ranks advance it in lockstep (one exchange per step).
+__global__ void flag_exchange_kernel(const long long *nonfinite, int nspecies, unsigned long long *const *slots,
+                                     int world, const unsigned long long *mine, unsigned long long *stamp,
+                                     unsigned long long *out, unsigned long long timeout_ns, int *timed_out) {
+    __shared__ unsigned long long word;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        bool bad = false;
+        for (int s = 0; s < nspecies; ++s) bad |= nonfinite[s] != -1LL;
+        const unsigned long long st = *stamp + 1;
+        *stamp = st;
+        word = (st << 1) | (bad ? 1ull : 0ull);
+    }
+    __syncthreads();
+    const unsigned long long w = word, st = w >> 1;
+    if (t < world) {
+        __threadfence_system();
+        atomicExch_system(slots[t], w);
+    }
+    unsigned long long any = 0;
+    if (t < world) {
+        const unsigned long long t0 = now_ns();
+        unsigned long long v;
+        while (((v = ld_acquire_sys(mine + t)) >> 1) < st) {
+            if (now_ns() - t0 > timeout_ns) {
+                atomicExch(timed_out, 1);
+                v = 1;  // a lost rank counts as diverged
+                break;
+            }
+            __nanosleep(100);
+        }
+        any = v & 1ull;
+    }
+    any = __any_sync(0xffffffffu, any != 0) ? 1ull : 0ull;
+    if (t == 0) *out = any;
+}
+
 }  // namespace vpfv
 
 using namespace vpfv;
+
+extern "C" int vpfv_flag_exchange(const long long *nonfinite, int nspecies, unsigned long long *const *slots,
+                                  int world, const unsigned long long *mine, unsigned long long *stamp,
+                                  unsigned long long *out, double timeout_s, int *timed_out, void *stream) {
+    if (world < 1 || world > 32 || nspecies < 1 || !nonfinite || !slots || !mine || !stamp || !out || !timed_out)
+        return set_error(VPFV_EARG, "flag_exchange: bad arguments");
+    flag_exchange_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(nonfinite, nspecies, slots, world, mine, stamp, out,
+                                                            (unsigned long long)(timeout_s * 1e9), timed_out);
+    return check_launch("flag_exchange");
+}
 
 extern "C" int vpfv_peer_signal(unsigned long long *sig_lo, unsigned long long *sig_hi, void *stream) {
     peer_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sig_lo, sig_hi);

@@ -579,6 +579,7 @@ class DistributedSimulation:
         self.field_conv = (self.fields.field_1d_ok() and os.environ.get("VPFV_FIELD_SPLIT", "0") != "1"
                            and os.environ.get("VPFV_FIELD_CONV", "1") != "0")
         self.peer = None
+        self._flagx = None
         self.use_graphs = use_graphs
         self._graphs = {}
         if halo == "peer":
@@ -587,6 +588,7 @@ class DistributedSimulation:
             bufs = [a for trio in zip(self.ctx.f0, self.ctx.f1, self.ctx.fout) for a in trio]
             self.peer = PeerHalo.ipc(bufs, self.comm, group, S, self.device)
             self._setup_density_push(group)
+            self._setup_flag_exchange(group)
             # the t = 0 ghosts by one ordinary exchange, then the first signal
             for trio in (self.ctx.f0, self.ctx.f1, self.ctx.fout):
                 self.comm.exchange_x(trio)
@@ -624,6 +626,39 @@ class DistributedSimulation:
     @property
     def step_count(self):
         return self.ctx.step
+
+    def _setup_flag_exchange(self, group):
+        """Peer mode: the end-of-step divergence verdict of every rank is
+        exchanged inside the step over peer memory (vpfv_flag_exchange) and
+        copied with the timeout words to pinned host memory, so a steady-state
+        ``advance`` waits for its step once and reads host memory -- no
+        host-side collective (the NCCL/gloo all-reduce of the eager path)."""
+        P, me = self.world, self.rank
+        flags = torch.zeros(P, dtype=torch.int64, device=self.device)  # slot r: rank r's word
+        allh = _ipc_all_gather([flags], group, P)
+        slots = [(flags.data_ptr() if q == me else _ipc_open(*allh[q][0])) + 8 * me for q in range(P)]
+        self._flagx = dict(flags=flags, slots=torch.tensor(slots, dtype=torch.int64, device=self.device),
+                           stamp=torch.zeros(1, dtype=torch.int64, device=self.device),
+                           out=torch.zeros(1, dtype=torch.int64, device=self.device),
+                           timed_out=torch.zeros(1, dtype=torch.int32, device=self.device),
+                           zero=torch.zeros(1, dtype=torch.int32, device=self.device),
+                           host_flag=torch.zeros(1, dtype=torch.int64, pin_memory=True),
+                           host_to=torch.zeros(3, dtype=torch.int32, pin_memory=True))
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group)
+
+    def _flag_exchange(self, stream):
+        """Enqueue the cross-rank verdict of this step's stage 4 and its
+        copies to pinned host memory (part of the captured step)."""
+        fx = self._flagx
+        _lib.call("vpfv_flag_exchange", self.nonfinite[3].data_ptr(), len(self.species), fx["slots"].data_ptr(),
+                  self.world, fx["flags"].data_ptr(), fx["stamp"].data_ptr(), fx["out"].data_ptr(),
+                  float(self.peer.timeout_s), fx["timed_out"].data_ptr(), stream)
+        fx["host_flag"].copy_(fx["out"], non_blocking=True)
+        fx["host_to"][0:1].copy_(self.peer.timed_out, non_blocking=True)
+        dto = self._dpush["timed_out"] if self._dpush is not None else fx["zero"]
+        fx["host_to"][1:2].copy_(dto, non_blocking=True)
+        fx["host_to"][2:3].copy_(fx["timed_out"], non_blocking=True)
 
     def _setup_density_push(self, group):
         """Peer mode: the slab densities go straight into every rank's
@@ -779,6 +814,8 @@ class DistributedSimulation:
         for slot, (dn, an, bn, sn, ca, cb, cd, div) in enumerate(RK4_STAGES):
             self._stage(bufs[dn], bufs[an], bufs[bn], bufs[sn], ca, cb, cd, 0.0, slot,
                         dt_dev=self.dt_dev, cL_div=div)
+        if self._flagx is not None:
+            self._flag_exchange(stream_handle(self.device))
         self._launches = _lib.launch_counter[0] - start
 
     def launch_step(self, dt):
@@ -790,6 +827,16 @@ class DistributedSimulation:
         self.dt_dev.fill_(float(dt))
         sig = lambda arrays: tuple((a.data_ptr(), a._version) for a in arrays)  # noqa: E731
         self._cached = self.fuse_moment and self._moment_of == sig(self.ctx.f0)
+        if self.peer is not None and self._dpush is not None and self.fuse_moment and not self._cached \
+                and self._moment_of is not None:
+            # f0 edited in place on this rank: rebuild its stage-4 partials from f0 so this rank keeps
+            # the pushed-density path every other rank is on (the density exchange is collective)
+            stream = stream_handle(self.device)
+            for a, p, lg in zip(self.ctx.f0, self.partials_next, self.lgrids):
+                _lib.call("vpfv_moment_chunk_partials", a.data_ptr(), p.data_ptr(), lg.ndim, _lib.int_array(lg.N),
+                          stream)
+            self._moment_of = sig(self.ctx.f0)
+            self._cached = True
         if self.use_graphs and self.peer is not None and self._dpush is not None and self._cached \
                 and not self._timing:
             d = self._dpush
@@ -845,15 +892,26 @@ class DistributedSimulation:
             for slot in range(4):
                 for a, b in self._events[slot]:
                     self._stage_ms[slot] += a.elapsed_time(b)
-        if self.peer is not None:
+        if self._flagx is not None:  # the verdict and the timeout words arrived with the step (pinned memory)
+            to = self._flagx["host_to"].tolist()
+            if to[0]:
+                raise RuntimeError("peer halo: a neighbour's signal did not arrive (timed out)")
+            if to[1]:
+                raise RuntimeError("peer densities: another rank's push did not arrive (timed out)")
+            if to[2]:
+                raise RuntimeError("divergence verdict: another rank's word did not arrive (timed out)")
+            any_bad = bool(self._flagx["host_flag"].item())
+        elif self.peer is not None:
             self.peer.check()
             if self._dpush is not None and int(self._dpush["timed_out"].item()):
                 raise RuntimeError("peer densities: another rank's push did not arrive (timed out)")
         self.ctx.t = self.ctx.t + dt
         self.ctx.rotate()
-        flags = self.nonfinite[3].cpu().numpy().astype(np.uint64)
-        bad_local = [s for s in range(len(self.species)) if flags[s] != np.uint64(_lib.VPFV_FINITE)]
-        if self.comm.any_flag(bool(bad_local), self.device):
+        bad_local = []
+        if self._flagx is None or any_bad:
+            flags = self.nonfinite[3].cpu().numpy().astype(np.uint64)
+            bad_local = [s for s in range(len(self.species)) if flags[s] != np.uint64(_lib.VPFV_FINITE)]
+        if (any_bad if self._flagx is not None else self.comm.any_flag(bool(bad_local), self.device)):
             self.ctx.f0, self.ctx.fout = self.ctx.fout, self.ctx.f0
             self.ctx.t -= dt
             self.ctx.step -= 1
