@@ -44,6 +44,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tma.cuh"
 #include "field.cuh"
@@ -347,6 +349,11 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
 #pragma unroll
         for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
+#ifdef VPFV_UNROLL_PLANES  // experiment: unrolled plane loop (window slide by renaming)
+#define VPFV_PRAGMA_(x) _Pragma(#x)
+#define VPFV_UNROLL_(n) VPFV_PRAGMA_(unroll n)
+    VPFV_UNROLL_(VPFV_UNROLL_PLANES)
+#endif
     for (int n = 0; n < nplanes; ++n) {
         const int p = p_first + n, q = p - 3;
         const bool inner = p >= i0 && p < i1;
@@ -398,7 +405,9 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         // ---- own rows (a = 0, 1): vy lines, vx lines, D and G -------------
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
+#ifndef VPFV_ROW_NOFENCE
             SCHED_FENCE();  // one row at a time
+#endif
             const double *ca = c + a * KL;
             double v[BB][7];
 #pragma unroll
@@ -443,6 +452,52 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 const double gp = ca[BB * TW - 1] - ca[BB * TW + 1];  // G at vx offset BB
                 const double avx = evx[a] + cBvy;                    // a_vx is independent of vx
                 const double avx_s = avx * mhvx;
+#ifdef VPFV_MERGE_STENCILS  // experiment (measured no gain): the row's vx and vy lines in one block
+                // the row's vx and vy lines in one sign-specialised block: 2 x BB
+                // independent 6-deep chains to interleave (in two separate
+                // branch blocks they were BB each), folded in the same order
+                {
+                    double wx[BB], wy[BB];
+                    auto lines = [&](auto vxp_tag, auto vys_tag) {
+                        constexpr bool VXP = decltype(vxp_tag)::value;
+                        constexpr int VYS = decltype(vys_tag)::value;
+#pragma unroll
+                        for (int b = 0; b < BB; ++b) {
+                            wx[b] = VXP ? wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5])
+                                        : wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]);
+                            if (VYS > 0)
+                                wy[b] = wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]);
+                            else if (VYS < 0)
+                                wy[b] = wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
+                            else
+                                wy[b] = evy[a] + bvx[b] > 0.0 ? wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
+                                                              : wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
+                        }
+                    };
+                    using T1 = std::true_type;
+                    using F1 = std::false_type;
+                    using YP = std::integral_constant<int, 1>;
+                    using YN = std::integral_constant<int, -1>;
+                    using YM = std::integral_constant<int, 0>;
+                    // a_vy = evy - cB vx: one sign for the row when the BB signs agree
+                    // (always when cB == 0; fl(e + x) is monotone in x)
+                    const int vys = evy[a] + bvx_min > 0.0 ? 1 : (evy[a] + bvx_max <= 0.0 ? -1 : 0);
+                    if (avx > 0.0) {
+                        if (vys > 0) lines(T1{}, YP{});
+                        else if (vys < 0) lines(T1{}, YN{});
+                        else lines(T1{}, YM{});
+                    } else {
+                        if (vys > 0) lines(F1{}, YP{});
+                        else if (vys < 0) lines(F1{}, YN{});
+                        else lines(F1{}, YM{});
+                    }
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) {
+                        acc[a * BB + b][3] = fma(avx_s, wx[b], acc[a * BB + b][3]);
+                        acc[a * BB + b][3] = fma((evy[a] + bvx[b]) * mhvy, wy[b], acc[a * BB + b][3]);
+                    }
+                }
+#else
 #ifdef VPFV_EXP_FORCE_AV
                 if (true) {
 #else
@@ -483,6 +538,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                         acc[a * BB + b][3] = fma(avy * mhvy, w, acc[a * BB + b][3]);
                     }
                 }
+#endif
                 // diag(vx,vy) = G(vx+1) - G(vx-1)
                 double gr[BB + 2];
                 gr[0] = gm;
@@ -495,11 +551,15 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         }
 
         // ---- y arms: y stencil, the arm rows' y corners, folded src operand --
-        if (inner) {
+        // (ypos is per thread: one branch around the loop, not one per b)
+        auto yarms = [&](auto ypos_tag) {
+            constexpr bool YP = decltype(ypos_tag)::value;
             const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
+#ifndef VPFV_YARM_NOFENCE
                 SCHED_FENCE();
+#endif
                 const double qm = rm[b * TW], qp = rp[b * TW];
                 const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
                 const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
@@ -507,7 +567,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 const double Dkp = rp[(b - 1) * TW] - rp[(b + 1) * TW];
                 const double z0 = s0[b], z1 = s0[BB + b];
                 double w0, w1;
-                if (ypos) {
+                if (YP) {
                     const double ym3 = c[-3 * KL + b * TW], ym2 = c[-2 * KL + b * TW], y3 = c[3 * KL + b * TW];
                     w0 = wpos(ym3, ym2, qm, z0, z1, qp);
                     w1 = wpos(ym2, qm, z0, z1, qp, y3);
@@ -522,6 +582,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 acc[b][3] = fma(kfold, z0, t0);
                 acc[BB + b][3] = fma(kfold, z1, t1);
             }
+        };
+        if (inner) {
+            if (ypos)
+                yarms(std::true_type{});
+            else
+                yarms(std::false_type{});
         }
 
         // ---- x stencil scatter, extract cell q, slide the window -------------

@@ -389,6 +389,59 @@ def test_tiled_stage_wrap_reads_interior_and_fused_moment(N):
     assert np.array_equal(n.cpu().numpy(), O.zeroth_moment(got, g))
 
 
+@pytest.mark.parametrize("vx", [(-3.5, 4.5), (-4.0, 4.0), (-4.5, 3.5), (-2.0, 6.0), (0.5, 8.5), (-8.5, -0.5)])
+@pytest.mark.parametrize("coef", [(1.0, 0.0, 0.0, 0.02), (-0.125, 0.375, 0.75, 0.00375)])
+def test_tiled_stage_vx_sign_layouts(vx, coef):
+    """The tiled kernel runs one plane loop per a_x sign: column blocks whose
+    vx cells share a sign take one pass, blocks straddling vx = 0 (inside a
+    tile, inside a thread's 4 cells, or with a centre exactly at 0, which
+    takes the a <= 0 branch) take both passes, each finalising its own sign's
+    cells.  All layouts match the oracle, partials fold to the reference tree,
+    RK operands (dest aliased) stay per cell."""
+    N = (8, 8, 32, 32)
+    g = O.Grid(2, 2, N, (0.0, 0.0, vx[0], -5.0), (2 * np.pi, 4 * np.pi, vx[1], 5.0), (True, True, False, False))
+    rng = np.random.default_rng(11)
+    src = 1.0 + 0.3 * rng.random(g.padded_shape)
+    O.fill_ghosts(src, g, O.capture_frozen(src, g))
+    cx, cy = g.centers(0), g.centers(1)
+    E = {"Ex": 0.4 * np.outer(np.sin(cx), np.cos(cy)) + 0.05, "Ey": 0.3 * np.outer(np.cos(cx), np.sin(2 * cy))}
+    sp = O.Species("e", -1.0, 1.0, 1.1, 0.3, 1.0, (0.02, -0.01))
+    A, dest0 = rng.random(g.padded_shape), rng.random(g.padded_shape)
+    ca, cb, cd, cL = coef
+    want = dest0.copy()
+    O.fused_stage(want, A, src, src, ca, cb, cd, cL, g, sp, E, check=False)
+    pg = pgrid(g)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tab = K.StageTables(pg, sp, torch.device("cuda"))
+    stream = K.stream_handle()
+    tab.update({k: dev(v) for k, v in E.items()}, stream, packed=True)
+    flags = K.wrap_flags(pg)
+    assert tab.fused_moment_ok(flags)
+    d_src, d_A, d_dest = dev(src), dev(A), dev(dest0)
+    part = torch.empty(tab.partials_shape(), dtype=torch.float64, device="cuda")
+    nf = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    tab.launch(d_dest, d_A, d_src, d_src, ca, cb, cd, cL, flags, stream, nonfinite=nf, partials=part, packed=True)
+    got = d_dest.cpu().numpy()
+    inner = g.inner()
+    assert int(nf.item()) == -1
+    assert np.max(np.abs(got[inner] - want[inner])) <= 2e-14 * np.max(np.abs(want[inner]))
+    assert np.array_equal(got[~_interior_mask(g)], dest0[~_interior_mask(g)])
+    n = torch.empty((N[0], N[1]), dtype=torch.float64, device="cuda")
+    _lib.call("vpfv_moment_partials", part.data_ptr(), n.data_ptr(), N[0] * N[1], N[2], part.shape[-1],
+              O.velocity_volume(g), stream)
+    assert np.array_equal(n.cpu().numpy(), O.zeroth_moment(got, g))
+    # a non-finite source cell is reported at its own index whichever pass finalises it
+    for ix in (5, 27):
+        bad = src.copy()
+        bad[3 + 2, 3 + 3, 3 + ix, 3 + 9] = np.inf
+        nf.fill_(-1)
+        d_dest.copy_(dev(dest0))
+        d_bad = dev(bad)
+        tab.launch(d_dest, d_A, d_bad, d_bad, ca, cb, cd, cL, flags, stream, nonfinite=nf, partials=part,
+                   packed=True)
+        assert int(nf.item()) >= 0
+
+
 def test_fused_moment_rejected_off_the_tiled_path():
     g, sp, src, E, rng = _tiled_case((8, 8, 8, 32), 3)
     pg = pgrid(g)
