@@ -86,7 +86,7 @@ def make_setup(name, world=1, device=None):
     raise ValueError(name)
 
 
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r1_end_rb_summary.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r2_rb_summary.json")
 
 
 def load_traffic():

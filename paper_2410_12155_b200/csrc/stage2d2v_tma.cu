@@ -377,6 +377,13 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
 #endif
             }
+#ifndef VPFV_OP_PF
+#define VPFV_OP_PF 0  // measured: +1 % on stage 4, -4 % on stage 1 (register schedule)
+#endif
+            // the operand tiles of cell plane q + VPFV_OP_PF into L2: the single
+            // operand buffer is loaded only one plane ahead of its use
+            if (VPFV_OP_PF > 0 && op_lane && o >= 0 && o < nops && q + VPFV_OP_PF >= i0 && q + VPFV_OP_PF < i1)
+                tma::prefetch4d(&M->op[o], l0 + 2, k0 + NG, j0 + NG, q + VPFV_OP_PF + NG);
         }
         // stage and parity from the plane number (loop-carried counters get spilled)
         const int nq3 = n / NS, stage_s = n - nq3 * NS;

@@ -87,6 +87,15 @@ __device__ __forceinline__ void load4d_s(unsigned dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// prefetch a 4D box into L2 (no shared memory, no barrier): a later load of
+// the same box then hits L2
+__device__ __forceinline__ void prefetch4d(const CUtensorMap *map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 // with an L2 cache policy (createpolicy), e.g. evict_first for read-once operands
 __device__ __forceinline__ void load4d_s_hint(unsigned dst, const CUtensorMap *map, unsigned bar, int c0, int c1,
                                               int c2, int c3, uint64_t policy) {

@@ -20,35 +20,36 @@ def main():
     rep, wl, cells = sys.argv[1], sys.argv[2], float(sys.argv[3])
     out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(__file__), "..", "profiles",
                                                               "r2_stage_profile.json")
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
-    per, cur, hdr = [], None, None
-    for r in rows:
-        if r and r[0] == "Kernel Name":
-            cur = {"DFMA": 0, "DMUL": 0, "DADD": 0, "total": 0}
-            per.append(cur)
-            continue
-        if r and r[0] == "Address":
-            hdr = r
-            continue
-        if cur is None or hdr is None or len(r) != len(hdr):
-            continue
-        d = dict(zip(hdr, r))
-        src = d["Source"].strip().split()
-        if not src:
-            continue
-        op = src[1] if src[0].startswith("@") and len(src) > 1 else src[0]
-        n = int(d.get("Predicated-On Thread Instructions Executed") or 0)
-        cur["total"] += int(d.get("Thread Instructions Executed") or 0)
-        for k in ("DFMA", "DMUL", "DADD"):
-            if op.split(".")[0] == k:
-                cur[k] += n
-    # the source page lists each launch once with sass (some ncu versions repeat sections): dedupe
     uniq = []
-    for p in per:
-        if p["total"] and (not uniq or p != uniq[-1]):
-            uniq.append(p)
+    for k in range(64):  # one launch at a time: the page may repeat a launch's section
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                              "--launch-skip", str(k), "--launch-count", "1"],
+                             capture_output=True, text=True).stdout
+        cur, hdr = None, None
+        for r in csv.reader(io.StringIO(txt)):
+            if r and r[0] == "Kernel Name":
+                if cur is not None:
+                    break  # the first section is this launch
+                cur = {"DFMA": 0, "DMUL": 0, "DADD": 0, "total": 0}
+                continue
+            if r and r[0] == "Address":
+                hdr = r
+                continue
+            if cur is None or hdr is None or len(r) != len(hdr):
+                continue
+            d = dict(zip(hdr, r))
+            src = d["Source"].strip().split()
+            if not src:
+                continue
+            op = src[1] if src[0].startswith("@") and len(src) > 1 else src[0]
+            n = int(d.get("Predicated-On Thread Instructions Executed") or 0)
+            cur["total"] += int(d.get("Thread Instructions Executed") or 0)
+            for key in ("DFMA", "DMUL", "DADD"):
+                if op.split(".")[0] == key:
+                    cur[key] += n
+        if not cur or not cur["total"]:
+            break
+        uniq.append(cur)
     ops = [(p["DFMA"] + p["DMUL"] + p["DADD"]) / cells for p in uniq]
     try:
         with open(out) as f:

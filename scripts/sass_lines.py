@@ -1,7 +1,10 @@
 """Join an ncu SASS source page (per-instruction counts) with nvdisasm -g line
 info, and print instructions/stalls per CUDA source line.
 
-    python scripts/sass_lines.py SASS_CSV NVDISASM_TXT KERNEL_MANGLED CELLS
+    python scripts/sass_lines.py SASS_CSV NVDISASM_TXT KERNEL_MANGLED CELLS [MAIN_FILE]
+
+Lines of MAIN_FILE (default stage2d2v_tma.cu) print as is; lines of every
+other file (inlined helpers) print offset by 100000.
 """
 import collections
 import csv
@@ -14,7 +17,7 @@ def main():
     rows = list(csv.reader(open(sass_csv)))
     h = rows[1]
     idx = {k: i for i, k in enumerate(h)}
-    recs = [r for r in rows[2:] if len(r) >= len(h)]
+    recs = [r for r in rows[2:] if len(r) >= len(h) and r[0].startswith("0x")]
     base = int(recs[0][idx["Address"]], 16)
     counts = {}
     for r in recs:
@@ -32,7 +35,10 @@ def main():
             continue
         m = re.search(r'line (\d+)', ln)
         if "//##" in ln and m:
-            line = int(m.group(1))
+            f = re.search(r'File "([^"]+)"', ln)
+            # lines of other files (tma.cuh, common.cuh helpers) are keyed apart
+            line = int(m.group(1)) + (0 if not f or f.group(1).endswith(sys.argv[5] if len(sys.argv) > 5
+                                                                        else "stage2d2v_tma.cu") else 100000)
             continue
         m = re.match(r'\s*/\*([0-9a-f]{4,})\*/\s', ln)
         if m and line is not None:
