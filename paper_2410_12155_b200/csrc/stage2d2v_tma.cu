@@ -141,6 +141,32 @@ __device__ __forceinline__ double wneg(double m2, double m1, double z, double p1
 // x-stencil offset -3 (a_x > 0) or -2 (a_x <= 0) -- so no slot is zeroed.
 template <int SIGN>  // +1: a_x > 0, -1: a_x <= 0
 __device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &fin) {
+#ifndef VPFV_SLIDE_DESC
+    // The slide as in-order renaming: slot j's FMA reads slot j+1, so each
+    // result can take the register its slot had, and the finished cell comes
+    // out of an instruction (w0 + 0: exact, and unlike 0*t + w0 it cannot pick
+    // up a non-finite value from this plane) instead of pinning w[0]'s
+    // register past the slide.  Measured 235 -> 95 register moves in the
+    // kernel, -5 % per RK4 step with the hoisted y-arm branch (bitwise).
+    if (SIGN > 0) {
+        fin = __dadd_rn(w[0], 0.0);
+        w[0] = fma(-3.0, ti, w[1]);
+        w[1] = fma(30.0, ti, w[2]);
+        w[2] = fma(20.0, ti, w[3]);
+        w[3] = fma(-60.0, ti, w[4]);
+        w[4] = fma(15.0, ti, w[5]);
+        w[5] = -2.0 * ti;  // cell p+3 enters
+    } else {
+        fin = fma(2.0, ti, w[0]);
+        w[0] = fma(-15.0, ti, w[1]);
+        w[1] = fma(60.0, ti, w[2]);
+        w[2] = fma(-20.0, ti, w[3]);
+        w[3] = fma(-30.0, ti, w[4]);
+        w[4] = 3.0 * ti;  // cell p+2 enters (its slot was freed last plane)
+        w[5] = 0.0;
+    }
+}
+#else  // round 1 order (VPFV_SLIDE_DESC, A/B only)
     if (SIGN > 0) {
         w[5] = fma(15.0, ti, w[5]);
         w[4] = fma(-60.0, ti, w[4]);
@@ -164,6 +190,7 @@ __device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &
         w[5] = 0.0;
     }
 }
+#endif
 
 // The sign of a_x is per vx; a thread's BB vx cells share it unless the zero
 // crossing falls inside them (one uniform branch, no predication).

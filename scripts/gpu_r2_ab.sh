@@ -1,7 +1,7 @@
 # Round-2 kernel iteration: targeted 2D-2V parity tests, then an interleaved
 # stage-time A/B of exp/libvpfv_*.so builds against the in-tree library.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu.py -x -q -k "tiled or landau2d or graph_replay or medium_step or vx_sign" > gpurun_out/ab_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests.log
+timeout 900 python -m pytest tests/test_gpu.py -x -q -k "tiled or landau2d or graph_replay or medium_step or vx_sign or nonfinite or aliasing or ep2d2v or peer or range" > gpurun_out/ab_tests.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests.log
 libs="main"
 for f in exp/libvpfv_*.so; do libs="$libs $f"; done
 : > gpurun_out/ab_stage.txt
