@@ -90,26 +90,23 @@ __device__ __forceinline__ double w12neg(double m2, double m1, double z, double 
 // extraction of cell p-3, slide (see scatter_cell in stage2d2v_tma.cu)
 template <int SIGN>
 __device__ __forceinline__ void scatter12(double (&w)[6], double ti, double &fin) {
+    // in-order renaming (slot j's FMA reads slot j+1) and an exact add for
+    // the a_x > 0 finished cell, as in the 2D-2V kernel's scatter_cell
     if (SIGN > 0) {
-        w[5] = fma(15.0, ti, w[5]);
-        w[4] = fma(-60.0, ti, w[4]);
-        w[3] = fma(20.0, ti, w[3]);
-        w[2] = fma(30.0, ti, w[2]);
-        w[1] = fma(-3.0, ti, w[1]);
-        fin = w[0];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) w[j] = w[j + 1];
+        fin = __dadd_rn(w[0], 0.0);
+        w[0] = fma(-3.0, ti, w[1]);
+        w[1] = fma(30.0, ti, w[2]);
+        w[2] = fma(20.0, ti, w[3]);
+        w[3] = fma(-60.0, ti, w[4]);
+        w[4] = fma(15.0, ti, w[5]);
         w[5] = -2.0 * ti;
     } else {
-        const double c2 = 3.0 * ti;
-        w[4] = fma(-30.0, ti, w[4]);
-        w[3] = fma(-20.0, ti, w[3]);
-        w[2] = fma(60.0, ti, w[2]);
-        w[1] = fma(-15.0, ti, w[1]);
         fin = fma(2.0, ti, w[0]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = w[j + 1];
-        w[4] = c2;
+        w[0] = fma(-15.0, ti, w[1]);
+        w[1] = fma(60.0, ti, w[2]);
+        w[2] = fma(-20.0, ti, w[3]);
+        w[3] = fma(-30.0, ti, w[4]);
+        w[4] = 3.0 * ti;
         w[5] = 0.0;
     }
 }
