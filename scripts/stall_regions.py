@@ -12,14 +12,14 @@ import sys
 
 REGIONS = [  # (name, first line, last line) in csrc/stage2d2v_tma.cu
     ("upwind 6-point chains wpos/wneg (inlined into every stencil)", 125, 130),
-    ("x scatter + window slide", 136, 195),
-    ("TMA issue (producer lanes)", 196, 230),
-    ("loop head, producer branch, stage wait", 357, 404),
-    ("own rows: loads, D/G, x-coupled, vx/vy lines, diag", 405, 552),
-    ("y arms: y lines, arm corners, fold", 553, 592),
-    ("finalise: RK combination, stores", 593, 632),
-    ("finalise: moment partials + non-finite", 633, 694),
-    ("plane advance + barrier", 695, 702),
+    ("x scatter + window slide", 138, 222),
+    ("TMA issue (producer lanes)", 223, 257),
+    ("loop head, producer branch, stage wait", 384, 438),
+    ("own rows: loads, D/G, x-coupled, vx/vy lines, diag", 439, 586),
+    ("y arms: y lines, arm corners, fold", 587, 626),
+    ("finalise: RK combination, stores", 627, 666),
+    ("finalise: moment partials + non-finite", 667, 728),
+    ("plane advance + barrier", 729, 736),
     ("inlined helpers (tma.cuh mbarrier waits, common.cuh)", 100000, 200000),
 ]
 
