@@ -252,8 +252,12 @@ __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Ma
 
 // PEER: the x-halo push of vpfv_stage_2d2v_fused_peer, compiled only into the
 // instantiation that needs it (the ordinary launches carry no extra code)
-template <class GEO, bool PEER>
-__global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
+// WS: warp-specialised variant -- a fourth warpgroup (warps 8-11, 24
+// registers; one lane works) issues every TMA load, driven by full/empty
+// mbarriers, and the compute warps (240 registers) never meet at a CTA
+// barrier inside the plane loop (VPFV_RB_WS=1).
+template <class GEO, bool PEER, bool WS = false>
+__global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
     RB_GEOMETRY(GEO);
@@ -307,6 +311,8 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
 
     if (tid == 0) {
         for (int s = 0; s <= NS; ++s) tma::mbar_init(&bars[s], 1);
+        if (WS)  // empty barriers: every compute thread arrives once per plane / per operand tile
+            for (int s = NS + 1; s <= 2 * NS + 1; ++s) tma::mbar_init(&bars[s], GEO::THREADS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -314,7 +320,45 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int p_first = i0 - 3, p_last = i1 + 2;
     const int nplanes = p_last - p_first + 1;
     const Maps *M = &maps;
-    if (tid == 0) {
+    const unsigned emptybar = sbase + BAR_OFF + (NS + 1) * 8, opempty = sbase + BAR_OFF + (2 * NS + 1) * 8;
+    if (WS) {
+        if (warp >= GEO::THREADS / 32) {  // the producer warpgroup
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if (tid == GEO::THREADS) {
+                // halo planes as soon as their ring slot is free, operand tiles as soon as
+                // the single operand buffer is (both polled, neither blocks the other)
+                const int nfin = P.nops ? i1 - i0 : 0;
+                int nh = 0, no = 0;
+                while (nh < nplanes || no < nfin) {
+                    if (nh < nplanes && (nh < NS || tma::mbar_test_s(emptybar + (nh % NS) * 8, (nh / NS - 1) & 1))) {
+                        for (int w = 0; w < 4; ++w)
+                            issue_plane_part<GEO>(w, sbase, M, nh, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core,
+                                                  cy_hi);
+                        ++nh;
+                    }
+                    if (no < nfin && (no == 0 || tma::mbar_test_s(opempty, (no - 1) & 1))) {
+                        const int q = i0 + no;
+                        tma::mbar_expect_tx_s(opbar, P.nops * OP_BYTES);
+                        for (int o = 0; o < P.nops; ++o)
+                            tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
+#ifndef VPFV_WS_OP_PF
+#define VPFV_WS_OP_PF 0  // measured: the prefetch code makes ptxas spill (12 B), +7 %
+#endif
+                        // the single operand buffer is refilled one plane ahead of its use:
+                        // later operand tiles go to L2 now, so the refill hits L2
+                        if (VPFV_WS_OP_PF > 0 && no + VPFV_WS_OP_PF < nfin)
+                            for (int o = 0; o < P.nops; ++o)
+                                tma::prefetch4d(&M->op[o], l0 + 2, k0 + NG, j0 + NG, q + VPFV_WS_OP_PF + NG);
+                        ++no;
+                    }
+                }
+            }
+            __syncwarp();
+            if (PEER) peer_done_signal(P);
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+    } else if (tid == 0) {
         for (int n = 0; n < NS - 1 && n < nplanes; ++n)
             for (int w = 0; w < 4; ++w)
                 issue_plane_part<GEO>(w, sbase, M, n, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
@@ -390,9 +434,9 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         // (plane parts from lane 0 of warps 0-3; operand o from lane 0 of warp
         // 4+o, or from lane 16 of warp o when the CTA has only 4 warps)
         constexpr int NWARPS = GEO::THREADS / 32;
-        if (lane == 0 && warp < 4 && n + NS - 1 < nplanes)
+        if (!WS && lane == 0 && warp < 4 && n + NS - 1 < nplanes)
             issue_plane_part<GEO>(warp, sbase, M, n + NS - 1, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
-        {
+        if (!WS) {
             const int o = NWARPS >= 4 + OPS_MAX ? warp - 4 : warp;
             const bool op_lane = NWARPS >= 4 + OPS_MAX ? lane == 0 : lane == 16;
             if (op_lane && o >= 0 && o < nops && fin_q) {
@@ -646,6 +690,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                     out[i] = fma(cL, fin[i], fma(oc1, op[OPE + oi], oc0 * op[oi]));
                 }
             }
+            if (WS && nops) tma::mbar_arrive_s(opempty);  // this thread is done with the operand tiles
             double *dq = P.dest + gq;
             if (fold_fb) {  // cL == 0: the src operand could not be folded
 #pragma unroll
@@ -728,7 +773,10 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         }
         gq += P1;
         ppart += pstep;
-        __syncthreads();  // the stage and the operand tiles are free for the next refill
+        if (WS)
+            tma::mbar_arrive_s(sbase + BAR_OFF + (NS + 1 + stage_s) * 8);  // this thread is done with the stage
+        else
+            __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
     if (PEER) peer_done_signal(P);
 }
@@ -936,13 +984,39 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     if (!attr) {
         cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
         cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        if constexpr (GEO::MINB == 1) {
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GEO::SMEM);
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GEO::SMEM);
+        }
         attr = true;
     }
+    static int ws = -1;
+    if (ws < 0) {
+        const char *e = getenv("VPFV_RB_WS");
+#ifndef VPFV_RB_WS_DEFAULT
+#define VPFV_RB_WS_DEFAULT 1
+#endif
+        ws = e ? atoi(e) != 0 : VPFV_RB_WS_DEFAULT;
+    }
     const int nblocks = (P.Ny / BJ) * (P.Nvx / GEO::BK) * (P.Nvy / BL) * P.nseg;
-    if (P.done)
+    bool launched = false;
+    if constexpr (GEO::MINB == 1) {  // one CTA per SM: the register pool setmaxnreg redistributes
+        if (ws) {
+            if (P.done)
+                stage2d2v_rb_kernel<GEO, true, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+            else
+                stage2d2v_rb_kernel<GEO, false, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+            launched = true;
+        }
+    }
+    if (launched) {
+    } else if (P.done) {
         stage2d2v_rb_kernel<GEO, true><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
-    else
+    } else {
         stage2d2v_rb_kernel<GEO, false><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    }
     return check_launch("stage_2d2v_tma");
 }
 
