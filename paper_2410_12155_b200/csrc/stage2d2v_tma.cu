@@ -87,9 +87,9 @@ constexpr int BJ = 8, BL = 16, OPS_MAX = 2;
 enum { T_EVX = 0, T_EVY = 1, T_C3 = 2, T_C4 = 3, T_C1 = 4, T_C5 = 5 };
 // Tile geometry: (BJ, BK, BL) column block, NS-deep stage ring, MINB CTAs
 // per SM; one thread per 2 (y) x BB (vx) cells at one vy lane.
-template <int BK_, int NS_, int MINB_>
+template <int BK_, int NS_, int MINB_, int NOPB_ = 1>
 struct Geo {
-    static constexpr int BK = BK_, NS = NS_, MINB = MINB_, BB = 4;
+    static constexpr int BK = BK_, NS = NS_, MINB = MINB_, BB = 4, NOPB = NOPB_;  // NOPB: operand buffers
     static constexpr int THREADS = (BJ / 2) * (BK / BB) * BL;
     static constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile (vy box starts 16 B aligned)
     static constexpr int KL = TK * TW, HALO = TJ * KL;
@@ -98,22 +98,28 @@ struct Geo {
     static constexpr int OPW = BL + 2;      // RK operand row (16 B aligned start)
     static constexpr int OPE = BJ * BK * OPW;
     static constexpr int HALO_BYTES = HALO * 8, CORE_BYTES = BJ * KL * 8, TAB_BYTES = TAB * 8, OP_BYTES = OPE * 8;
-    static constexpr int BAR_OFF = NS * STAGE * 8 + OPS_MAX * OPE * 8;  // NS stage barriers, then the operand barrier
+    // barriers: NS stage-full, NOPB operand-full, then (warp-specialised) NS
+    // stage-empty and NOPB operand-empty
+    static constexpr int BAR_OFF = NS * STAGE * 8 + NOPB * OPS_MAX * OPE * 8;
     static constexpr int SMEM = BAR_OFF + 64;
+    static_assert(2 * (NS + NOPB) <= 8, "barrier block");
     static_assert((STAGE * 8) % 128 == 0 && (HALO * 8) % 128 == 0 && (OPE * 8) % 128 == 0,
                   "TMA destinations must stay 128 B aligned");
     static_assert(SMEM * MINB <= 228 * 1024 - MINB * 1024, "shared memory budget");
 };
 using GeoWide = Geo<16, 3, 1>;   // (8, 16, 16) tiles, 1 CTA of 8 warps per SM
 using GeoPair = Geo<8, 2, 2>;    // (8, 8, 16) tiles, 2 CTAs of 4 warps per SM (desynchronised)
+// stages with RK operands, warp-specialised: a 2-deep halo ring and double-
+// buffered operand tiles, so compute warps are not coupled through one buffer
+using GeoWideOp = Geo<16, 2, 1, 2>;
 }  // namespace rb
 
 #define RB_GEOMETRY(G)                                                                                          \
     constexpr int BK = G::BK, NS = G::NS, BB = G::BB, TK = G::TK, TW = G::TW, KL = G::KL, HALO = G::HALO,     \
                   STAGE = G::STAGE, OPW = G::OPW, OPE = G::OPE, HALO_BYTES = G::HALO_BYTES,                    \
                   CORE_BYTES = G::CORE_BYTES, TAB_BYTES = G::TAB_BYTES, OP_BYTES = G::OP_BYTES,                \
-                  BAR_OFF = G::BAR_OFF;                                                                         \
-    (void)BK, (void)NS, (void)BB, (void)TK, (void)TW, (void)KL, (void)HALO, (void)STAGE, (void)OPW, (void)OPE, \
+                  BAR_OFF = G::BAR_OFF, NOPB = G::NOPB;                                                          \
+    (void)NOPB, (void)BK, (void)NS, (void)BB, (void)TK, (void)TW, (void)KL, (void)HALO, (void)STAGE, (void)OPW, (void)OPE, \
         (void)HALO_BYTES, (void)CORE_BYTES, (void)TAB_BYTES, (void)OP_BYTES, (void)BAR_OFF
 
 struct Maps {
@@ -261,6 +267,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
     RB_GEOMETRY(GEO);
+    static_assert(WS || NOPB == 1, "double-buffered operands need the producer warpgroup");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     const double *opbuf = stages + NS * STAGE;
@@ -310,9 +317,9 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     const int cy_lo = yl + NG, cy_core = j0 + NG, cy_hi = yh + NG;
 
     if (tid == 0) {
-        for (int s = 0; s <= NS; ++s) tma::mbar_init(&bars[s], 1);
+        for (int s = 0; s < NS + NOPB; ++s) tma::mbar_init(&bars[s], 1);
         if (WS)  // empty barriers: every compute thread arrives once per plane / per operand tile
-            for (int s = NS + 1; s <= 2 * NS + 1; ++s) tma::mbar_init(&bars[s], GEO::THREADS);
+            for (int s = NS + NOPB; s < 2 * (NS + NOPB); ++s) tma::mbar_init(&bars[s], GEO::THREADS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -320,7 +327,9 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     const int p_first = i0 - 3, p_last = i1 + 2;
     const int nplanes = p_last - p_first + 1;
     const Maps *M = &maps;
-    const unsigned emptybar = sbase + BAR_OFF + (NS + 1) * 8, opempty = sbase + BAR_OFF + (2 * NS + 1) * 8;
+    // operand buffer k: full barrier opbar + 8k, empty barrier opempty + 8k, tiles at opdst + k * OPB
+    const unsigned emptybar = sbase + BAR_OFF + (NS + NOPB) * 8, opempty = sbase + BAR_OFF + (2 * NS + NOPB) * 8;
+    constexpr int OPB = OPS_MAX * OPE * 8;
     if (WS) {
         if (warp >= GEO::THREADS / 32) {  // the producer warpgroup
             asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
@@ -336,11 +345,13 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                                                   cy_hi);
                         ++nh;
                     }
-                    if (no < nfin && (no == 0 || tma::mbar_test_s(opempty, (no - 1) & 1))) {
+                    const int kb = no % NOPB;
+                    if (no < nfin && (no < NOPB || tma::mbar_test_s(opempty + kb * 8, (no / NOPB - 1) & 1))) {
                         const int q = i0 + no;
-                        tma::mbar_expect_tx_s(opbar, P.nops * OP_BYTES);
+                        tma::mbar_expect_tx_s(opbar + kb * 8, P.nops * OP_BYTES);
                         for (int o = 0; o < P.nops; ++o)
-                            tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
+                            tma::load4d_s(opdst + kb * OPB + o * OPE * 8, &M->op[o], opbar + kb * 8, l0 + 2, k0 + NG,
+                                          j0 + NG, q + NG);
 #ifndef VPFV_WS_OP_PF
 #define VPFV_WS_OP_PF 0  // measured: the prefetch code makes ptxas spill (12 B), +7 %
 #endif
@@ -674,8 +685,9 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
 
         // ---- finalise cells q: RK combination, store, non-finite, moment ----
         if (fin_q) {
-            if (nops) tma::mbar_wait_s(opbar, (q - i0) & 1);  // the (q-i0)-th use of the operand barrier
-            const double *op = opbuf + ooff;
+            const int kb = (q - i0) % NOPB;  // operand buffer of this plane
+            if (nops) tma::mbar_wait_s(opbar + kb * 8, ((q - i0) / NOPB) & 1);  // its ((q-i0)/NOPB)-th fill
+            const double *op = opbuf + kb * (OPB / 8) + ooff;
             double out[NC];
             if (nops == 0) {
 #pragma unroll
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                     out[i] = fma(cL, fin[i], fma(oc1, op[OPE + oi], oc0 * op[oi]));
                 }
             }
-            if (WS && nops) tma::mbar_arrive_s(opempty);  // this thread is done with the operand tiles
+            if (WS && nops) tma::mbar_arrive_s(opempty + kb * 8);  // this thread is done with the operand tiles
             double *dq = P.dest + gq;
             if (fold_fb) {  // cL == 0: the src operand could not be folded
 #pragma unroll
@@ -774,7 +786,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
         gq += P1;
         ppart += pstep;
         if (WS)
-            tma::mbar_arrive_s(sbase + BAR_OFF + (NS + 1 + stage_s) * 8);  // this thread is done with the stage
+            tma::mbar_arrive_s(emptybar + stage_s * 8);  // this thread is done with the stage
         else
             __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
@@ -942,6 +954,18 @@ int tma_2d2v_columns(int Ny, int Nvx, int Nvy) {
     return (Ny / rb::BJ) * (Nvx / tile_bk(Nvx, Nvy)) * (Nvy / rb::BL);
 }
 
+static bool rb_ws_enabled() {  // VPFV_RB_WS: the warp-specialised 2D-2V kernel (default on)
+    static int ws = -1;
+    if (ws < 0) {
+        const char *e = getenv("VPFV_RB_WS");
+#ifndef VPFV_RB_WS_DEFAULT
+#define VPFV_RB_WS_DEFAULT 1
+#endif
+        ws = e ? atoi(e) != 0 : VPFV_RB_WS_DEFAULT;
+    }
+    return ws != 0;
+}
+
 template <class GEO>
 static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
                       unsigned flags, int nseg, cudaStream_t s) {
@@ -982,8 +1006,11 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     P.sk = sjk[1] > 0 ? sjk[1] : 1;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
-        cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        if constexpr (GEO::NOPB == 1) {
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GEO::SMEM);
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
+        }
         if constexpr (GEO::MINB == 1) {
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GEO::SMEM);
@@ -992,14 +1019,7 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
         }
         attr = true;
     }
-    static int ws = -1;
-    if (ws < 0) {
-        const char *e = getenv("VPFV_RB_WS");
-#ifndef VPFV_RB_WS_DEFAULT
-#define VPFV_RB_WS_DEFAULT 1
-#endif
-        ws = e ? atoi(e) != 0 : VPFV_RB_WS_DEFAULT;
-    }
+    const bool ws = rb_ws_enabled();
     const int nblocks = (P.Ny / BJ) * (P.Nvx / GEO::BK) * (P.Nvy / BL) * P.nseg;
     bool launched = false;
     if constexpr (GEO::MINB == 1) {  // one CTA per SM: the register pool setmaxnreg redistributes
@@ -1011,11 +1031,13 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
             launched = true;
         }
     }
-    if (launched) {
-    } else if (P.done) {
-        stage2d2v_rb_kernel<GEO, true><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
-    } else {
-        stage2d2v_rb_kernel<GEO, false><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+    if constexpr (GEO::NOPB != 1) {
+        if (!launched) return set_error(VPFV_EARG, "double-buffered operand geometry needs the warp-specialised kernel");
+    } else if (!launched) {
+        if (P.done)
+            stage2d2v_rb_kernel<GEO, true><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+        else
+            stage2d2v_rb_kernel<GEO, false><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
     }
     return check_launch("stage_2d2v_tma");
 }
@@ -1023,6 +1045,15 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
 static int launch_rb(const double *src, const double *const ops[rb::OPS_MAX], const double *tab, Stage22 P,
                      unsigned flags, int nseg, cudaStream_t s) {
     if (tile_cfg(P.Nvx, P.Nvy) == 1) return launch_geo<rb::GeoPair>(src, ops, tab, P, flags, nseg, s);
+    static int opdb = -1;
+    if (opdb < 0) {
+        const char *e = getenv("VPFV_RB_OPDB");
+#ifndef VPFV_RB_OPDB_DEFAULT
+#define VPFV_RB_OPDB_DEFAULT 0  // measured: stages 2-4 +2 % (the 2-deep halo ring costs more than the decoupling gains)
+#endif
+        opdb = e ? atoi(e) != 0 : VPFV_RB_OPDB_DEFAULT;
+    }
+    if (opdb && P.nops > 0 && rb_ws_enabled()) return launch_geo<rb::GeoWideOp>(src, ops, tab, P, flags, nseg, s);
     return launch_geo<rb::GeoWide>(src, ops, tab, P, flags, nseg, s);
 }
 
