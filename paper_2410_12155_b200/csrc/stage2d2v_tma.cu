@@ -333,35 +333,28 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     if (WS) {
         if (warp >= GEO::THREADS / 32) {  // the producer warpgroup
             asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            // two producer lanes, each blocked in mbarrier.try_wait (suspended, not
+            // spinning) on its own stream: warp 8 issues halo planes as soon as
+            // their ring slot's empty barrier completes, warp 9 operand tiles as
+            // soon as the operand buffer's does
             if (tid == GEO::THREADS) {
-                // halo planes as soon as their ring slot is free, operand tiles as soon as
-                // the single operand buffer is (both polled, neither blocks the other)
-                const int nfin = P.nops ? i1 - i0 : 0;
-                int nh = 0, no = 0;
-                while (nh < nplanes || no < nfin) {
-                    if (nh < nplanes && (nh < NS || tma::mbar_test_s(emptybar + (nh % NS) * 8, (nh / NS - 1) & 1))) {
-                        for (int w = 0; w < 4; ++w)
-                            issue_plane_part<GEO>(w, sbase, M, nh, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core,
-                                                  cy_hi);
-                        ++nh;
-                    }
-                    const int kb = no % NOPB;
-                    if (no < nfin && (no < NOPB || tma::mbar_test_s(opempty + kb * 8, (no / NOPB - 1) & 1))) {
-                        const int q = i0 + no;
-                        tma::mbar_expect_tx_s(opbar + kb * 8, P.nops * OP_BYTES);
-                        for (int o = 0; o < P.nops; ++o)
-                            tma::load4d_s(opdst + kb * OPB + o * OPE * 8, &M->op[o], opbar + kb * 8, l0 + 2, k0 + NG,
-                                          j0 + NG, q + NG);
-#ifndef VPFV_WS_OP_PF
-#define VPFV_WS_OP_PF 0  // measured: the prefetch code makes ptxas spill (12 B), +7 %
+                for (int nh = 0; nh < nplanes; ++nh) {
+#ifndef VPFV_WS_HINT_NS
+#define VPFV_WS_HINT_NS 1000000
 #endif
-                        // the single operand buffer is refilled one plane ahead of its use:
-                        // later operand tiles go to L2 now, so the refill hits L2
-                        if (VPFV_WS_OP_PF > 0 && no + VPFV_WS_OP_PF < nfin)
-                            for (int o = 0; o < P.nops; ++o)
-                                tma::prefetch4d(&M->op[o], l0 + 2, k0 + NG, j0 + NG, q + VPFV_WS_OP_PF + NG);
-                        ++no;
-                    }
+                    if (nh >= NS) tma::mbar_wait_sleep_s(emptybar + (nh % NS) * 8, (nh / NS - 1) & 1, VPFV_WS_HINT_NS);
+                    for (int w = 0; w < 4; ++w)
+                        issue_plane_part<GEO>(w, sbase, M, nh, p_first, P, i0, i1, l0, k0, j0, cy_lo, cy_core, cy_hi);
+                }
+            } else if (tid == GEO::THREADS + 32 && P.nops) {
+                for (int no = 0; no < i1 - i0; ++no) {
+                    const int kb = no % NOPB;
+                    if (no >= NOPB) tma::mbar_wait_sleep_s(opempty + kb * 8, (no / NOPB - 1) & 1, VPFV_WS_HINT_NS);
+                    const int q = i0 + no;
+                    tma::mbar_expect_tx_s(opbar + kb * 8, P.nops * OP_BYTES);
+                    for (int o = 0; o < P.nops; ++o)
+                        tma::load4d_s(opdst + kb * OPB + o * OPE * 8, &M->op[o], opbar + kb * 8, l0 + 2, k0 + NG,
+                                      j0 + NG, q + NG);
                 }
             }
             __syncwarp();

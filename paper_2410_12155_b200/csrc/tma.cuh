@@ -138,6 +138,21 @@ __device__ __forceinline__ void mbar_arrive_s(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// blocking wait with a suspend-time hint: the thread may sleep up to `ns`
+// nanoseconds per try (woken when the phase completes), for waiters with
+// nothing else to do (the producer lanes)
+__device__ __forceinline__ void mbar_wait_sleep_s(unsigned bar, unsigned parity, unsigned ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
+
 // non-blocking: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test_s(unsigned bar, unsigned parity) {
     unsigned done;
