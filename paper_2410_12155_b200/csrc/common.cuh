@@ -34,11 +34,16 @@ bool pdl_enabled();  // VPFV_PDL != 0
 // has made its stores (peer ones included) visible system-wide, count the
 // CTA; the last one bumps both neighbours' signal words (csrc/peer.cu).
 // P: a stage parameter block with done / sig_lo / sig_hi.
+// nthreads > 0: only the first nthreads threads take part (named barrier 1),
+// for warp-specialised kernels whose producer warps make no peer stores
 template <class StageParams>
-__device__ __forceinline__ void peer_done_signal(const StageParams &P) {
+__device__ __forceinline__ void peer_done_signal(const StageParams &P, int nthreads = 0) {
     if (!P.done) return;
     __threadfence_system();
-    __syncthreads();
+    if (nthreads > 0)
+        asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+    else
+        __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned prev = atomicAdd(P.done, 1u);
         if (prev == gridDim.x - 1) {

@@ -357,9 +357,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                                       j0 + NG, q + NG);
                 }
             }
-            __syncwarp();
-            if (PEER) peer_done_signal(P);
-            return;
+            return;  // no peer stores here: the compute threads count the CTA (named barrier)
         }
         asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
     } else if (tid == 0) {
@@ -783,7 +781,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
         else
             __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
-    if (PEER) peer_done_signal(P);
+    if (PEER) peer_done_signal(P, WS ? GEO::THREADS : 0);
 }
 
 // ---------------------------------------------------------------------------

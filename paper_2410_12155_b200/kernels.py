@@ -275,7 +275,9 @@ class _DropIn:
 
     def __init__(self, grid, species, device, exact):
         self.grid, self.device = grid, device
-        self.bufs = [torch.empty(grid.padded_shape, dtype=torch.float64, device=device) for _ in range(4)]
+        # zeroed once: the chunked download moves whole planes (ghosts included)
+        # and keeps only interiors; no copy then reads uninitialised memory
+        self.bufs = [torch.zeros(grid.padded_shape, dtype=torch.float64, device=device) for _ in range(4)]
         self.tables = StageTables(grid, species, device)
         self.flags = _lib.VPFV_EXACT if exact else 0
         self.tiled = self.tables.fused_moment_ok(self.flags)

@@ -2,7 +2,8 @@
 # synchronisation code: the TMA/mbarrier rings of the tiled 2D-2V and 1D-2V
 # kernels, the bulk-copy ring of the 1D-1V march kernel, the PDL field chain,
 # the x-range launches, the last-CTA `done` counters, the fused moment finish
-# and the linked-slab peer push (system-scope signal words).
+# the linked-slab peer push (system-scope signal words), and (round 2) the
+# warp-specialised 2D-2V kernel's full/empty mbarrier protocol (the default).
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash scripts/gpu_sanitize.sh'
 # Logs: gpurun_out/san_<tool>.log; summary: gpurun_out/san_summary.txt
 mkdir -p gpurun_out
@@ -17,7 +18,8 @@ SEL='test_tiled_stage_vs_oracle and coef0-N0
   or test_tiled_stage_nonfinite_index
   or test_landau2d_steps_fused_path_vs_c_oracle and 32
   or test_moment_partials_finish_is_the_fold_tree
-  or test_peer_halo_push_linked_slabs_equal_simulation and 2'
+  or test_peer_halo_push_linked_slabs_equal_simulation and 2
+  or test_tiled_stage_vx_sign_layouts and coef1-vx0'
 SEL=$(echo $SEL)
 : > gpurun_out/san_summary.txt
 for tool in memcheck racecheck synccheck initcheck; do
