@@ -87,9 +87,9 @@ constexpr int BJ = 8, BL = 16, OPS_MAX = 2;
 enum { T_EVX = 0, T_EVY = 1, T_C3 = 2, T_C4 = 3, T_C1 = 4, T_C5 = 5 };
 // Tile geometry: (BJ, BK, BL) column block, NS-deep stage ring, MINB CTAs
 // per SM; one thread per 2 (y) x BB (vx) cells at one vy lane.
-template <int BK_, int NS_, int MINB_, int NOPB_ = 1>
+template <int BK_, int NS_, int MINB_, int NOPB_ = 1, int BB_ = 4>
 struct Geo {
-    static constexpr int BK = BK_, NS = NS_, MINB = MINB_, BB = 4, NOPB = NOPB_;  // NOPB: operand buffers
+    static constexpr int BK = BK_, NS = NS_, MINB = MINB_, BB = BB_, NOPB = NOPB_;  // NOPB: operand buffers
     static constexpr int THREADS = (BJ / 2) * (BK / BB) * BL;
     static constexpr int TJ = BJ + 6, TK = BK + 6, TW = BL + 8;  // halo tile (vy box starts 16 B aligned)
     static constexpr int KL = TK * TW, HALO = TJ * KL;
@@ -1002,7 +1002,7 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
                                  GEO::SMEM);
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEO::SMEM);
         }
-        if constexpr (GEO::MINB == 1) {
+        if constexpr (GEO::MINB == 1 && GEO::THREADS == 256) {
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GEO::SMEM);
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1013,7 +1013,7 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     const bool ws = rb_ws_enabled();
     const int nblocks = (P.Ny / BJ) * (P.Nvx / GEO::BK) * (P.Nvy / BL) * P.nseg;
     bool launched = false;
-    if constexpr (GEO::MINB == 1) {  // one CTA per SM: the register pool setmaxnreg redistributes
+    if constexpr (GEO::MINB == 1 && GEO::THREADS == 256) {  // one CTA per SM: the register pool setmaxnreg redistributes
         if (ws) {
             if (P.done)
                 stage2d2v_rb_kernel<GEO, true, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);

@@ -10,16 +10,17 @@ Line ranges follow the current source (update them when the kernel moves).
 import re
 import sys
 
-REGIONS = [  # (name, first line, last line) in csrc/stage2d2v_tma.cu
-    ("upwind 6-point chains wpos/wneg (inlined into every stencil)", 125, 130),
-    ("x scatter + window slide", 138, 222),
-    ("TMA issue (producer lanes)", 223, 257),
-    ("loop head, producer branch, stage wait", 384, 438),
-    ("own rows: loads, D/G, x-coupled, vx/vy lines, diag", 439, 586),
-    ("y arms: y lines, arm corners, fold", 587, 626),
-    ("finalise: RK combination, stores", 627, 666),
-    ("finalise: moment partials + non-finite", 667, 728),
-    ("plane advance + barrier", 729, 736),
+REGIONS = [  # (name, first line, last line) in csrc/stage2d2v_tma.cu (round-2 final source)
+    ("upwind 6-point chains wpos/wneg (inlined into every stencil)", 131, 136),
+    ("x scatter + window slide", 143, 228),
+    ("TMA issue (producer lanes)", 229, 264),
+    ("kernel setup, producer warpgroup", 265, 429),
+    ("loop head, stage wait, tables", 430, 484),
+    ("own rows: loads, D/G, x-coupled, vx/vy lines, diag", 485, 632),
+    ("y arms: y lines, arm corners, fold", 633, 672),
+    ("finalise: RK combination, stores", 673, 714),
+    ("finalise: moment partials + non-finite", 715, 776),
+    ("plane advance + empty-barrier arrive", 777, 786),
     ("inlined helpers (tma.cuh mbarrier waits, common.cuh)", 100000, 200000),
 ]
 
