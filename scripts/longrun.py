@@ -8,7 +8,8 @@
   total-energy drift.
 
 Diagnostics rows come from the device (Simulation.run -> DeviceDiagnostics).
-Writes profiles/r1_longrun.json and a CSV per run.
+Writes <outdir>/<tag>_longrun.json and a CSV per run (tag: VPFV_LONGRUN_TAG,
+default r2).
 
     python scripts/longrun.py [outdir]
 """
@@ -23,6 +24,7 @@ from paper_2410_12155_b200 import problems as P, runner as R  # noqa: E402
 from paper_2410_12155_b200.diagnostics import DiagnosticsRow, fit_growth_rate, fit_peak_rate  # noqa: E402
 
 out = sys.argv[1] if len(sys.argv) > 1 else "profiles"
+TAG = os.environ.get("VPFV_LONGRUN_TAG", "r2")
 os.makedirs(out, exist_ok=True)
 
 
@@ -32,7 +34,7 @@ def run(name, setup, t_end, cadence, max_steps=10 ** 7):
     rows = sim.run(t_end, cadence=cadence, max_steps=max_steps)
     wall = time.perf_counter() - t0
     names = [f.species for f in setup.dists]
-    with open(os.path.join(out, f"r1_longrun_{name}.csv"), "w", newline="") as fh:
+    with open(os.path.join(out, f"{TAG}_longrun_{name}.csv"), "w", newline="") as fh:
         w = csv.writer(fh)
         w.writerow(DiagnosticsRow.header(names))
         for r in rows:
@@ -59,6 +61,6 @@ m0, m1 = rows[0].mass[0][1], rows[-1].mass[0][1]
 e0, e1 = rows[0].total_energy, rows[-1].total_energy
 summary["landau2d_128"] = {"steps": sim.step_count, "t_end": sim.t, "wall_s": wall,
                            "mass_rel_drift": abs(m1 - m0) / abs(m0), "energy_rel_drift": abs(e1 - e0) / abs(e0)}
-with open(os.path.join(out, "r1_longrun.json"), "w") as fh:
+with open(os.path.join(out, f"{TAG}_longrun.json"), "w") as fh:
     json.dump(summary, fh, indent=1)
 print(json.dumps(summary, indent=1))
