@@ -262,7 +262,10 @@ __device__ __forceinline__ void issue_plane_part(int w, unsigned sbase, const Ma
 // registers; one lane works) issues every TMA load, driven by full/empty
 // mbarriers, and the compute warps (240 registers) never meet at a CTA
 // barrier inside the plane loop (VPFV_RB_WS=1).
-template <class GEO, bool PEER, bool WS = false>
+// NV > 0: an instantiation for Nvx == Nvy == NV, so the padded strides are
+// compile-time and the epilogue's eight stores take one base address plus
+// immediate offsets (VPFV_RB_NV; the launcher picks it when the extents match)
+template <class GEO, bool PEER, bool WS = false, int NV = 0>
 __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     stage2d2v_rb_kernel(const __grid_constant__ Maps maps, const Stage22 P) {
     using namespace rb;
@@ -404,7 +407,8 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     const int ooff = ((2 * tj) * BK + BB * tk) * OPW + tl + 1;          // cell (0, 0) in an operand tile
     const int toff = (2 * tj) * 8;                                      // table entry of row y0, plane p-1
 
-    const long long P3 = P.Nvy + 2 * NG, P2 = (long long)(P.Nvx + 2 * NG) * P3,
+    const long long P3 = NV > 0 ? NV + 2 * NG : P.Nvy + 2 * NG,
+                    P2 = (long long)(NV > 0 ? NV + 2 * NG : P.Nvx + 2 * NG) * P3,
                     P1 = (long long)(P.Ny + 2 * NG) * P2;
     // padded index of cell (q = p - 3, y0, vx0, vy) for the first plane
     long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(y0 + NG) * P2 +
@@ -1007,6 +1011,8 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
                                  GEO::SMEM);
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GEO::SMEM);
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GEO::SMEM);
         }
         attr = true;
     }
@@ -1015,8 +1021,18 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
     bool launched = false;
     if constexpr (GEO::MINB == 1 && GEO::THREADS == 256) {  // one CTA per SM: the register pool setmaxnreg redistributes
         if (ws) {
+#ifndef VPFV_RB_NV_DEFAULT
+#define VPFV_RB_NV_DEFAULT 1
+#endif
+            static int nv = -1;
+            if (nv < 0) {
+                const char *e = getenv("VPFV_RB_NV");
+                nv = e ? atoi(e) != 0 : VPFV_RB_NV_DEFAULT;
+            }
             if (P.done)
                 stage2d2v_rb_kernel<GEO, true, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+            else if (nv && P.Nvx == 128 && P.Nvy == 128)
+                stage2d2v_rb_kernel<GEO, false, true, 128><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
             else
                 stage2d2v_rb_kernel<GEO, false, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
             launched = true;
