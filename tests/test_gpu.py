@@ -616,6 +616,37 @@ def test_tiled_stage_x_ranges_equal_full_launch(N):
 
 
 @pytest.mark.gpu
+def test_tiled_kernel_variants_bitwise(tmp_path):
+    """Every 2D-2V kernel variant the VPFV_RB_* switches select runs the same
+    arithmetic: the warp-specialised default (compile-time strides at
+    Nvx = Nvy = 128), its runtime-stride instantiation, the round-1 barrier
+    loop, and the double-buffered operand geometry give bitwise the same
+    RK4 step (buffers, fused partials, non-finite word).  One process per
+    variant (the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(__file__), "helpers", "kernel_variant_step.py")
+    variants = {"default": {}, "runtime_strides": {"VPFV_RB_NV": "0"}, "barrier_loop": {"VPFV_RB_WS": "0"},
+                "double_buffered_operands": {"VPFV_RB_OPDB": "1"}}
+    got = {}
+    for name, env in variants.items():
+        out = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ)
+        for k in ("VPFV_RB_NV", "VPFV_RB_WS", "VPFV_RB_OPDB", "VPFV_RB_CFG"):
+            e.pop(k, None)
+        e.update(env)
+        subprocess.run([sys.executable, helper, out], env=e, check=True, timeout=300)
+        got[name] = np.load(out)
+    ref = got["default"]
+    assert int(ref["nonfinite"][0]) == -1
+    for name, z in got.items():
+        for key in ("f0", "f1", "fout", "partials", "nonfinite"):
+            assert np.array_equal(z[key], ref[key]), (name, key)
+
+
+@pytest.mark.gpu
 def test_host_pipeline_equals_advance():
     """runner.HostPipeline (overlapped H2D / step / D2H of host states) gives
     bitwise the state Simulation.advance gives for each input."""
