@@ -1013,6 +1013,8 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
                                  GEO::SMEM);
             cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GEO::SMEM);
+            cudaFuncSetAttribute(stage2d2v_rb_kernel<GEO, false, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GEO::SMEM);
         }
         attr = true;
     }
@@ -1033,6 +1035,8 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
                 stage2d2v_rb_kernel<GEO, true, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
             else if (nv && P.Nvx == 128 && P.Nvy == 128)
                 stage2d2v_rb_kernel<GEO, false, true, 128><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+            else if (nv && P.Nvx == 64 && P.Nvy == 64)  // config 5's 2 x 64^4
+                stage2d2v_rb_kernel<GEO, false, true, 64><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
             else
                 stage2d2v_rb_kernel<GEO, false, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
             launched = true;
