@@ -639,16 +639,33 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
         auto yarms = [&](auto ypos_tag) {
             constexpr bool YP = decltype(ypos_tag)::value;
             const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
+#ifndef VPFV_YARM_PERCELL
+            // the arm rows at the thread's vy, vx offsets -1 .. BB, loaded once:
+            // qm/qp and the D differences of all BB cells come from them
+            // (12 loads instead of 24 per plane)
+            double am[BB + 2], ap[BB + 2];
+#pragma unroll
+            for (int b = 0; b < BB + 2; ++b) {
+                am[b] = rm[(b - 1) * TW];
+                ap[b] = rp[(b - 1) * TW];
+            }
+#endif
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
 #ifndef VPFV_YARM_NOFENCE
                 SCHED_FENCE();
 #endif
+#ifndef VPFV_YARM_PERCELL
+                const double qm = am[b + 1], qp = ap[b + 1];
+                const double Dkm = am[b] - am[b + 2];
+                const double Dkp = ap[b] - ap[b + 2];
+#else
                 const double qm = rm[b * TW], qp = rp[b * TW];
-                const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
-                const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
                 const double Dkm = rm[(b - 1) * TW] - rm[(b + 1) * TW];
                 const double Dkp = rp[(b - 1) * TW] - rp[(b + 1) * TW];
+#endif
+                const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
+                const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
                 const double z0 = s0[b], z1 = s0[BB + b];
                 double w0, w1;
                 if (YP) {
