@@ -191,6 +191,10 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     const int ooff = BB * tk * OPW + tl + 1;
     const long long P2 = P.Nvy + 2 * NG, P1 = (long long)(P.Nvx + 2 * NG) * P2;
     long long gq = (long long)(p_first - 3 + NG) * P1 + (long long)(vx0 + NG) * P2 + (vy + NG);
+    // moment partials of row vx0 + tl for the first iteration's cell plane (lanes tl < BB store),
+    // advanced one plane per iteration
+    const long long pstep = (long long)P.Nvx * nlt;
+    double *ppart = P.partials + (long long)(p_first - 3) * pstep + (long long)(vx0 + (tl % BB)) * nlt + lt;
 
     double acc[BB][6];
 #pragma unroll
@@ -349,10 +353,11 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 double w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
                 w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
                 w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
-                if (tl < BB) P.partials[((long long)q * P.Nvx + vx0 + tl) * nlt + lt] = w1;  // lane tl: row tl
+                if (tl < BB) *ppart = w1;  // lane tl: row tl
             }
         }
         gq += P1;
+        ppart += pstep;
         __syncthreads();  // the stage and the operand tiles are free for the next refill
     }
     if (PEER) peer_done_signal(P);
