@@ -147,7 +147,6 @@ __device__ __forceinline__ double wneg(double m2, double m1, double z, double p1
 // x-stencil offset -3 (a_x > 0) or -2 (a_x <= 0) -- so no slot is zeroed.
 template <int SIGN>  // +1: a_x > 0, -1: a_x <= 0
 __device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &fin) {
-#ifndef VPFV_SLIDE_DESC
     // The slide as in-order renaming: slot j's FMA reads slot j+1, so each
     // result can take the register its slot had, and the finished cell comes
     // out of an instruction (w0 + 0: exact, and unlike 0*t + w0 it cannot pick
@@ -172,31 +171,6 @@ __device__ __forceinline__ void scatter_cell(double (&w)[6], double ti, double &
         w[5] = 0.0;
     }
 }
-#else  // round 1 order (VPFV_SLIDE_DESC, A/B only)
-    if (SIGN > 0) {
-        w[5] = fma(15.0, ti, w[5]);
-        w[4] = fma(-60.0, ti, w[4]);
-        w[3] = fma(20.0, ti, w[3]);
-        w[2] = fma(30.0, ti, w[2]);
-        w[1] = fma(-3.0, ti, w[1]);
-        fin = w[0];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) w[j] = w[j + 1];
-        w[5] = -2.0 * ti;  // cell p+3 enters
-    } else {
-        const double c2 = 3.0 * ti;  // cell p+2 enters (its slot was freed last plane)
-        w[4] = fma(-30.0, ti, w[4]);
-        w[3] = fma(-20.0, ti, w[3]);
-        w[2] = fma(60.0, ti, w[2]);
-        w[1] = fma(-15.0, ti, w[1]);
-        fin = fma(2.0, ti, w[0]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = w[j + 1];
-        w[4] = c2;
-        w[5] = 0.0;
-    }
-}
-#endif
 
 // The sign of a_x is per vx; a thread's BB vx cells share it unless the zero
 // crossing falls inside them (one uniform branch, no predication).
@@ -426,11 +400,6 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
 #pragma unroll
         for (int m = 0; m < 6; ++m) acc[i][m] = 0.0;
 
-#ifdef VPFV_UNROLL_PLANES  // experiment: unrolled plane loop (window slide by renaming)
-#define VPFV_PRAGMA_(x) _Pragma(#x)
-#define VPFV_UNROLL_(n) VPFV_PRAGMA_(unroll n)
-    VPFV_UNROLL_(VPFV_UNROLL_PLANES)
-#endif
     for (int n = 0; n < nplanes; ++n) {
         const int p = p_first + n, q = p - 3;
         const bool inner = p >= i0 && p < i1;
@@ -454,13 +423,6 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                 tma::load4d_s(opdst + o * OPE * 8, &M->op[o], opbar, l0 + 2, k0 + NG, j0 + NG, q + NG);
 #endif
             }
-#ifndef VPFV_OP_PF
-#define VPFV_OP_PF 0  // measured: +1 % on stage 4, -4 % on stage 1 (register schedule)
-#endif
-            // the operand tiles of cell plane q + VPFV_OP_PF into L2: the single
-            // operand buffer is loaded only one plane ahead of its use
-            if (VPFV_OP_PF > 0 && op_lane && o >= 0 && o < nops && q + VPFV_OP_PF >= i0 && q + VPFV_OP_PF < i1)
-                tma::prefetch4d(&M->op[o], l0 + 2, k0 + NG, j0 + NG, q + VPFV_OP_PF + NG);
         }
         // stage and parity from the plane number (loop-carried counters get spilled)
         const int nq3 = n / NS, stage_s = n - nq3 * NS;
@@ -489,9 +451,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
         // ---- own rows (a = 0, 1): vy lines, vx lines, D and G -------------
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
-#ifndef VPFV_ROW_NOFENCE
             SCHED_FENCE();  // one row at a time
-#endif
             const double *ca = c + a * KL;
             double v[BB][7];
 #pragma unroll
@@ -536,52 +496,6 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                 const double gp = ca[BB * TW - 1] - ca[BB * TW + 1];  // G at vx offset BB
                 const double avx = evx[a] + cBvy;                    // a_vx is independent of vx
                 const double avx_s = avx * mhvx;
-#ifdef VPFV_MERGE_STENCILS  // experiment (measured no gain): the row's vx and vy lines in one block
-                // the row's vx and vy lines in one sign-specialised block: 2 x BB
-                // independent 6-deep chains to interleave (in two separate
-                // branch blocks they were BB each), folded in the same order
-                {
-                    double wx[BB], wy[BB];
-                    auto lines = [&](auto vxp_tag, auto vys_tag) {
-                        constexpr bool VXP = decltype(vxp_tag)::value;
-                        constexpr int VYS = decltype(vys_tag)::value;
-#pragma unroll
-                        for (int b = 0; b < BB; ++b) {
-                            wx[b] = VXP ? wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5])
-                                        : wneg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]);
-                            if (VYS > 0)
-                                wy[b] = wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]);
-                            else if (VYS < 0)
-                                wy[b] = wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
-                            else
-                                wy[b] = evy[a] + bvx[b] > 0.0 ? wpos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
-                                                              : wneg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
-                        }
-                    };
-                    using T1 = std::true_type;
-                    using F1 = std::false_type;
-                    using YP = std::integral_constant<int, 1>;
-                    using YN = std::integral_constant<int, -1>;
-                    using YM = std::integral_constant<int, 0>;
-                    // a_vy = evy - cB vx: one sign for the row when the BB signs agree
-                    // (always when cB == 0; fl(e + x) is monotone in x)
-                    const int vys = evy[a] + bvx_min > 0.0 ? 1 : (evy[a] + bvx_max <= 0.0 ? -1 : 0);
-                    if (avx > 0.0) {
-                        if (vys > 0) lines(T1{}, YP{});
-                        else if (vys < 0) lines(T1{}, YN{});
-                        else lines(T1{}, YM{});
-                    } else {
-                        if (vys > 0) lines(F1{}, YP{});
-                        else if (vys < 0) lines(F1{}, YN{});
-                        else lines(F1{}, YM{});
-                    }
-#pragma unroll
-                    for (int b = 0; b < BB; ++b) {
-                        acc[a * BB + b][3] = fma(avx_s, wx[b], acc[a * BB + b][3]);
-                        acc[a * BB + b][3] = fma((evy[a] + bvx[b]) * mhvy, wy[b], acc[a * BB + b][3]);
-                    }
-                }
-#else
 #ifdef VPFV_EXP_FORCE_AV
                 if (true) {
 #else
@@ -622,7 +536,6 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                         acc[a * BB + b][3] = fma(avy * mhvy, w, acc[a * BB + b][3]);
                     }
                 }
-#endif
                 // diag(vx,vy) = G(vx+1) - G(vx-1)
                 double gr[BB + 2];
                 gr[0] = gm;
@@ -639,7 +552,6 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
         auto yarms = [&](auto ypos_tag) {
             constexpr bool YP = decltype(ypos_tag)::value;
             const double *rm = c - KL, *rp = c + 2 * KL;  // rows a = -1 and a = 2
-#ifndef VPFV_YARM_PERCELL
             // the arm rows at the thread's vy, vx offsets -1 .. BB, loaded once:
             // qm/qp and the D differences of all BB cells come from them
             // (12 loads instead of 24 per plane)
@@ -649,21 +561,12 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                 am[b] = rm[(b - 1) * TW];
                 ap[b] = rp[(b - 1) * TW];
             }
-#endif
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
-#ifndef VPFV_YARM_NOFENCE
                 SCHED_FENCE();
-#endif
-#ifndef VPFV_YARM_PERCELL
                 const double qm = am[b + 1], qp = ap[b + 1];
                 const double Dkm = am[b] - am[b + 2];
                 const double Dkp = ap[b] - ap[b + 2];
-#else
-                const double qm = rm[b * TW], qp = rp[b * TW];
-                const double Dkm = rm[(b - 1) * TW] - rm[(b + 1) * TW];
-                const double Dkp = rp[(b - 1) * TW] - rp[(b + 1) * TW];
-#endif
                 const double Gm = rm[b * TW - 1] - rm[b * TW + 1];
                 const double Gp = rp[b * TW - 1] - rp[b * TW + 1];
                 const double z0 = s0[b], z1 = s0[BB + b];
