@@ -305,7 +305,8 @@ def run_b200(args, rank, world, device):
     stage_ms = sim.stage_kernel_ms()  # per RK stage slot, summed over the pass's steps and species
     sim.enable_stage_timing(False)
     launches_per_step = sim.launches_per_step()
-    nvlink = nvlink_line(sim, world, ms_local / args.steps)
+    p2p = measured_p2p_gbs(device, world) if world > 1 and rank == 0 else None
+    nvlink = nvlink_line(sim, world, ms_local / args.steps, p2p)
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], dtype=torch.float64, device=device)
@@ -469,19 +470,41 @@ def l2_note(setup):
             f"not flushed -- a parity configuration, not the bench line of record")
 
 
-def nvlink_line(sim, world, ms_per_step):
-    """Halo traffic of the multi-GPU step against the NVLink 5 roofline
-    (900 GB/s per direction per GPU, B200_PROFILING.md): the bytes each rank
-    sends per step and the rate they would need if the exchange were not
-    overlapped with compute (a lower bound on the link share of the step)."""
+def measured_p2p_gbs(device, world):
+    """NVLink peer copy bandwidth from this rank's GPU to the next one
+    (scripts/probes/nvlink_p2p.py's measurement, 256 MiB, best of 5), or None
+    when the ranks share a GPU or have no peer access."""
+    try:
+        import torch
+
+        sys.path.insert(0, os.path.join(ROOT, "scripts", "probes"))
+        from nvlink_p2p import p2p_gbs
+
+        src = device.index if device.index is not None else torch.cuda.current_device()
+        if torch.cuda.device_count() < 2:
+            return None
+        return p2p_gbs(src, (src + 1) % torch.cuda.device_count(), mib=256)
+    except Exception:  # noqa: BLE001 -- a probe; the line falls back to the nominal peak
+        return None
+
+
+def nvlink_line(sim, world, ms_per_step, p2p=None):
+    """Halo traffic of the multi-GPU step against the NVLink 5 roofline: the
+    bytes each rank sends per step and the rate they would need if the
+    exchange were not overlapped with compute (a lower bound on the link
+    share of the step), against the measured peer copy bandwidth of this box
+    when there is one (else the nominal 900 GB/s per direction,
+    B200_PROFILING.md)."""
     if world == 1 or not hasattr(sim, "traffic_report"):
         return None
     t = sim.traffic_report()
     per_step = 4 * t["total_bytes"]
     gbs = per_step / (ms_per_step / 1e3) / 1e9
+    peak = p2p if p2p else 900.0
     return {"bytes_per_rank_per_step": per_step, "x_halo_bytes_per_stage": t["x_halo_bytes"],
             "v_face_bytes_per_stage": t["v_face_bytes"], "density_bytes_per_stage": t["density_bytes"],
-            "rate_at_step_time_GBs": gbs, "peak_GBs": 900.0, "frac": gbs / 900.0}
+            "rate_at_step_time_GBs": gbs, "peak_GBs": peak, "peak_kind": "measured p2p copy" if p2p else "nominal",
+            "frac": gbs / peak}
 
 
 def e2e_measure(sim, dt, steps, device, cells):
