@@ -35,6 +35,14 @@
 //    four levels of the reference fold tree over each aligned 16-wide vy
 //    chunk (transpose-reduce over the 16 vy lanes), finished by
 //    vpfv_moment_partials.  This replaces a separate moment pass over f.
+//  * Round 2 (default, 1 CTA/SM geometry): warp-specialised.  A fourth
+//    warpgroup gives up its registers (setmaxnreg 24; the 8 compute warps
+//    take 240) and two of its lanes issue every TMA load -- halo planes and
+//    RK operand tiles -- each blocked in mbarrier.try_wait on the empty
+//    barrier its stream refills; compute warps wait on full barriers and
+//    arrive on empty ones, with no CTA barrier in the plane loop.  The
+//    headline 128-wide velocity shape (and config 5's 64-wide one) runs an
+//    instantiation with compile-time padded strides.
 //
 // Requirements (checked by the launcher, else the generic kernel runs):
 // Ny % 8 == 0, Nvx % 16 == 0, Nvy % 16 == 0, periodic-or-halo x/y, stored
