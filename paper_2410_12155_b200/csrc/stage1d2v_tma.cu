@@ -1,5 +1,5 @@
-// 1D-2V fused stage: x-marching, TMA-staged (vx, vy) halo tiles, 4-cell
-// register blocks (sm_100a, fast arithmetic path).
+// 1D-2V fused stage: x-marching, TMA-staged (vx, vy) halo tiles, 8-cell
+// (default) or 4-cell register blocks (sm_100a, fast arithmetic path).
 //
 // Operator of stage_1d2v (/root/reference/pkg/src/vpfv/_kernels.py:153-197):
 //   rhs = -a_x D_x f - a_vx D_vx f - a_vy D_vy f + c1 diag(x,vx) - c2 diag(vx,vy)
@@ -7,16 +7,20 @@
 // with a_x = vxc[j], a_vx = evx[i] + cB vyc[k], a_vy = avy[j].
 //
 // The 2D-2V kernel's design (stage2d2v_tma.cu) with no y direction:
-//  * a CTA (128 threads, 3 per SM) owns a (vx, vy) = (32, 16) column block
+//  * a CTA (64 threads, 4 per SM; round 1: 128 threads, 3 per SM) owns a
+//    (vx, vy) = (32, 16) column block
 //    and marches x; each thread keeps, per cell, a sliding window of 6 fp64
 //    accumulators (cells p-3..p+2) and scatters s(p) into it -- the x
 //    direction costs no shared-memory traffic;
 //  * per plane one (38, 24) halo tile, the packed (evx, c1) rows of planes
-//    p-1..p+1 and the RK operand tiles of cell plane p-3 arrive by TMA, 4
-//    stages deep on mbarrier transaction counts (a 1D-2V plane is too short
-//    a step to hide an operand load issued one plane ahead);
-//  * a thread owns 4 consecutive vx cells at one vy lane: 38 shared loads per
-//    plane, 9.5 per cell; diag(vx,vy) = G(vx+1) - G(vx-1) with
+//    p-1..p+1 and the RK operand tiles of cell plane p-3 arrive by TMA, 3
+//    (8-cell) or 4 (4-cell) stages deep on mbarrier transaction counts (a
+//    1D-2V plane is too short a step to hide an operand load issued one
+//    plane ahead);
+//  * a thread owns 8 (or 4) consecutive vx cells at one vy lane: 70 (38)
+//    shared loads per plane, 8.75 (9.5) per cell, and the per-plane
+//    overhead (ring wait, barrier, epilogue branches, partials) over twice
+//    the cells; diag(vx,vy) = G(vx+1) - G(vx-1) with
 //    G = s[vy-1] - s[vy+1], and the x-coupled correction uses
 //    D = s[vx-1] - s[vx+1];
 //  * RK operands aliasing src are folded into the accumulator (cfold/cL s);
@@ -56,10 +60,12 @@ struct Stage12 {
 };
 
 namespace r12 {
-constexpr int BL = 16, BB = 4, NS = 4, OPS_MAX = 2;
-template <int BK_, int MINB_>
+constexpr int BL = 16, OPS_MAX = 2;
+// BB: consecutive vx cells per thread (4, or 8: half the per-plane overhead
+// per cell at half the warps); NS: stage ring depth
+template <int BK_, int MINB_, int BB_ = 4, int NS_ = 4>
 struct Geo {
-    static constexpr int BK = BK_, MINB = MINB_;
+    static constexpr int BK = BK_, MINB = MINB_, BB = BB_, NS = NS_;
     static constexpr int THREADS = (BK / BB) * BL;
     static constexpr int TK = BK + 6, TW = BL + 8;  // halo tile (vy box starts 16 B aligned)
     static constexpr int HALO = TK * TW;
@@ -118,7 +124,8 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     stage1d2v_rb_kernel(const __grid_constant__ Maps12 maps, const Stage12 P) {
     using namespace r12;
     constexpr int BK = GEO::BK, TW = GEO::TW, HALO = GEO::HALO, TAB = GEO::TAB, STAGE = GEO::STAGE, OPW = GEO::OPW,
-                  OPE = GEO::OPE, BAR_OFF = GEO::BAR_OFF;
+                  OPE = GEO::OPE, BAR_OFF = GEO::BAR_OFF, BB = GEO::BB, NS = GEO::NS;
+    static_assert(BB % 4 == 0 && BB <= 8, "4 or 8 cells per thread");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + BAR_OFF);  // NS stage barriers
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         return;
     }
 
-    // thread -> cells (vx0 + b, vy), b < 4; half-warps are 16-lane vy rows
+    // thread -> cells (vx0 + b, vy), b < BB; half-warps are 16-lane vy rows
     const int lane = tid & 31, warp = tid >> 5;
     const int tl = lane & 15;
     const int tk = (warp << 1) | (lane >> 4);
@@ -178,8 +185,12 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         avy_s[b] = ay * P.mhvy;
         ypos[b] = ay > 0.0;
     }
-    const bool ypos_all = ypos[0] && ypos[1] && ypos[2] && ypos[3];
-    const bool yneg_all = !ypos[0] && !ypos[1] && !ypos[2] && !ypos[3];
+    bool ypos_all = true, yneg_all = true;
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+        ypos_all = ypos_all && ypos[b];
+        yneg_all = yneg_all && !ypos[b];
+    }
     const double cBvy = __ldg(P.vyc + P.Nvy) * __ldg(P.vyc + vy);  // cB rides in vyc[Nvy] (_kernels.py:166)
     const double cL = P.dt_dev ? __ddiv_rn(*P.dt_dev, P.cL_div) : P.cL;
     const bool fold = P.fold && cL != 0.0;
@@ -214,25 +225,22 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
         const double *tb = stage + HALO;  // table rows p-1, p, p+1: (evx, c1)
         const double evx = tb[8], c1m = tb[1], c1p = tb[17];
 
-        double v[BB][7];
-#pragma unroll
-        for (int b = 0; b < BB; ++b)
-#pragma unroll
-            for (int d = 0; d < 7; ++d) v[b][d] = c[b * TW + d - 3];
-        double r0[BB + 6];  // vy-offset-0 values at vx offsets -3 .. BB+2
+        // the vx line at the thread's vy: offsets -3 .. BB+2 (the cells' own
+        // values included); then the vy lines in groups of four cells.  Per
+        // cell the arithmetic and its order are those of the 4-cell layout,
+        // so every BB gives bitwise the same stage.
+        double r0[BB + 6];
         r0[0] = c[-3 * TW];
         r0[1] = c[-2 * TW];
         r0[2] = c[-TW];
+#pragma unroll
+        for (int b = 0; b < BB; ++b) r0[b + 3] = c[b * TW];
         r0[BB + 3] = c[BB * TW];
         r0[BB + 4] = c[(BB + 1) * TW];
         r0[BB + 5] = c[(BB + 2) * TW];
         double s0[BB], G[BB];
 #pragma unroll
-        for (int b = 0; b < BB; ++b) {
-            r0[b + 3] = v[b][3];
-            s0[b] = v[b][3];
-            G[b] = v[b][2] - v[b][4];
-        }
+        for (int b = 0; b < BB; ++b) s0[b] = r0[b + 3];
         // x-coupled correction c1 diag(x,vx): D(p) = s[vx-1] - s[vx+1] feeds cells p-1 and p+1
 #pragma unroll
         for (int b = 0; b < BB; ++b) {
@@ -240,9 +248,9 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             acc[b][2] = fma(c1m, D, acc[b][2]);
             acc[b][4] = fma(-c1p, D, acc[b][4]);
         }
+        const double avx = evx + cBvy;  // independent of vx
+        const double avx_s = avx * mhvx;
         if (inner) {
-            const double avx = evx + cBvy;  // independent of vx
-            const double avx_s = avx * mhvx;
             if (avx > 0.0) {
 #pragma unroll
                 for (int b = 0; b < BB; ++b)
@@ -253,22 +261,39 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                     acc[b][3] = fma(avx_s, w12neg(r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5], r0[b + 6]),
                                     acc[b][3]);
             }
-            if (ypos_all) {
+        }
 #pragma unroll
-                for (int b = 0; b < BB; ++b)
-                    acc[b][3] = fma(avy_s[b], w12pos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5]), acc[b][3]);
-            } else if (yneg_all) {
+        for (int h = 0; h < BB; h += 4) {
+            if (BB > 4) asm volatile("" ::: "memory");  // one group of four vy lines at a time (registers)
+            double v[4][7];
 #pragma unroll
-                for (int b = 0; b < BB; ++b)
-                    acc[b][3] = fma(avy_s[b], w12neg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]), acc[b][3]);
-            } else {
+            for (int bb = 0; bb < 4; ++bb)
 #pragma unroll
-                for (int b = 0; b < BB; ++b) {
-                    const double w = ypos[b] ? w12pos(v[b][0], v[b][1], v[b][2], v[b][3], v[b][4], v[b][5])
-                                             : w12neg(v[b][1], v[b][2], v[b][3], v[b][4], v[b][5], v[b][6]);
-                    acc[b][3] = fma(avy_s[b], w, acc[b][3]);
+                for (int d = 0; d < 7; ++d) v[bb][d] = d == 3 ? s0[h + bb] : c[(h + bb) * TW + d - 3];
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) G[h + bb] = v[bb][2] - v[bb][4];
+            if (inner) {
+                if (ypos_all) {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb)
+                        acc[h + bb][3] = fma(avy_s[h + bb], w12pos(v[bb][0], v[bb][1], v[bb][2], v[bb][3], v[bb][4],
+                                                                    v[bb][5]), acc[h + bb][3]);
+                } else if (yneg_all) {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb)
+                        acc[h + bb][3] = fma(avy_s[h + bb], w12neg(v[bb][1], v[bb][2], v[bb][3], v[bb][4], v[bb][5],
+                                                                    v[bb][6]), acc[h + bb][3]);
+                } else {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const double w = ypos[h + bb] ? w12pos(v[bb][0], v[bb][1], v[bb][2], v[bb][3], v[bb][4], v[bb][5])
+                                                      : w12neg(v[bb][1], v[bb][2], v[bb][3], v[bb][4], v[bb][5], v[bb][6]);
+                        acc[h + bb][3] = fma(avy_s[h + bb], w, acc[h + bb][3]);
+                    }
                 }
             }
+        }
+        if (inner) {
             // -c2 diag(vx,vy) = -c2 (G(vx+1) - G(vx-1)); fold of the src operand
             const double gm = c[-TW - 1] - c[-TW + 1], gp = c[BB * TW - 1] - c[BB * TW + 1];
             double gr[BB + 2];
@@ -329,7 +354,9 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
                 for (int b = 0; b < BB; ++b) pq[b * P2] = out[b];
             }
             if (P.nonfinite) {
-                const double sum = (out[0] + out[1]) + (out[2] + out[3]);
+                double sum = (out[0] + out[1]) + (out[2] + out[3]);
+#pragma unroll
+                for (int b = 4; b < BB; b += 4) sum += (out[b] + out[b + 1]) + (out[b + 2] + out[b + 3]);
                 if (!isfinite(sum)) {
 #pragma unroll
                     for (int b = 0; b < BB; ++b)
@@ -339,20 +366,43 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
             }
             if (P.partials) {
                 // reference fold tree (fields.py:28-47) over each aligned
-                // 16-wide vy chunk: transpose-reduce the 4 rows over the lanes
-                const bool o1 = tl & 1, o2 = tl & 2;
-                double w2[2];
+                // 16-wide vy chunk: transpose-reduce the BB rows over the lanes
+                // (after level k, lane bit k-1 selects the row half)
+                double w1;
+                if (BB == 8) {
+                    const bool o1 = tl & 1, o2 = tl & 2, o4 = tl & 4;
+                    double w4[4], w2[2];
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    const double keep = o1 ? out[2 * m + 1] : out[2 * m];
-                    const double send = o1 ? out[2 * m] : out[2 * m + 1];
-                    w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                    for (int m = 0; m < 4; ++m) {
+                        const double keep = o1 ? out[(2 * m + 1) % BB] : out[(2 * m) % BB];
+                        const double send = o1 ? out[(2 * m) % BB] : out[(2 * m + 1) % BB];
+                        w4[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                    }
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const double keep = o2 ? w4[2 * m + 1] : w4[2 * m];
+                        const double send = o2 ? w4[2 * m] : w4[2 * m + 1];
+                        w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                    }
+                    const double keep = o4 ? w2[1] : w2[0];
+                    const double send = o4 ? w2[0] : w2[1];
+                    w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
+                } else {
+                    const bool o1 = tl & 1, o2 = tl & 2;
+                    double w2[2];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const double keep = o1 ? out[2 * m + 1] : out[2 * m];
+                        const double send = o1 ? out[2 * m] : out[2 * m + 1];
+                        w2[m] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1));
+                    }
+                    const double keep = o2 ? w2[1] : w2[0];
+                    const double send = o2 ? w2[0] : w2[1];
+                    w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
+                    w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
                 }
-                const double keep = o2 ? w2[1] : w2[0];
-                const double send = o2 ? w2[0] : w2[1];
-                double w1 = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 2));
-                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 4));
-                w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 8));
                 if (tl < BB) *ppart = w1;  // lane tl: row tl
             }
         }
@@ -363,15 +413,21 @@ __global__ void __launch_bounds__(GEO::THREADS, GEO::MINB)
     if (PEER) peer_done_signal(P);
 }
 
-// Geometry (VPFV_R12_CFG): 1 = (32, 16) tiles, 128 threads, <=168 registers,
-// 3 CTAs per SM (default; measured best at 256^3), 0 = the same at 2 CTAs
-// per SM, 2 = (64, 16) tiles at 1 CTA per SM.
+// Geometry (VPFV_R12_CFG): 4 = (32, 16) tiles with 8 cells per thread (64
+// threads, <=256 registers), 4 CTAs per SM, 3-deep ring (default: -5 % at
+// 256^3 against 1); 1 = the same tiles with 4 cells per thread (128
+// threads, <=168 registers) at 3 CTAs per SM and a 4-deep ring (round 1's
+// default); 0 = that at 2 CTAs per SM; 2 = (64, 16) tiles at 1 CTA per SM;
+// 3 = 8 cells per thread at 3 CTAs per SM (+18 %: too few warps).
 static int geo12_cfg() {
+#ifndef VPFV_R12_CFG_DEFAULT
+#define VPFV_R12_CFG_DEFAULT 4
+#endif
     static int c = -1;
     if (c < 0) {
         const char *e = getenv("VPFV_R12_CFG");
-        c = e ? atoi(e) : 1;
-        if (c < 0 || c > 2) c = 1;
+        c = e ? atoi(e) : VPFV_R12_CFG_DEFAULT;
+        if (c < 0 || c > 4) c = VPFV_R12_CFG_DEFAULT;
     }
     return c;
 }
@@ -520,6 +576,8 @@ static int stage_1d2v_fused_impl(double *dest, const double *A, const double *B,
     const int cfg = geo12_cfg();
     if (cfg == 2 && Nvx % 64 == 0) return launch12<r12::Geo<64, 1>>(src, opp, packed_tables, P, xsegments, st);
     if (cfg == 1) return launch12<r12::Geo<32, 3>>(src, opp, packed_tables, P, xsegments, st);
+    if (cfg == 3) return launch12<r12::Geo<32, 3, 8, 4>>(src, opp, packed_tables, P, xsegments, st);
+    if (cfg == 4) return launch12<r12::Geo<32, 4, 8, 3>>(src, opp, packed_tables, P, xsegments, st);
     return launch12<r12::Geo<32, 2>>(src, opp, packed_tables, P, xsegments, st);
 }
 

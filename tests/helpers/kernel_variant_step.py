@@ -1,11 +1,12 @@
-"""Child process for test_tiled_kernel_variants_bitwise: one RK4 step's four
-fused 2D-2V stage launches (the RK4 3/8 aliasing, fused partials, non-finite
-word) on a seeded 8 x 8 x 128 x 128 state, with whatever VPFV_RB_* switches
-the parent set in the environment; writes the three buffers and the last
-partials to an .npz.  The switches are read once per process, so every
-variant runs in its own process.  Test infrastructure only.
+"""Child process for the kernel-variant tests: one RK4 step's four fused stage
+launches (the RK4 3/8 aliasing, fused partials, non-finite word) on a seeded
+state -- 2D-2V 8 x 8 x 128 x 128 or, with MODE 1d2v, 1D-2V 24 x 64 x 64 --
+with whatever VPFV_RB_* / VPFV_R12_* switches the parent set in the
+environment; writes the three buffers and the last partials to an .npz.
+The switches are read once per process, so every variant runs in its own
+process.  Test infrastructure only.
 
-    python tests/helpers/kernel_variant_step.py OUT.npz
+    python tests/helpers/kernel_variant_step.py OUT.npz [2d2v|1d2v]
 """
 import os
 import sys
@@ -20,19 +21,24 @@ from paper_2410_12155_b200.kernels import StageTables, stream_handle, wrap_flags
 from paper_2410_12155_b200.timestepping import RK4_STAGES  # noqa: E402
 
 
-def main(out):
+def main(out, mode="2d2v"):
     dev = torch.device("cuda", 0)
-    g = make_grid(2, 2, (8, 8, 128, 128), (0.0, 0.0, -6.0, -6.0), (2 * np.pi, 4 * np.pi, 6.0, 6.0),
-                  periodic=(True, True, False, False))
     sp = SpeciesConfig(q=-1.0, kappa_c=0.02, Bz=0.5)
     gen = torch.Generator(device=dev)
     gen.manual_seed(5)
+    if mode == "1d2v":
+        g = make_grid(1, 2, (24, 64, 64), (0.0, -6.0, -6.0), (2 * np.pi, 6.0, 6.0), periodic=(True, False, False))
+        cx = torch.as_tensor(g.centers(0), device=dev)
+        E = {"Ex": 0.4 * torch.sin(cx) + 0.05}
+    else:
+        g = make_grid(2, 2, (8, 8, 128, 128), (0.0, 0.0, -6.0, -6.0), (2 * np.pi, 4 * np.pi, 6.0, 6.0),
+                      periodic=(True, True, False, False))
+        cx = torch.as_tensor(g.centers(0), device=dev)
+        cy = torch.as_tensor(g.centers(1), device=dev)
+        E = {"Ex": 0.4 * torch.outer(torch.sin(cx), torch.cos(0.5 * cy)) + 0.05,
+             "Ey": 0.3 * torch.outer(torch.cos(cx), torch.sin(cy))}
     bufs = {k: 1.0 + 0.3 * torch.rand(g.padded_shape, dtype=torch.float64, device=dev, generator=gen)
             for k in ("f0", "f1", "fout")}
-    cx = torch.as_tensor(g.centers(0), device=dev)
-    cy = torch.as_tensor(g.centers(1), device=dev)
-    E = {"Ex": 0.4 * torch.outer(torch.sin(cx), torch.cos(0.5 * cy)) + 0.05,
-         "Ey": 0.3 * torch.outer(torch.cos(cx), torch.sin(cy))}
     tab = StageTables(g, sp, dev)
     stream = stream_handle(dev)
     tab.update(E, stream, packed=True)
@@ -48,4 +54,4 @@ def main(out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "2d2v")

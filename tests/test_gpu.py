@@ -647,6 +647,30 @@ def test_tiled_kernel_variants_bitwise(tmp_path):
 
 
 @pytest.mark.gpu
+def test_1d2v_kernel_geometries_bitwise(tmp_path):
+    """The 1D-2V kernel's geometries (VPFV_R12_CFG: 8 cells per thread at 4
+    CTAs/SM, the default; 4 cells per thread at 3 or 2 CTAs/SM; (64, 16)
+    tiles) keep each cell's arithmetic and its order, so an RK4 step is
+    bitwise the same under every one (buffers, partials, non-finite word)."""
+    import os
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(__file__), "helpers", "kernel_variant_step.py")
+    got = {}
+    for cfg in ("4", "1", "0", "2"):
+        out = str(tmp_path / f"cfg{cfg}.npz")
+        e = dict(os.environ, VPFV_R12_CFG=cfg)
+        subprocess.run([sys.executable, helper, out, "1d2v"], env=e, check=True, timeout=300)
+        got[cfg] = np.load(out)
+    ref = got["4"]
+    assert int(ref["nonfinite"][0]) == -1
+    for cfg, z in got.items():
+        for key in ("f0", "f1", "fout", "partials", "nonfinite"):
+            assert np.array_equal(z[key], ref[key]), (cfg, key)
+
+
+@pytest.mark.gpu
 def test_host_pipeline_equals_advance():
     """runner.HostPipeline (overlapped H2D / step / D2H of host states) gives
     bitwise the state Simulation.advance gives for each input."""
