@@ -131,6 +131,7 @@ class ClockSampler:
         self._stop = threading.Event()
         self._thread = None
         self._proc = None
+        self.power_limit_w = None
 
     def __enter__(self):
         try:
@@ -140,12 +141,21 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
             smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(h) / 1e3
+            except pynvml.NVMLError:
+                self.power_limit_w = None
+
             def poll():
                 while not self._stop.is_set():
                     try:
+                        try:
+                            pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1e3
+                        except pynvml.NVMLError:
+                            pw = None
                         self.samples.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
                                              float(smax),
-                                             int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                                             int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)), pw))
                     except pynvml.NVMLError:
                         pass
                     self._stop.wait(self.period)
@@ -170,7 +180,7 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 3:
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), None))
                 except ValueError:
                     pass
 
@@ -190,12 +200,21 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [s[0] for s in self.samples]
         reasons = set()
-        for _, _, bits in self.samples:
+        for _, _, bits, _ in self.samples:
             for b, n in REASON_BITS.items():
                 if bits & b and n != "gpu_idle":
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": sorted(reasons), "samples": len(sm)}
+            unknown = bits & ~sum(REASON_BITS)
+            if unknown:
+                reasons.add(f"unmapped_bits_{unknown:#x}")
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+               "reasons": sorted(reasons), "samples": len(sm), "sm_mhz_min": min(sm)}
+        pw = [s[3] for s in self.samples if s[3] is not None]
+        if pw:  # board power while the step runs: a kernel held at the power limit clocks below max
+            out["power_w_median"] = statistics.median(pw)
+            out["power_w_max"] = max(pw)
+            out["power_limit_w"] = self.power_limit_w
+        return out
 
 
 # ---------------------------------------------------------------------------
