@@ -633,7 +633,8 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                     out[i] = fma(P.cfold, P.src[gq + (i / BB) * P2 + (i % BB) * P3], out[i]);
             }
 #pragma unroll
-            for (int i = 0; i < NC; ++i) __stcs(dq + (i / BB) * P2 + (i % BB) * P3, out[i]);
+            for (int i = 0; i < NC; ++i)  // default L2 policy (evict-first measured 0.3-0.5 % slower)
+                dq[(i / BB) * P2 + (i % BB) * P3] = out[i];
             if (PEER && P.peer_lo && q < NG) {  // my plane q -> the low neighbour's ghost plane Nx + q
                 double *pq = P.peer_lo + gq + (long long)P.Nx * P1;
 #pragma unroll
