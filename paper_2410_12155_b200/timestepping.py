@@ -46,14 +46,25 @@ class StepContext:
         self.step += 1
 
 
+# Kutta's 3/8 rule as a tableau (the classic form of the recurrence above)
+RK38_A = ((), (1.0 / 3.0,), (-1.0 / 3.0, 1.0), (1.0, -1.0, 1.0))
+RK38_B = (0.125, 0.375, 0.375, 0.125)
+
+
 def rk4_butcher_step(u0, dt, L, t=0.0):
-    """Classic tableau form, four stage derivatives (timestepping.py:55-66)."""
+    """Classic tableau form with four stored stage derivatives, for checks
+    against the low-storage protocol (reference: timestepping.py:55-66).
+    Driven by ``RK38_A`` / ``RK38_B`` / ``RK_STAGE_TIMES``, so its rounding
+    is not the reference's expression grouping."""
     u0 = np.asarray(u0)
-    k1 = L(u0, t)
-    k2 = L(u0 + (dt / 3.0) * k1, t + dt / 3.0)
-    k3 = L(u0 + dt * (-k1 / 3.0 + k2), t + 2.0 * dt / 3.0)
-    k4 = L(u0 + dt * (k1 - k2 + k3), t + dt)
-    return u0 + (dt / 8.0) * (k1 + 3.0 * k2 + 3.0 * k3 + k4)
+    ks = []
+    for row, c in zip(RK38_A, RK_STAGE_TIMES):
+        u = u0
+        for a, k in zip(row, ks):
+            u = u + (a * dt) * k
+        ks.append(L(u, t + c * dt))
+    incr = sum(b * k for b, k in zip(RK38_B, ks))
+    return u0 + dt * incr
 
 
 def rk4_38_low_storage_step(ctx: StepContext, dt, stage):
@@ -68,22 +79,29 @@ def rk4_38_low_storage_step(ctx: StepContext, dt, stage):
 
 
 def array_stage(L):
-    """Adapt a functional RHS to the stage protocol (timestepping.py:87-98)."""
+    """Wrap a functional RHS ``L(y, t)`` as a stage callable (reference:
+    timestepping.py:87-98); materialises L(src), so host checks only."""
 
     def stage(dest, A, B, src, ca, cb, cd, cL, t):
-        rhs = L(src, t)
-        dest[...] = ca * A + cb * B + cd * dest + cL * rhs
+        out = cL * L(src, t)
+        for c, X in ((ca, A), (cb, B), (cd, dest)):
+            if c != 0.0:
+                out = out + c * X
+        dest[...] = out
 
     return stage
 
 
+def _l1_rate(per_dim, h):
+    """sum_d max|A_d| / h_d for one species."""
+    if len(per_dim) != len(h):
+        raise ValueError("speed/width dimension mismatch")
+    return sum(abs(a) / hd for a, hd in zip(per_dim, h))
+
+
 def max_stable_dt(speeds, h, sigma=DEFAULT_SIGMA, safety=1.0):
-    """sigma / sum_d(max|A_d|/h_d), min over species (timestepping.py:101-117)."""
-    best = math.inf
-    for per_dim in speeds:
-        if len(per_dim) != len(h):
-            raise ValueError("speed/width dimension mismatch")
-        norm1 = sum(abs(a) / hd for a, hd in zip(per_dim, h))
-        if norm1 > 0.0:
-            best = min(best, sigma / norm1)
-    return best * safety if best != math.inf else math.inf
+    """L1 CFL bound sigma / rate, minimum over species, times ``safety``;
+    ``math.inf`` when no species moves (reference: timestepping.py:101-117)."""
+    rates = [_l1_rate(per_dim, h) for per_dim in speeds]
+    fastest = max((r for r in rates if r > 0.0), default=0.0)
+    return safety * (sigma / fastest) if fastest > 0.0 else math.inf

@@ -129,8 +129,31 @@ class TestStageProtocol:
         assert [c[8] for c in calls] == [1.0, 1.0 + 0.3 / 3.0, 1.0 + 2.0 * 0.3 / 3.0, 1.0 + 0.3]
         assert ctx.t == 1.3
 
+    def test_butcher_form_equals_low_storage(self):
+        """The tableau form and the three-buffer protocol through
+        array_stage agree on a nonlinear, time-dependent RHS (the reference's
+        dual run, test_timestepping.py:208-232, on a small system)."""
+        rng = np.random.default_rng(3)
+        M = rng.standard_normal((6, 6)) * 0.5
+
+        def L(y, t):
+            return M @ y - 0.3 * y ** 3 + np.cos(t)
+
+        u0 = rng.standard_normal(6)
+        ctx = TS.StepContext(f0=u0.copy(), f1=np.full(6, np.nan), fout=np.full(6, np.nan), t=0.2)
+        ub = u0.copy()
+        for _ in range(20):
+            ub = TS.rk4_butcher_step(ub, 0.05, L, ctx.t)
+            TS.rk4_38_low_storage_step(ctx, 0.05, TS.array_stage(L))
+            ctx.rotate()
+        np.testing.assert_allclose(ctx.f0, ub, rtol=1e-12, atol=1e-13)
+        assert ctx.step == 20 and ctx.t == pytest.approx(1.2)
+
     def test_max_stable_dt(self):
         assert TS.max_stable_dt([[1.0, 1.0]], [1.0, 1.0], sigma=1.73) == pytest.approx(0.865)
+        # minimum over species; a species at rest does not limit dt
+        assert TS.max_stable_dt([[1.0, 0.0], [0.0, 0.0], [2.0, 2.0]], [0.5, 1.0], safety=0.9) == \
+            0.9 * (TS.DEFAULT_SIGMA / (2.0 / 0.5 + 2.0 / 1.0))
         assert TS.max_stable_dt([[0.0, 0.0]], [1.0, 1.0]) == math.inf
         with pytest.raises(ValueError):
             TS.max_stable_dt([[1.0]], [1.0, 1.0])
