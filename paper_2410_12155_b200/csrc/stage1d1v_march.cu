@@ -121,16 +121,10 @@ __global__ void __launch_bounds__(160, 1) stage_1d1v_march_kernel(const March11 
         tabs[0][k] = __ldg(P.avx + i0 + k);
         tabs[1][k] = __ldg(P.c1 + i0 + k);
     }
-#ifdef VPFV_MARCH_NOTMA
-    for (int k = tid; k < NP * 2 * (RS + P.nops * OS); k += blockDim.x) sm[k] = 0.0;
-#endif
     __syncthreads();
 
     if (warp == 4) {  // producer: pair q = ring rows 2q, 2q+1 (src segments + operand rows of interior rows)
         if (lane != 0) return;
-#ifdef VPFV_MARCH_NOTMA  // timing experiment: compute on whatever the ring holds
-        return;
-#endif
         const unsigned ring_s = tma::smem_addr(ring), opr_s = tma::smem_addr(opr);
         const unsigned src_bytes = RS * 8, op_bytes = OS * 8;
         const int nops = P.nops;
@@ -159,11 +153,7 @@ __global__ void __launch_bounds__(160, 1) stage_1d1v_march_kernel(const March11 
         return;
     }
 
-#ifdef VPFV_MARCH_NOTMA
-    auto wait_pair = [&](int) {};
-#else
     auto wait_pair = [&](int q) { tma::mbar_wait_s(full_s + (q & (NP - 1)) * 8, (q / NP) & 1); };
-#endif
     const double a_x = __ldg(P.ax + j);
     const double kx = a_x * P.mhx, mhv = P.mhv;
     const bool posx = a_x > 0.0;

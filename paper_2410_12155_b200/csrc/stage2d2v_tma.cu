@@ -363,13 +363,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     }
     const double vyv = __ldg(P.vyc + vy);
     const double ay_s = vyv * P.mhy;
-#ifdef VPFV_EXP_FORCE_SIGNS  // timing experiment only (wrong results): compile-time x/y upwind signs
-#pragma unroll
-    for (int b = 0; b < BB; ++b) xpos[b] = true;
-    const bool ypos = true;
-#else
     const bool ypos = vyv > 0.0;
-#endif
     const double cBvy = P.cB * vyv;
     double bvx_min = bvx[0], bvx_max = bvx[0];
 #pragma unroll
@@ -504,11 +498,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                 const double gp = ca[BB * TW - 1] - ca[BB * TW + 1];  // G at vx offset BB
                 const double avx = evx[a] + cBvy;                    // a_vx is independent of vx
                 const double avx_s = avx * mhvx;
-#ifdef VPFV_EXP_FORCE_AV
-                if (true) {
-#else
                 if (avx > 0.0) {
-#endif
 #pragma unroll
                     for (int b = 0; b < BB; ++b)
                         acc[a * BB + b][3] = fma(avx_s, wpos(r0[b], r0[b + 1], r0[b + 2], r0[b + 3], r0[b + 4], r0[b + 5]),
@@ -521,11 +511,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
                 }
                 // a_vy = evy - cB vx: one branch for the row when the four
                 // signs agree (always when cB == 0; fl(e + x) is monotone in x)
-#ifdef VPFV_EXP_FORCE_AV
-                if (true) {
-#else
                 if (evy[a] + bvx_min > 0.0) {
-#endif
 #pragma unroll
                     for (int b = 0; b < BB; ++b)
                         acc[a * BB + b][3] = fma((evy[a] + bvx[b]) * mhvy,
