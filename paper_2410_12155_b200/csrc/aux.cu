@@ -84,6 +84,8 @@ __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const doub
                                        double *__restrict__ tab, int nx, int ny, double qmk2,
                                        double nqmk2, double gx, double gy, double t1, double t4,
                                        double denx, double deny) {
+    pdl_trigger();  // the programmatic stage kernel after this waits before reading the tables
+    pdl_wait();     // E of the Poisson solve
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (nx + 2) * ny) return;
     const int row = t / ny, j = t - row * ny;
@@ -108,6 +110,8 @@ __global__ void tables2d_packed_kernel(const double *__restrict__ Ex, const doub
 __global__ void charge_kernel(const double *__restrict__ n, Charges q, int ns, int nphys,
                               double *__restrict__ rho) {
     __shared__ double red[32];
+    pdl_trigger();  // a programmatic successor waits before reading rho
+    pdl_wait();     // n of the moment finish
     charge_block(n, q, ns, nphys, rho, red);
 }
 
@@ -221,8 +225,8 @@ extern "C" int vpfv_tables_2d_packed(const double *Ex, const double *Ey, double 
                                      double qmk2, double nqmk2, double gx, double gy, double t1,
                                      double t4, double denx, double deny, void *stream) {
     int n = (Nx + 2) * Ny;
-    tables2d_packed_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        Ex, Ey, packed, Nx, Ny, qmk2, nqmk2, gx, gy, t1, t4, denx, deny);
+    launch_pdl(tables2d_packed_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream, Ex, Ey, packed, Nx,
+               Ny, qmk2, nqmk2, gx, gy, t1, t4, denx, deny);
     return check_launch("tables_2d_packed");
 }
 
@@ -231,7 +235,7 @@ extern "C" int vpfv_charge_density(const double *n, const double *q_host, int ns
     if (nspecies < 1 || nspecies > 8) return set_error(VPFV_EARG, "1..8 species supported");
     Charges q;
     for (int s = 0; s < 8; ++s) q.q[s] = s < nspecies ? q_host[s] : 0.0;
-    charge_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n, q, nspecies, nphys, rho);
+    launch_pdl(charge_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream, n, q, nspecies, nphys, rho);
     return check_launch("charge_density");
 }
 

@@ -18,13 +18,14 @@ __device__ __forceinline__ double ldg(const double *p) { return __ldg(p); }
 int set_error(int code, const char *msg);
 int check_launch(const char *what);
 
-// Programmatic dependent launch (the short 1D chains): a kernel launched with
-// launch_pdl may start while its predecessor in the stream drains; it runs
-// its independent prologue, then pdl_wait() before touching anything the
-// predecessor wrote.  pdl_trigger() lets the successor start launching --
-// only in kernels whose successor is always PDL-aware (the 1D field kernel,
-// followed by the stage kernels): measured, a stage kernel that triggered
-// let the ordinary moment launch after it read a half-written f.
+// Programmatic dependent launch (the 1D chains; the 2D field chain moment
+// finish -> charge -> FFT passes -> tables -> 2D-2V stage kernel): a kernel
+// launched with launch_pdl may start while its predecessor in the stream
+// drains; it runs its independent prologue, then pdl_wait() before touching
+// anything the predecessor wrote.  pdl_trigger() lets the successor start
+// launching -- only in kernels whose successors wait first (the field chain
+// links): measured, a stage kernel that triggered let the ordinary moment
+// launch after it read a half-written f, so no stage kernel triggers.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

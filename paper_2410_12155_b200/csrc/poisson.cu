@@ -385,6 +385,8 @@ __global__ void __launch_bounds__(256) field1d_conv_kernel(double *__restrict__ 
 __global__ void rows_fwd_kernel(const double *__restrict__ rho, double2 *__restrict__ C, int nx,
                                 int ny, const double2 *__restrict__ twy, int pow2, int logn) {
     extern __shared__ double2 sm2[];
+    pdl_trigger();  // the column pass waits before reading C
+    pdl_wait();     // rho
     double2 *a = sm2, *tmp = sm2 + ny;
     const int i = blockIdx.x;
     for (int m = threadIdx.x; m < ny; m += blockDim.x)
@@ -401,6 +403,8 @@ __global__ void cols_kernel(const double2 *__restrict__ C, double2 *__restrict__
                             const double *__restrict__ ky, const double *__restrict__ kxd,
                             const double *__restrict__ kyd, int nout, int pow2, int logn) {
     extern __shared__ double2 sm2[];
+    pdl_trigger();  // the inverse row pass waits before reading D
+    pdl_wait();     // C of the forward row pass
     double2 *a = sm2, *tmp = sm2 + nx, *ph = sm2 + 2 * nx;
     const int j = blockIdx.x;
     const long long plane = (long long)nx * ny;
@@ -437,6 +441,8 @@ __global__ void rows_inv_kernel(const double2 *__restrict__ D, double *__restric
                                 double *__restrict__ Ey, double *__restrict__ phi, int nx, int ny,
                                 const double2 *__restrict__ twy, int nout, int pow2, int logn) {
     extern __shared__ double2 sm2[];
+    pdl_trigger();  // the tables kernel waits before reading E
+    pdl_wait();     // D of the column pass
     double2 *a = sm2, *tmp = sm2 + ny;
     const int i = blockIdx.x;
     const long long plane = (long long)nx * ny;
@@ -608,10 +614,13 @@ extern "C" int vpfv_poisson_2d(const double *rho, double *Ex, double *Ey, double
     double2 *D = C + (size_t)Nx * Ny;  // up to 3 planes follow... reuse C's plane for phi
     const int nout = phi ? 3 : 2;
     // D needs nout planes; scratch holds 1 + 3 planes when phi is requested
-    rows_fwd_kernel<<<Nx, 256, smy, s>>>(rho, C, Nx, Ny, (const double2 *)twy, ly >= 0, ly < 0 ? 0 : ly);
-    cols_kernel<<<Ny, 256, smx, s>>>(C, D, Nx, Ny, (const double2 *)twx, kx, ky, kxd, kyd, nout,
-                                     lx >= 0, lx < 0 ? 0 : lx);
-    rows_inv_kernel<<<Nx, 256, smy, s>>>(D, Ex, Ey, phi, Nx, Ny, (const double2 *)twy, nout,
-                                         ly >= 0, ly < 0 ? 0 : ly);
+    // programmatic links: each launches while its predecessor drains and
+    // waits (griddepcontrol.wait) before its first read
+    const int py = ly >= 0, lgy = ly < 0 ? 0 : ly, px = lx >= 0, lgx = lx < 0 ? 0 : lx;
+    launch_pdl(rows_fwd_kernel, dim3(Nx), dim3(256), smy, s, rho, C, Nx, Ny, (const double2 *)twy, py, lgy);
+    launch_pdl(cols_kernel, dim3(Ny), dim3(256), smx, s, (const double2 *)C, D, Nx, Ny, (const double2 *)twx, kx, ky,
+               kxd, kyd, nout, px, lgx);
+    launch_pdl(rows_inv_kernel, dim3(Nx), dim3(256), smy, s, (const double2 *)D, Ex, Ey, phi, Nx, Ny,
+               (const double2 *)twy, nout, py, lgy);
     return check_launch("poisson_2d");
 }

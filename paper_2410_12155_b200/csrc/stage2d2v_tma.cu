@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(GEO::THREADS + (WS ? 128 : 0), GEO::MINB)
     using namespace rb;
     RB_GEOMETRY(GEO);
     static_assert(WS || NOPB == 1, "double-buffered operands need the producer warpgroup");
+    pdl_wait();  // programmatic dependent of the tables kernel: nothing global before this
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     const double *opbuf = stages + NS * STAGE;
@@ -769,6 +770,8 @@ template <int NLT>
 __global__ void __launch_bounds__(1024) moment_partials_row_kernel(const double *__restrict__ part,
                                                                    double *__restrict__ n, double vol) {
     __shared__ double wsum[32];
+    pdl_trigger();  // the 2D field chain after this is programmatic (every link waits first)
+    pdl_wait();     // the stage kernel's partials
     const int p = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
     double v = fold_pow2<NLT>(part + ((size_t)p * blockDim.x + t) * NLT);
 #pragma unroll
@@ -947,13 +950,13 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
                 nv = e ? atoi(e) != 0 : VPFV_RB_NV_DEFAULT;
             }
             if (P.done)
-                stage2d2v_rb_kernel<GEO, true, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+                launch_pdl(stage2d2v_rb_kernel<GEO, true, true>, dim3(nblocks), dim3(GEO::THREADS + 128), GEO::SMEM, s, maps, P);
             else if (nv && P.Nvx == 128 && P.Nvy == 128)
-                stage2d2v_rb_kernel<GEO, false, true, 128><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+                launch_pdl(stage2d2v_rb_kernel<GEO, false, true, 128>, dim3(nblocks), dim3(GEO::THREADS + 128), GEO::SMEM, s, maps, P);
             else if (nv && P.Nvx == 64 && P.Nvy == 64)  // config 5's 2 x 64^4
-                stage2d2v_rb_kernel<GEO, false, true, 64><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+                launch_pdl(stage2d2v_rb_kernel<GEO, false, true, 64>, dim3(nblocks), dim3(GEO::THREADS + 128), GEO::SMEM, s, maps, P);
             else
-                stage2d2v_rb_kernel<GEO, false, true><<<nblocks, GEO::THREADS + 128, GEO::SMEM, s>>>(maps, P);
+                launch_pdl(stage2d2v_rb_kernel<GEO, false, true>, dim3(nblocks), dim3(GEO::THREADS + 128), GEO::SMEM, s, maps, P);
             launched = true;
         }
     }
@@ -961,9 +964,9 @@ static int launch_geo(const double *src, const double *const ops[rb::OPS_MAX], c
         if (!launched) return set_error(VPFV_EARG, "double-buffered operand geometry needs the warp-specialised kernel");
     } else if (!launched) {
         if (P.done)
-            stage2d2v_rb_kernel<GEO, true><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+            launch_pdl(stage2d2v_rb_kernel<GEO, true>, dim3(nblocks), dim3(GEO::THREADS), GEO::SMEM, s, maps, P);
         else
-            stage2d2v_rb_kernel<GEO, false><<<nblocks, GEO::THREADS, GEO::SMEM, s>>>(maps, P);
+            launch_pdl(stage2d2v_rb_kernel<GEO, false>, dim3(nblocks), dim3(GEO::THREADS), GEO::SMEM, s, maps, P);
     }
     return check_launch("stage_2d2v_tma");
 }
@@ -988,11 +991,11 @@ int launch_moment_from_partials(const double *part, double *n, int nphys, int nv
     if (nlt > 16) return set_error(VPFV_EARG, "moment partials: at most 16 vy chunks");
     if (nvx >= 32 && nvx <= 1024 && (nvx & (nvx - 1)) == 0 && (nlt & (nlt - 1)) == 0) {
         switch (nlt) {
-            case 1: moment_partials_row_kernel<1><<<nphys, nvx, 0, s>>>(part, n, vol); break;
-            case 2: moment_partials_row_kernel<2><<<nphys, nvx, 0, s>>>(part, n, vol); break;
-            case 4: moment_partials_row_kernel<4><<<nphys, nvx, 0, s>>>(part, n, vol); break;
-            case 8: moment_partials_row_kernel<8><<<nphys, nvx, 0, s>>>(part, n, vol); break;
-            default: moment_partials_row_kernel<16><<<nphys, nvx, 0, s>>>(part, n, vol); break;
+            case 1: launch_pdl(moment_partials_row_kernel<1>, dim3(nphys), dim3(nvx), 0, s, part, n, vol); break;
+            case 2: launch_pdl(moment_partials_row_kernel<2>, dim3(nphys), dim3(nvx), 0, s, part, n, vol); break;
+            case 4: launch_pdl(moment_partials_row_kernel<4>, dim3(nphys), dim3(nvx), 0, s, part, n, vol); break;
+            case 8: launch_pdl(moment_partials_row_kernel<8>, dim3(nphys), dim3(nvx), 0, s, part, n, vol); break;
+            default: launch_pdl(moment_partials_row_kernel<16>, dim3(nphys), dim3(nvx), 0, s, part, n, vol); break;
         }
         return check_launch("moment_from_partials");
     }

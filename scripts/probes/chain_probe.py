@@ -57,10 +57,4 @@ def chain():
             tab.update(E, st, packed=sim.tiled[s])
 
 
-def finish_only():
-    for _ in range(4):
-        sim.fields.moment_from_partials_only(sim.partials, stream=stream_handle(dev)) \
-            if hasattr(sim.fields, "moment_from_partials_only") else None
-
-
 print(f"{N}^4: step {step:.4f} ms; field chain x4 {graph_time(chain):.4f} ms")
