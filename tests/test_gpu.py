@@ -647,6 +647,32 @@ def test_tiled_kernel_variants_bitwise(tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("problem,n", [("landau2d", 32), ("ep2d2v", 16), ("landau1d", 128), ("twostream", 512),
+                                       ("bimax1d2v", 32)])
+def test_programmatic_launches_bitwise_stream_order(tmp_path, problem, n):
+    """Graph-replayed steps with the programmatic launches (the 1D field
+    chain, the 2D moment finish -> charge -> FFT -> tables -> stage chain)
+    equal the same steps in plain stream order (VPFV_PDL=0), bitwise: every
+    programmatic kernel waits for its predecessor before touching its data.
+    One process per mode (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(__file__), "helpers", "sim_steps.py")
+    got = {}
+    for mode in ("1", "0"):
+        out = str(tmp_path / f"pdl{mode}.npz")
+        e = dict(os.environ)
+        e["VPFV_PDL"] = mode
+        subprocess.run([sys.executable, helper, out, problem, str(n), "6"], env=e, check=True, timeout=300)
+        got[mode] = np.load(out)
+    for key in got["1"].files:
+        assert np.all(np.isfinite(got["1"][key]))
+        assert np.array_equal(got["1"][key], got["0"][key]), (problem, key)
+
+
+@pytest.mark.gpu
 def test_1d2v_kernel_geometries_bitwise(tmp_path):
     """The 1D-2V kernel's geometries (VPFV_R12_CFG: 8 cells per thread at 4
     CTAs/SM, the default; 4 cells per thread at 3 or 2 CTAs/SM; (64, 16)
