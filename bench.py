@@ -132,6 +132,20 @@ class ClockSampler:
         self._thread = None
         self._proc = None
         self.power_limit_w = None
+        self._viol0 = None
+        self.violations_ms = None
+
+    def _violations(self, pynvml, h):
+        """Cumulative time (ns) the driver held clocks down for power / thermal
+        reasons: NVML violation counters, which a sparse reason sample can miss."""
+        out = {}
+        for name, pol in (("power", pynvml.NVML_PERF_POLICY_POWER), ("thermal", pynvml.NVML_PERF_POLICY_THERMAL),
+                          ("reliability", pynvml.NVML_PERF_POLICY_RELIABILITY)):
+            try:
+                out[name] = int(pynvml.nvmlDeviceGetViolationStatus(h, pol).violationTime)
+            except pynvml.NVMLError:
+                pass
+        return out
 
     def __enter__(self):
         try:
@@ -145,6 +159,8 @@ class ClockSampler:
                 self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(h) / 1e3
             except pynvml.NVMLError:
                 self.power_limit_w = None
+            self._nvml, self._h = pynvml, h
+            self._viol0 = self._violations(pynvml, h)
 
             def poll():
                 while not self._stop.is_set():
@@ -186,6 +202,9 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         self._stop.set()
+        if self._viol0 is not None:
+            v1 = self._violations(self._nvml, self._h)
+            self.violations_ms = {k: (v1[k] - self._viol0[k]) / 1e6 for k in v1 if k in self._viol0}
         if self._proc is not None:
             self._proc.terminate()
             try:
@@ -209,6 +228,12 @@ class ClockSampler:
                 reasons.add(f"unmapped_bits_{unknown:#x}")
         out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
                "reasons": sorted(reasons), "samples": len(sm), "sm_mhz_min": min(sm)}
+        if self.violations_ms is not None:
+            # time the driver spent holding clocks down while the region ran
+            out["violation_ms"] = {k: round(v, 3) for k, v in self.violations_ms.items()}
+            if self.violations_ms.get("power", 0.0) > 0.0:
+                reasons.add("sw_power_cap")
+            out["reasons"] = sorted(reasons)
         pw = [s[3] for s in self.samples if s[3] is not None]
         if pw:  # board power while the step runs: a kernel held at the power limit clocks below max
             out["power_w_median"] = statistics.median(pw)
