@@ -139,8 +139,36 @@ __global__ void box_copy_kernel(double *__restrict__ dst, const double *__restri
     }
 }
 
+// rows of a unit-stride innermost dim: one warp per row, the row index split
+// once per warp (the host pipeline's interior pack/unpack of whole states)
+__global__ void box_rows_kernel(double *__restrict__ dst, const double *__restrict__ src, Box b, long long rows) {
+    const int lane = threadIdx.x & 31, L = b.ndim - 1, n = b.ext[L];
+    const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5,
+                    nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long w = w0; w < rows; w += nw) {
+        long long r = w, doff = b.dorig[L], soff = b.sorig[L];
+        for (int k = L - 1; k >= 0; --k) {
+            const long long c = r % b.ext[k];
+            r /= b.ext[k];
+            doff += (c + b.dorig[k]) * b.ds[k];
+            soff += (c + b.sorig[k]) * b.ss[k];
+        }
+        const double *s = src + soff;
+        double *d = dst + doff;
+        for (int i = lane; i < n; i += 32) d[i] = __ldcs(s + i);
+    }
+}
+
 static int launch_box(double *dst, const double *src, const Box &b, cudaStream_t s) {
     if (b.total <= 0) return VPFV_OK;
+    const int L = b.ndim - 1;
+    if (b.ds[L] == 1 && b.ss[L] == 1 && b.ext[L] >= 32 && dst != src) {
+        const long long rows = b.total / b.ext[L];
+        long long blocks = (rows + 7) / 8;
+        if (blocks > 148 * 64) blocks = 148 * 64;
+        box_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, b, rows);
+        return check_launch("box_copy");
+    }
     long long blocks = (b.total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     box_copy_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, b);

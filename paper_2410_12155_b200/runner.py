@@ -19,6 +19,7 @@ epilogue flag, read back once per step, with the reference's rollback.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 
@@ -412,7 +413,7 @@ class HostPipeline:
     """Advance host-resident states through the device, one RK4 step each,
     with the copies overlapped: while state k steps on the compute stream,
     state k+1 is uploaded on one copy stream and the result of step k-1 is
-    downloaded on another (double-buffered device input and output).
+    downloaded on another.
 
     This is the host-buffer entry of the library: the reference's stage and
     step functions take host (numpy) arrays, so every call moves the state
@@ -422,13 +423,27 @@ class HostPipeline:
     once, never by the kernels) or periodic images read by modular index, so
     only interiors cross PCIe.  There is no divergence rollback here -- the
     per-stage non-finite flags of the last step remain in ``sim.nonfinite``.
+
+    The copy streams move contiguous device staging buffers only (pure DMA,
+    double-buffered); the interior unpack into the padded input and the pack
+    of the padded result are ``vpfv_box_copy`` launches on the compute stream
+    around the step.  (Copying straight into / out of the strided interior
+    views makes torch run a gather/scatter kernel on the copy stream, which
+    waits for SMs behind the one-CTA-per-SM stage kernels and stalls the link
+    (``staging=False`` keeps that path for comparison).)
     """
 
-    def __init__(self, sim: Simulation):
+    def __init__(self, sim: Simulation, staging: bool = True):
         self.sim = sim
+        self.staging = staging
         dev = sim.device
-        self.din = [[a.clone() for a in sim.ctx.f0] for _ in range(2)]   # ghosts included:
-        self.dout = [[a.clone() for a in sim.ctx.f0] for _ in range(2)]  # kernels write interiors only
+        nb = 1 if staging else 2
+        self.din = [[a.clone() for a in sim.ctx.f0] for _ in range(nb)]   # ghosts included:
+        self.dout = [[a.clone() for a in sim.ctx.f0] for _ in range(nb)]  # kernels write interiors only
+        if staging:
+            mk_st = lambda: [[torch.empty(tuple(g.N), dtype=torch.float64, device=dev)  # noqa: E731
+                              for g in sim.grids] for _ in range(2)]
+            self.sin, self.sout = mk_st(), mk_st()
         self.h2d = torch.cuda.Stream(dev)
         self.d2h = torch.cuda.Stream(dev)
         mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
@@ -449,9 +464,54 @@ class HostPipeline:
         sim, main = self.sim, torch.cuda.current_stream(self.sim.device)
         saved = (sim.ctx.f0, sim.ctx.fout)
         try:
-            self._run(sim, main, host_in, host_out, dt, steps)
+            (self._run_staged if self.staging else self._run)(sim, main, host_in, host_out, dt, steps)
         finally:  # the simulation's own state buffers, not the pipeline's double buffers
             sim.ctx.f0, sim.ctx.fout = saved
+
+    @staticmethod
+    def _interior_copy(dst, src, g, pack, stream):
+        """Interior of the padded ``src`` -> contiguous ``dst`` (pack) or the
+        reverse (unpack), one ``vpfv_box_copy`` launch on ``stream``."""
+        D = len(g.N)
+        pad, flat = [sl.start for sl in g.interior_slices()], [0] * D
+        so, do = (pad, flat) if pack else (flat, pad)
+        _lib.call("vpfv_box_copy", dst.data_ptr(), _lib.ll_array(dst.stride()), _lib.int_array(do),
+                  src.data_ptr(), _lib.ll_array(src.stride()), _lib.int_array(so), D,
+                  _lib.int_array(g.N), ctypes.c_void_p(stream.cuda_stream))
+
+    def _run_staged(self, sim, main, host_in, host_out, dt, steps):
+        din, dout = self.din[0], self.dout[0]
+        with torch.cuda.stream(self.h2d):
+            for d, h in zip(self.sin[0], host_in(0)):
+                d.copy_(h, non_blocking=True)
+            self.in_ready[0].record()
+        for k in range(steps):
+            b = k & 1
+            if k + 1 < steps:  # prefetch the next state once step k-1 has unpacked its staging buffer
+                if k >= 1:
+                    self.h2d.wait_event(self.step_done[1 - b])
+                with torch.cuda.stream(self.h2d):
+                    for d, h in zip(self.sin[1 - b], host_in(k + 1)):
+                        d.copy_(h, non_blocking=True)
+                    self.in_ready[1 - b].record()
+            main.wait_event(self.in_ready[b])
+            for d, s, g in zip(din, self.sin[b], sim.grids):
+                self._interior_copy(d, s, g, False, main)
+            sim.ctx.f0, sim.ctx.fout = din, dout
+            sim.launch_step(dt)
+            if k >= 2:
+                main.wait_event(self.out_done[b])  # sout[b] drained by the download of step k-2
+            for d, s, g in zip(self.sout[b], dout, sim.grids):
+                self._interior_copy(d, s, g, True, main)
+            self.step_done[b].record(main)
+            self.d2h.wait_event(self.step_done[b])
+            with torch.cuda.stream(self.d2h):
+                for h, d in zip(host_out(k), self.sout[b]):
+                    h.copy_(d, non_blocking=True)
+                self.out_done[b].record()
+        self.d2h.synchronize()
+        self.h2d.synchronize()
+        main.synchronize()
 
     def _run(self, sim, main, host_in, host_out, dt, steps):
         with torch.cuda.stream(self.h2d):

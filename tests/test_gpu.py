@@ -897,24 +897,32 @@ def test_manufactured_fourth_order_2d2v_on_device():
 
 
 @pytest.mark.gpu
-def test_host_pipeline_equals_advance():
+@pytest.mark.parametrize("staging", [True, False])
+@pytest.mark.parametrize("maker", ["landau2d", "landau1d", "weibel", "ep"])
+def test_host_pipeline_equals_advance(maker, staging):
     """runner.HostPipeline (overlapped H2D / step / D2H of host states) gives
-    bitwise the state Simulation.advance gives for each input."""
-    setup = P.make_problem(P.landau_spec(), 32, 32)
+    bitwise the state Simulation.advance gives for each input, through the
+    contiguous staging buffers (interior pack/unpack by vpfv_box_copy on the
+    compute stream) and through the strided-view copies."""
+    setup = {"landau2d": lambda: P.make_problem(P.landau_spec(), 32, 32),
+             "landau1d": lambda: P.make_landau_1d(P.landau_spec(alpha=0.01), 32, 64),
+             "weibel": lambda: P.make_problem(P.ProblemSpec("weibel"), 16, 32),
+             "ep": lambda: P.make_electron_proton_2d2v(16, 32)}[maker]()
     sim = R.Simulation(setup)
     dt = 0.9 * sim.max_dt()
     sim.fixed_dt = dt
-    pipe = R.HostPipeline(sim)
-    base = pipe.host_state()[0]
-    inputs = [[(base * (1.0 + 0.01 * k)).pin_memory()] for k in range(4)]
-    outs = [[torch.empty_like(base).pin_memory()] for _ in range(4)]
-    pipe.run(lambda k: inputs[k], lambda k: outs[k], dt, 4)
-    inner = (slice(3, -3),) * 4
-    for k in range(4):
+    pipe = R.HostPipeline(sim, staging=staging)
+    base = pipe.host_state()
+    inputs = [[(h * (1.0 + 0.01 * k)).pin_memory() for h in base] for k in range(5)]
+    outs = [[torch.empty_like(h).pin_memory() for h in base] for _ in range(5)]
+    pipe.run(lambda k: inputs[k], lambda k: outs[k], dt, 5)
+    for k in range(5):
         ref = R.Simulation(setup, dt=dt)
-        ref.ctx.f0[0][inner].copy_(inputs[k][0])
+        for f, g, h in zip(ref.ctx.f0, ref.grids, inputs[k]):
+            f[g.interior_slices()].copy_(h)
         ref.advance(dt)
-        assert torch.equal(ref.ctx.f0[0][inner].cpu(), outs[k][0]), k
+        for f, g, o in zip(ref.ctx.f0, ref.grids, outs[k]):
+            assert torch.equal(f[g.interior_slices()].cpu(), o), k
 
 
 @pytest.mark.gpu
