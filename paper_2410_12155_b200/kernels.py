@@ -200,6 +200,7 @@ class _HostStager:
 
     CHUNK_BYTES = 64 << 20
     THREADS = 8
+    NBUF = 2
 
     def __init__(self, device, plane_shape):
         from concurrent.futures import ThreadPoolExecutor
@@ -209,9 +210,9 @@ class _HostStager:
         self.plane = int(np.prod(plane_shape))
         self.nplanes = max(1, self.CHUNK_BYTES // (8 * self.plane))
         self.bufs = [torch.empty(self.nplanes * self.plane, dtype=torch.float64, pin_memory=True)
-                     for _ in range(2)]
+                     for _ in range(self.NBUF)]
         self.views = [b.numpy().reshape((self.nplanes,) + self.plane_shape) for b in self.bufs]
-        self.events = [torch.cuda.Event() for _ in range(2)]
+        self.events = [torch.cuda.Event() for _ in range(self.NBUF)]
         self.stream = torch.cuda.Stream(device)
         self.pool = ThreadPoolExecutor(self.THREADS)
 
@@ -232,7 +233,7 @@ class _HostStager:
         k = 0
         for a in range(p0, p1, self.nplanes):
             b = min(p1, a + self.nplanes)
-            j = k & 1
+            j = k % self.NBUF
             self.events[j].synchronize()  # the transfer that last used this chunk is done
             view = self.views[j][:b - a]
             if inner is None:
@@ -253,18 +254,19 @@ class _HostStager:
 
         def issue(k):
             a, b = chunks[k]
-            j = k & 1
+            j = k % self.NBUF
             with torch.cuda.stream(self.stream):
                 self.bufs[j][:(b - a) * self.plane].view((b - a,) + self.plane_shape).copy_(dev[a:b], non_blocking=True)
                 self.events[j].record(self.stream)
 
-        for k in range(min(2, len(chunks))):
+        nb = self.NBUF
+        for k in range(min(nb, len(chunks))):
             issue(k)
         for k, (a, b) in enumerate(chunks):
-            self.events[k & 1].synchronize()
-            self._copy(host[(slice(a, b),) + inner], self.views[k & 1][:b - a][(slice(None),) + inner])
-            if k + 2 < len(chunks):  # chunk k's buffer is free again
-                issue(k + 2)
+            self.events[k % nb].synchronize()
+            self._copy(host[(slice(a, b),) + inner], self.views[k % nb][:b - a][(slice(None),) + inner])
+            if k + nb < len(chunks):  # chunk k's buffer is free again
+                issue(k + nb)
 
 
 class _DropIn:
