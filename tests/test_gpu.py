@@ -1286,3 +1286,37 @@ def test_device_initial_conditions_bitwise_host(build):
         assert np.array_equal(x, y)
     for x, y in zip(a._host_state(), b._host_state()):  # ghosts too (frozen slabs captured from the device)
         assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,ext", [((7, 9, 40), (5, 6, 33)), ((4, 6, 11, 134), (2, 3, 7, 128)),
+                                       ((5, 70), (3, 64)), ((6, 5, 20), (4, 3, 17)), ((300,), (257,))])
+def test_box_copy_matches_slicing(shape, ext):
+    """vpfv_box_copy (the warp-per-row kernel for unit-stride rows of >= 32
+    cells, the element kernel otherwise) equals torch slicing, both ways
+    between a padded array and a contiguous box, leaving the rest untouched."""
+    gen = torch.Generator().manual_seed(len(shape) * 131 + ext[-1])
+    src = torch.rand(shape, generator=gen, dtype=torch.float64).cuda()
+    so = [(n - e) // 2 for n, e in zip(shape, ext)]
+    box = torch.full(ext, -1.0, dtype=torch.float64, device="cuda")
+    st = ctypes_stream()
+    _lib.call("vpfv_box_copy", box.data_ptr(), _lib.ll_array(box.stride()), _lib.int_array([0] * len(ext)),
+              src.data_ptr(), _lib.ll_array(src.stride()), _lib.int_array(so), len(ext), _lib.int_array(ext), st)
+    sl = tuple(slice(o, o + e) for o, e in zip(so, ext))
+    torch.cuda.synchronize()
+    assert torch.equal(box, src[sl])
+    dst = torch.zeros(shape, dtype=torch.float64, device="cuda")
+    do = [n - e for n, e in zip(shape, ext)]
+    _lib.call("vpfv_box_copy", dst.data_ptr(), _lib.ll_array(dst.stride()), _lib.int_array(do),
+              box.data_ptr(), _lib.ll_array(box.stride()), _lib.int_array([0] * len(ext)), len(ext),
+              _lib.int_array(ext), st)
+    torch.cuda.synchronize()
+    want = torch.zeros_like(dst)
+    want[tuple(slice(o, o + e) for o, e in zip(do, ext))] = src[sl]
+    assert torch.equal(dst, want)
+
+
+def ctypes_stream():
+    import ctypes
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
