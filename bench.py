@@ -572,7 +572,8 @@ def e2e_measure(sim, dt, steps, device, cells):
             "how": "per step: H2D of the input state (interior; ghosts are frozen or periodic images) from "
                    "pinned host memory, the graph-replayed RK4 step, D2H of the new state; "
                    "runner.HostPipeline overlaps the upload of step k+1 and the download of step k-1 with "
-                   "step k (wall clock, host-synchronised at the end)"}
+                   "step k (copy streams on contiguous device staging buffers, interior unpack/pack by "
+                   "vpfv_box_copy on the compute stream; wall clock, host-synchronised at the end)"}
 
 
 def e2e_dropin_measure(setup, f0, E, dt, device, cells, steps=1):
